@@ -1,0 +1,446 @@
+#!/usr/bin/env python
+"""Benchmark of the lbwind time step on B200 (BASELINE.json metric:
+"MLUP/s (D3Q27 cumulant fp64 + ALM) at 1/2/4/8 B200; % of HBM roofline").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--arithmetic exact|fast] [--config c2|c1|c3]
+
+Workload (BASELINE.json configs[1], "C2"): 256x128x128 D3Q27 cumulant fp64,
+velocity inflow / zero-gradient outflow in x, periodic y/z, one rotating
+three-bladed actuator-line rotor (6 points per blade, r = 0.48 m, 96 rad/s,
+symmetric polar) in a uniform 8 m/s inflow, 32 cells per diameter, Mach
+0.05, nu 0.1732 -> omega 1.7857.  Synthetic data: the rotor and polar are
+generated here (no files), the state starts from the uniform-wind product
+equilibrium.  With N > 1 the run is weak-scaled: (256 N)x128x128 on N
+GPUs, one x-slab of 256 planes per GPU, the same single rotor.
+
+A step = actuator kinematics + sampling + blade forces + Roma spreading +
+fused pull-stream-collide sweep over every cell (sim.py:264-300).  value:
+device time (CUDA events on the domain stream, max over ranks) of K steps
+with the state resident in HBM.  e2e: the same K steps through the public
+Simulation.step() API with each step's kinematics copied host->device and
+its blade loads (the thrust/power time series) read back device->host,
+wall-clock, synchronised.  The state (2 x 0.9 GB) exceeds the 126 MB L2, so
+no flush is needed between steps.
+
+--impl reference times the reference algorithm on the host cores: the
+bit-exact C restatement in oracle/ (OpenMP, all host threads) on the same
+config; rank 0 only.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ROTOR = """
+name: hawt
+components:
+  - name: tower
+    position: [0.0, 0.0, 0.0]
+  - name: nacelle
+    parent: tower
+    position: [0.0, 0.0, 0.8]
+  - name: hub
+    parent: nacelle
+    position: [-0.05, 0.0, 0.0]
+    rotation: {axis: [1.0, 0.0, 0.0], rate_rad_per_s: 96.0}
+  - name: blade1
+    parent: hub
+    discretization: {type: line, points: 6, r_end: 0.48, chord: 0.08, twist_deg: 8.0,
+                     polar: sym}
+  - name: blade2
+    parent: hub
+    orientation: {axis: [1.0, 0.0, 0.0], angle_deg: 120.0}
+    discretization: {type: line, points: 6, r_end: 0.48, chord: 0.08, twist_deg: 8.0,
+                     polar: sym}
+  - name: blade3
+    parent: hub
+    orientation: {axis: [1.0, 0.0, 0.0], angle_deg: 240.0}
+    discretization: {type: line, points: 6, r_end: 0.48, chord: 0.08, twist_deg: 8.0,
+                     polar: sym}
+"""
+
+BYTES_PER_LUP = 2 * 27 * 8     # algorithmic bytes of the fused sweep (fp64)
+METRIC = "MLUP/s (D3Q27 cumulant fp64 + ALM)"
+
+
+def polar_csv():
+    a = np.arange(-180.0, 181.0, 15.0)
+    t = np.deg2rad(a)
+    rows = ["alpha_deg,cl,cd"] + [
+        f"{float(x)!r},{float(0.9 * np.sin(2 * s))!r},{float(0.08 + 0.3 * (1 - np.cos(2 * s)))!r}"
+        for x, s in zip(a, t)]
+    return "\n".join(rows) + "\n"
+
+
+def workload(name, n_gpus):
+    """(raw config dict, description) of the benchmark workload."""
+    if name == "c1":
+        raw = {"domain": {"cells": [64 * n_gpus, 64, 64]},
+               "fluid": {"kinematic_viscosity": 0.1353, "wind": [0.0, 0.0, 0.0],
+                         "reference_velocity": 1.0},
+               "resolution": {"mach": 0.02}, "run": {"collision": {"operator": "cumulant"}}}
+        return raw, f"C1 TGV {64 * n_gpus}x64x64 periodic cumulant fp64, no turbine"
+    side = {"c2": (256, 128, 128), "c3": (256, 256, 256)}[name]
+    cells = [side[0] * n_gpus, side[1], side[2]]
+    pos = [2.0, 2.0, 1.2] if name == "c2" else [2.0, 4.0, 3.2]
+    raw = {"domain": {"cells": cells, "periodicity": [False, True, True]},
+           "fluid": {"kinematic_viscosity": 0.1732, "wind": [8.0, 0.0, 0.0]},
+           "resolution": {"cells_per_diameter": 32, "reference_diameter": 1.0, "mach": 0.05},
+           "run": {"boundary": "velocity_inflow_outflow", "collision": {"operator": "cumulant"}},
+           "turbines": [{"file": "rotor.yaml", "position": pos}],
+           "polars": [{"id": "sym", "file": "sym.csv"}]}
+    desc = (f"{'C2' if name == 'c2' else 'C3'} {cells[0]}x{cells[1]}x{cells[2]} cumulant fp64, "
+            "inflow/outflow x, one 3-blade ALM rotor (18 points)")
+    return raw, desc
+
+
+def make_config(name, n_gpus, arithmetic, tmpdir):
+    from paper_2402_13171_b200 import parse_config
+    with open(os.path.join(tmpdir, "rotor.yaml"), "w") as fh:
+        fh.write(ROTOR)
+    with open(os.path.join(tmpdir, "sym.csv"), "w") as fh:
+        fh.write(polar_csv())
+    raw, desc = workload(name, n_gpus)
+    raw.setdefault("run", {})["arithmetic"] = arithmetic
+    return parse_config(raw, base_dir=tmpdir), desc
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
+                stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 7:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    smax = float(parts[1])
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[3:7]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# --------------------------------------------------------------- our arm
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    from paper_2402_13171_b200 import Simulation, _lib
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    tmp = tempfile.TemporaryDirectory()
+    cfg, desc = make_config(args.config, world, args.arithmetic, tmp.name)
+    if world > 1:
+        from paper_2402_13171_b200 import parallel
+        sim = parallel.SlabSimulation(cfg, rank=rank, nranks=world, device=local_rank)
+    else:
+        sim = Simulation(cfg, device=local_rank)
+    cells_total = int(np.prod(cfg.cells))
+    cells_local = int(np.prod(sim.fields[0].size))
+    lib = _lib.load()
+    stream_ptr = _lib.ctypes.c_void_p()
+    _lib.check(lib.lbw_domain_stream(sim._domain, _lib.ctypes.byref(stream_ptr)))
+    stream = torch.cuda.ExternalStream(stream_ptr.value, device=torch.device("cuda", local_rank))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        sim.step()
+    sim.synchronize()
+
+    # ---- device-timed region (value)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    _lib.check(lib.lbw_domain_sweep_timing(sim._domain, 1))
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.kernel_launches()
+    with ClockSampler(local_rank) as clocks:
+        start.record(stream)
+        for _ in range(args.steps):
+            sim.step()
+        stop.record(stream)
+        sim.synchronize()
+    launches = _lib.kernel_launches() - launches0
+    torch.cuda.synchronize()
+    barrier()
+    ms = start.elapsed_time(stop)
+    sweep_ms = _lib.ctypes.c_double()
+    sweep_n = _lib.ctypes.c_int64()
+    _lib.check(lib.lbw_domain_sweep_time(sim._domain, _lib.ctypes.byref(sweep_ms),
+                                         _lib.ctypes.byref(sweep_n)))
+    _lib.check(lib.lbw_domain_sweep_timing(sim._domain, 0))
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = cells_total * args.steps / (ms / 1e3) / 1e6
+    sweep_avg_ms = sweep_ms.value / max(1, sweep_n.value)
+
+    # ---- end to end through the public API (host copies in the loop)
+    P = len(sim.points)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    loads = []
+    for _ in range(args.steps):
+        sim.step()
+        if P:
+            loads.append(sim._alm_results()[2].sum(axis=0))
+    sim.synchronize()
+    t_e2e = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+    e2e = cells_total * args.steps / t_e2e / 1e6
+
+    peaks = _measured_peaks()
+    achieved = BYTES_PER_LUP * cells_local / (sweep_avg_ms / 1e3) / 1e9
+    out = None
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 2), "unit": "MLUP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "cells": list(cfg.cells),
+                       "cells_per_gpu": cells_local, "actuator_points": P,
+                       "arithmetic": cfg.arithmetic, "parallelism": f"x-slab x{world}",
+                       "l2": "state (2 x 27 x 8 B x cells) far larger than the 126 MB L2; "
+                             "no flush needed"},
+            "e2e": {"value": round(e2e, 2), "unit": "MLUP/s",
+                    "h2d_bytes_per_step": P * 15 * 8,
+                    "d2h_bytes_per_step": P * 3 * 8 + 8},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1),
+                         "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(achieved / peaks["hbm_gbs"], 4),
+                         "traffic": _ncu_traffic(args.config, cells_local),
+                         "kernel": "lbw::k_sweep<cumulant,pull> (fused stream-collide)",
+                         "bytes_per_lup": BYTES_PER_LUP,
+                         "sweep_ms": round(sweep_avg_ms, 4),
+                         "sweep_share_of_step": round(sweep_avg_ms / (ms / args.steps), 4),
+                         "peak_source": peaks["source"],
+                         "lup_ceiling_mlups": round(peaks["hbm_gbs"] * 1e3 / BYTES_PER_LUP, 1)},
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+        }
+    sim.close()
+    tmp.cleanup()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_budget)
+    if dist is not None:
+        dist.destroy_process_group()
+    return out
+
+
+def _measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    except (OSError, KeyError, ValueError):
+        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md 6.65 TB/s)"}
+
+
+def _ncu_traffic(config, cells_local):
+    """dram bytes per sweep launch from the committed ncu capture, scaled to
+    this launch's cell count (profiles/ncu_sweep.json), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_sweep.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return round(float(d["dram_bytes_per_lup"]) * cells_local)
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+# ------------------------------------------------------------ CPU legs
+
+def _oracle_run(cfg, steps, sim_host):
+    """Time `steps` reference-algorithm steps (oracle/) of cfg on the host."""
+    from oracle import oracle as orc
+    from tests.scenarios import oracle_for
+    ref = oracle_for(sim_host)
+    kins = []
+    for _ in range(steps + 1):
+        sim_host.refresh_points()
+        kins.append(sim_host._kin.copy())
+        for topo in cfg.topologies:
+            topo.advance(cfg.units.dt)
+    ref.step(kins[0] if ref.points else None)      # untimed warm step
+    t0 = time.perf_counter()
+    for n in range(steps):
+        ref.step(kins[n + 1] if ref.points else None)
+    return time.perf_counter() - t0
+
+
+class _HostOnlySim:
+    """The host half of Simulation (kinematics, parameters) without a GPU,
+    used to drive the oracle with identical actuator kinematics."""
+
+    def __init__(self, cfg):
+        from paper_2402_13171_b200.halo import BoundarySpec
+        from paper_2402_13171_b200.sim import Simulation, SlabGrid
+        from paper_2402_13171_b200.turbine import LineSpec
+        self.cfg, self.units = cfg, cfg.units
+        self.grid = SlabGrid(cfg.cells, cfg.periodicity, 1, 0)
+        self.boundary = BoundarySpec(cfg.boundary_kind, cfg.units.velocity_to_lattice(
+            np.asarray(cfg.wind, dtype=np.float64)))
+        self.points, self._line_groups = [], []
+        gid = 0
+        for topo in cfg.topologies:
+            for comp in topo.components:
+                spec = comp.discretization
+                if isinstance(spec, LineSpec):
+                    for pi in range(spec.n_points):
+                        pid = spec.polar[pi]
+                        self.points.append(type("P", (), dict(
+                            chord=spec.chord[pi], element_length=spec.element_length[pi],
+                            twist=spec.twist[pi],
+                            polar=cfg.polars.get(pid) if pid is not None else None))())
+                    self._line_groups.append((comp, spec, slice(gid, gid + spec.n_points)))
+                    gid += spec.n_points
+        self._kin = np.zeros((gid, 15))
+        self._pos_m = np.zeros((gid, 3))
+        self.refresh_points = Simulation.refresh_points.__get__(self)
+
+
+def cpu_baseline(args, budget_s=20.0):
+    """Reference algorithm (C oracle, OpenMP over every host thread) on the
+    same workload; steps sized to ~budget_s of CPU time."""
+    from oracle import oracle as orc
+    orc.build()
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    tmp = tempfile.TemporaryDirectory()
+    cfg, desc = make_config(args.config, 1, "exact", tmp.name)
+    host = _HostOnlySim(cfg)
+    t1 = _oracle_run(cfg, 1, host)
+    steps = int(max(1, min(50, budget_s / max(t1, 1e-3))))
+    cfg, desc = make_config(args.config, 1, "exact", tmp.name)
+    host = _HostOnlySim(cfg)
+    t = _oracle_run(cfg, steps, host)
+    cells = int(np.prod(cfg.cells))
+    tmp.cleanup()
+    return {"value": round(cells * steps / t / 1e6, 3), "unit": "MLUP/s", "cores": cores,
+            "kind": "port",
+            "sample": f"{steps} full steps of {desc} (after 1 warm step), C oracle "
+                      f"(-O2 -ffp-contract=off, OpenMP {cores} threads), {t:.1f} s"}
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return None
+    cb = cpu_baseline(args, budget_s=args.cpu_budget)
+    tmp = tempfile.TemporaryDirectory()
+    cfg, desc = make_config(args.config, 1, "exact", tmp.name)
+    tmp.cleanup()
+    # time exactly K steps (after W warm-ups) so the arm is comparable
+    from oracle import oracle as orc  # noqa: F401
+    tmp = tempfile.TemporaryDirectory()
+    cfg, desc = make_config(args.config, 1, "exact", tmp.name)
+    host = _HostOnlySim(cfg)
+    t = _oracle_run(cfg, args.steps, host)
+    tmp.cleanup()
+    cells = int(np.prod(cfg.cells))
+    value = cells * args.steps / t / 1e6
+    cb["value"] = round(value, 3)
+    cb["sample"] = f"{args.steps} full steps of {desc}, C oracle, {cb['cores']} threads"
+    return {"metric": METRIC, "value": round(value, 3), "unit": "MLUP/s", "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * t / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "cells": list(cfg.cells), "parallelism": "host threads"},
+            "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": round(value, 3), "unit": "MLUP/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=("c1", "c2", "c3"), default="c2")
+    ap.add_argument("--arithmetic", choices=("exact", "fast"), default="fast")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        world = max(world, 1)
+    if args.impl == "reference":
+        out = run_reference(args, rank)
+    else:
+        out = run_ours(args, rank, world, local_rank)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

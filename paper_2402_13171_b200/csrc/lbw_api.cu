@@ -1,0 +1,610 @@
+// lbw_api.cu — C ABI of liblbw.so: host-array kernel entry points and the
+// device-resident domain (one x-slab on one GPU).  See include/lbw.h.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "lbw_domain.h"
+
+namespace lbw {
+
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_err = msg; }
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+namespace {
+
+Relax make_relax(double omega, double w3, double w4, double w5, double w6, double dt) {
+    Relax r;
+    r.omega = omega;
+    r.w3 = w3;
+    r.w4 = w4;
+    r.w5 = w5;
+    r.w6 = w6;
+    r.dt = dt;
+    return r;
+}
+
+// RAII device scratch for the host-array entry points
+struct DevBuf {
+    void* p = nullptr;
+    cudaError_t alloc(size_t n) { return n ? cudaMalloc(&p, n) : cudaSuccess; }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+int collide_batch(int op, double* f2, const double* F2, double* macro2, int64_t n, Relax r,
+                  int mode) {
+    LBW_REQ(n >= 0, "n must be >= 0");
+    LBW_REQ(mode == LBW_MODE_EXACT || mode == LBW_MODE_FAST, "unknown mode");
+    if (n == 0) return LBW_OK;
+    LBW_REQ(f2 && F2 && macro2, "null array");
+    DevBuf df, dF, dm;
+    LBW_CK(df.alloc(n * 27 * sizeof(double)));
+    LBW_CK(dF.alloc(n * 3 * sizeof(double)));
+    LBW_CK(dm.alloc(n * 4 * sizeof(double)));
+    LBW_CK(cudaMemcpy(df.p, f2, n * 27 * sizeof(double), cudaMemcpyHostToDevice));
+    LBW_CK(cudaMemcpy(dF.p, F2, n * 3 * sizeof(double), cudaMemcpyHostToDevice));
+    if (mode == LBW_MODE_EXACT)
+        LBW_CK(launch_batch_exact(op, df.as<double>(), dF.as<double>(), dm.as<double>(), n, r, 0));
+    else
+        LBW_CK(launch_batch_fast(op, df.as<double>(), dF.as<double>(), dm.as<double>(), n, r, 0));
+    LBW_CK(cudaMemcpy(f2, df.p, n * 27 * sizeof(double), cudaMemcpyDeviceToHost));
+    LBW_CK(cudaMemcpy(macro2, dm.p, n * 4 * sizeof(double), cudaMemcpyDeviceToHost));
+    return LBW_OK;
+}
+
+int collide_block(int op, double* f, const double* force, double* macro, int64_t nx, int64_t ny,
+                  int64_t nz, Relax r, int mode) {
+    LBW_REQ(nx >= 1 && ny >= 1 && nz >= 1, "block size must be positive");
+    LBW_REQ(mode == LBW_MODE_EXACT || mode == LBW_MODE_FAST, "unknown mode");
+    LBW_REQ(f && force && macro, "null array");
+    const int64_t cells = (nx + 2) * (ny + 2) * (nz + 2);
+    DevBuf df, dF, dm;
+    LBW_CK(df.alloc(cells * 27 * sizeof(double)));
+    LBW_CK(dF.alloc(cells * 3 * sizeof(double)));
+    LBW_CK(dm.alloc(cells * 4 * sizeof(double)));
+    LBW_CK(cudaMemcpy(df.p, f, cells * 27 * sizeof(double), cudaMemcpyHostToDevice));
+    LBW_CK(cudaMemcpy(dF.p, force, cells * 3 * sizeof(double), cudaMemcpyHostToDevice));
+    LBW_CK(cudaMemcpy(dm.p, macro, cells * 4 * sizeof(double), cudaMemcpyHostToDevice));
+    if (mode == LBW_MODE_EXACT)
+        LBW_CK(launch_block_collide_exact(op, df.as<double>(), dF.as<double>(), dm.as<double>(), nx,
+                                          ny, nz, r, 0));
+    else
+        LBW_CK(launch_block_collide_fast(op, df.as<double>(), dF.as<double>(), dm.as<double>(), nx,
+                                         ny, nz, r, 0));
+    LBW_CK(cudaMemcpy(f, df.p, cells * 27 * sizeof(double), cudaMemcpyDeviceToHost));
+    LBW_CK(cudaMemcpy(macro, dm.p, cells * 4 * sizeof(double), cudaMemcpyDeviceToHost));
+    return LBW_OK;
+}
+
+}  // namespace
+
+int ensure_stage(lbw_domain* d, size_t bytes) {
+    if (d->stage_bytes >= bytes) return LBW_OK;
+    if (d->stage) {
+        LBW_CK(cudaStreamSynchronize(d->stream));
+        cudaFree(d->stage);
+        d->bytes -= (int64_t)d->stage_bytes;
+        d->stage = nullptr;
+        d->stage_bytes = 0;
+    }
+    if (cudaMalloc(&d->stage, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("cannot allocate transfer staging buffer");
+        return LBW_ENOMEM;
+    }
+    d->stage_bytes = bytes;
+    d->bytes += (int64_t)bytes;
+    return LBW_OK;
+}
+
+}  // namespace lbw
+
+using namespace lbw;
+
+// ============================================================== C entry points
+extern "C" {
+
+int lbw_abi_version(void) { return LBW_ABI_VERSION; }
+const char* lbw_last_error(void) { return g_err.c_str(); }
+int lbw_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+int64_t lbw_kernel_launches(void) { return g_launches.load(); }
+
+int lbw_collide_cumulant_batch(double* f2, const double* F2, double* macro2, int64_t n,
+                               double omega, double w3, double w4, double w5, double w6,
+                               double dt, int mode) {
+    return collide_batch(1, f2, F2, macro2, n, make_relax(omega, w3, w4, w5, w6, dt), mode);
+}
+int lbw_collide_bgk_batch(double* f2, const double* F2, double* macro2, int64_t n, double omega,
+                          double dt, int mode) {
+    return collide_batch(0, f2, F2, macro2, n, make_relax(omega, 1, 1, 1, 1, dt), mode);
+}
+int lbw_collide_cumulant_block(double* f, const double* force, double* macro, int64_t nx,
+                               int64_t ny, int64_t nz, double omega, double w3, double w4,
+                               double w5, double w6, double dt, int mode) {
+    return collide_block(1, f, force, macro, nx, ny, nz, make_relax(omega, w3, w4, w5, w6, dt),
+                         mode);
+}
+int lbw_collide_bgk_block(double* f, const double* force, double* macro, int64_t nx, int64_t ny,
+                          int64_t nz, double omega, double dt, int mode) {
+    return collide_block(0, f, force, macro, nx, ny, nz, make_relax(omega, 1, 1, 1, 1, dt), mode);
+}
+int lbw_moments_block(const double* f, const double* force, double* macro, int64_t nx,
+                      int64_t ny, int64_t nz, double dt) {
+    LBW_REQ(nx >= 1 && ny >= 1 && nz >= 1, "block size must be positive");
+    LBW_REQ(f && force && macro, "null array");
+    const int64_t cells = (nx + 2) * (ny + 2) * (nz + 2);
+    DevBuf df, dF, dm;
+    LBW_CK(df.alloc(cells * 27 * sizeof(double)));
+    LBW_CK(dF.alloc(cells * 3 * sizeof(double)));
+    LBW_CK(dm.alloc(cells * 4 * sizeof(double)));
+    LBW_CK(cudaMemcpy(df.p, f, cells * 27 * sizeof(double), cudaMemcpyHostToDevice));
+    LBW_CK(cudaMemcpy(dF.p, force, cells * 3 * sizeof(double), cudaMemcpyHostToDevice));
+    LBW_CK(cudaMemcpy(dm.p, macro, cells * 4 * sizeof(double), cudaMemcpyHostToDevice));
+    LBW_CK(launch_block_moments(df.as<double>(), dF.as<double>(), dm.as<double>(), nx, ny, nz, dt, 0));
+    LBW_CK(cudaMemcpy(macro, dm.p, cells * 4 * sizeof(double), cudaMemcpyDeviceToHost));
+    return LBW_OK;
+}
+int lbw_stream_pull_block(const double* fsrc, double* fdst, int64_t nx, int64_t ny, int64_t nz) {
+    LBW_REQ(nx >= 1 && ny >= 1 && nz >= 1, "block size must be positive");
+    LBW_REQ(fsrc && fdst, "null array");
+    const int64_t cells = (nx + 2) * (ny + 2) * (nz + 2);
+    DevBuf ds, dd;
+    LBW_CK(ds.alloc(cells * 27 * sizeof(double)));
+    LBW_CK(dd.alloc(cells * 27 * sizeof(double)));
+    LBW_CK(cudaMemcpy(ds.p, fsrc, cells * 27 * sizeof(double), cudaMemcpyHostToDevice));
+    LBW_CK(cudaMemcpy(dd.p, fdst, cells * 27 * sizeof(double), cudaMemcpyHostToDevice));
+    LBW_CK(launch_block_stream(ds.as<double>(), dd.as<double>(), nx, ny, nz, 0));
+    LBW_CK(cudaMemcpy(fdst, dd.p, cells * 27 * sizeof(double), cudaMemcpyDeviceToHost));
+    return LBW_OK;
+}
+
+// ------------------------------------------------------------------ domain
+
+static int alloc_dev(lbw_domain* d, void** p, size_t bytes) {
+    if (cudaMalloc(p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("device allocation of " + std::to_string(bytes) + " bytes failed");
+        return LBW_ENOMEM;
+    }
+    d->bytes += (int64_t)bytes;
+    return LBW_OK;
+}
+
+static void free_domain(lbw_domain* d) {
+    if (!d) return;
+    cudaSetDevice(d->device);
+    if (d->stream) cudaStreamSynchronize(d->stream);
+    alm_destroy(d);
+    for (void* p : d->peer_mapped) cudaIpcCloseMemHandle(p);
+    for (double*& b : d->buf)
+        if (b) cudaFree(b);
+    if (d->user.row_slot) cudaFree(d->user.row_slot);
+    if (d->user.pool) cudaFree(d->user.pool);
+    if (d->macro_dense) cudaFree(d->macro_dense);
+    if (d->d_nan) cudaFree(d->d_nan);
+    if (d->h_nan) cudaFreeHost(d->h_nan);
+    if (d->nan_event) cudaEventDestroy(d->nan_event);
+    if (d->stage) cudaFree(d->stage);
+    for (cudaEvent_t ev : d->ev_pool) cudaEventDestroy(ev);
+    if (d->stream) cudaStreamDestroy(d->stream);
+    delete d;
+}
+
+static void polynomial_equilibrium(double rho, const double u[3], double out[27]) {
+    // equilibrium_pdf (collision.py:54-67) for a single (rho, u); the host
+    // wrapper passes the numpy-evaluated values instead when it has them.
+    const double usq = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+    for (int i = 0; i < 27; ++i) {
+        const double cu = cx_of(i) * u[0] + cy_of(i) * u[1] + cz_of(i) * u[2];
+        out[i] = w_of(i) * rho * (1.0 + 3.0 * cu + 4.5 * cu * cu - 1.5 * usq);
+    }
+}
+
+int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out) {
+    LBW_REQ(desc && out, "null argument");
+    *out = nullptr;
+    const lbw_domain_desc& s = *desc;
+    for (int k = 0; k < 3; ++k) LBW_REQ(s.cells[k] >= 1, "cells must be positive");
+    LBW_REQ(s.cells[1] <= (1 << 30) && s.cells[2] <= (1 << 30), "y/z extent too large");
+    LBW_REQ(s.slab_nx >= 1 && s.slab_x0 >= 0 && s.slab_x0 + s.slab_nx <= s.cells[0],
+            "slab outside the x extent");
+    LBW_REQ(s.op == LBW_OP_BGK || s.op == LBW_OP_CUMULANT, "unknown collision operator");
+    LBW_REQ(s.mode == LBW_MODE_EXACT || s.mode == LBW_MODE_FAST, "unknown arithmetic mode");
+    LBW_REQ(s.boundary == LBW_BC_PERIODIC || s.boundary == LBW_BC_INFLOW_OUTFLOW,
+            "unknown boundary kind");
+    LBW_REQ(s.omega > 0.0 && s.omega < 2.0, "omega must lie in (0, 2)");
+    for (int k = 0; k < 4; ++k)
+        LBW_REQ(s.rates[k] >= 0.0 && s.rates[k] <= 2.0, "higher-order rate outside [0, 2]");
+    LBW_REQ(!(s.boundary == LBW_BC_INFLOW_OUTFLOW && s.periodic[0]),
+            "velocity_inflow_outflow needs a non-periodic x axis");
+    LBW_REQ(s.nranks >= 1 && s.rank >= 0 && s.rank < s.nranks, "bad rank/nranks");
+    const int ndev = lbw_device_count();
+    LBW_REQ(ndev > 0, "no CUDA device visible");
+    LBW_REQ(s.device >= 0 && s.device < ndev, "device ordinal out of range");
+
+    lbw_domain* d = new lbw_domain();
+    d->desc = s;
+    d->device = s.device;
+    if (cudaSetDevice(d->device) != cudaSuccess) {
+        cudaGetLastError();
+        delete d;
+        set_error("cudaSetDevice failed");
+        return LBW_ECUDA;
+    }
+    Geom& g = d->g;
+    g.nxl = (int32_t)s.slab_nx;
+    g.ny = (int32_t)s.cells[1];
+    g.nz = (int32_t)s.cells[2];
+    g.zp = (g.nz + 15) / 16 * 16;   // 128-byte aligned z rows
+    if (g.nz < 16) g.zp = g.nz;
+    g.dir_stride = (int64_t)g.ny * g.zp;
+    g.plane_stride = 27 * g.dir_stride;
+    g.x0 = s.slab_x0;
+    g.nxg = s.cells[0];
+    g.per_y = s.periodic[1] ? 1 : 0;
+    g.per_z = s.periodic[2] ? 1 : 0;
+    const bool at_lo = s.slab_x0 == 0, at_hi = s.slab_x0 + s.slab_nx == s.cells[0];
+    auto face = [&](bool lo) -> int {
+        const bool edge = lo ? at_lo : at_hi;
+        if (!edge) return XS_GHOST;
+        if (s.boundary == LBW_BC_INFLOW_OUTFLOW) return lo ? XS_CONST : XS_CLAMP;
+        if (!s.periodic[0]) return XS_ZERO;
+        return s.nranks == 1 ? XS_WRAP : XS_GHOST;
+    };
+    g.lo_src = face(true);
+    g.hi_src = face(false);
+    if (s.feq_in_given)
+        for (int i = 0; i < 27; ++i) g.feq_in[i] = s.feq_in[i];
+    else
+        polynomial_equilibrium(1.0, s.u_in, g.feq_in);
+    d->relax = make_relax(s.omega, s.rates[0], s.rates[1], s.rates[2], s.rates[3], 1.0);
+
+    int rc = LBW_OK;
+    const size_t buf_bytes = (size_t)(g.nxl + 2) * g.plane_stride * sizeof(double);
+    if (cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        free_domain(d);
+        set_error("cudaStreamCreate failed");
+        return LBW_ECUDA;
+    }
+    for (int b = 0; b < 2 && rc == LBW_OK; ++b) rc = alloc_dev(d, (void**)&d->buf[b], buf_bytes);
+    if (rc == LBW_OK) rc = alloc_dev(d, (void**)&d->d_nan, sizeof(unsigned long long));
+    if (rc != LBW_OK) {
+        free_domain(d);
+        return rc;
+    }
+    if (cudaMallocHost(&d->h_nan, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d->nan_event, cudaEventDisableTiming) != cudaSuccess ||
+        cudaMemsetAsync(d->buf[0], 0, buf_bytes, d->stream) != cudaSuccess ||
+        cudaMemsetAsync(d->buf[1], 0, buf_bytes, d->stream) != cudaSuccess ||
+        cudaMemsetAsync(d->d_nan, 0xff, sizeof(unsigned long long), d->stream) != cudaSuccess ||
+        cudaStreamSynchronize(d->stream) != cudaSuccess) {
+        cudaGetLastError();
+        free_domain(d);
+        set_error("domain initialisation failed");
+        return LBW_ECUDA;
+    }
+    *d->h_nan = ~0ull;
+    // inflow ghost data is constant: feq_in lives in the kernel parameters.
+    *out = d;
+    return LBW_OK;
+}
+
+int lbw_domain_destroy(lbw_domain* d) {
+    free_domain(d);
+    return LBW_OK;
+}
+
+int lbw_domain_stream(lbw_domain* d, void** s) {
+    LBW_REQ(d && s, "null argument");
+    *s = (void*)d->stream;
+    return LBW_OK;
+}
+
+int64_t lbw_domain_device_bytes(lbw_domain* d) { return d ? d->bytes : 0; }
+
+static size_t interior_cells(const lbw_domain* d) {
+    return (size_t)d->g.nxl * d->g.ny * d->g.nz;
+}
+
+// The ALM samples a macro field defined by buffers the caller is about to
+// overwrite: freeze it into the dense snapshot first.
+static int freeze_macro_if(lbw_domain* d, bool touches_buf_cur, bool touches_user_force) {
+    if (!alm_active(d) || d->msrc.kind != MS_GATHER) return LBW_OK;
+    const bool hit = (touches_buf_cur && d->msrc.buf == d->cur) ||
+                     (touches_user_force && d->msrc.fv.row_slot == d->user.row_slot &&
+                      d->user.row_slot != nullptr);
+    if (!hit) return LBW_OK;
+    if (!d->macro_dense) {
+        int rc = alloc_dev(d, (void**)&d->macro_dense, interior_cells(d) * 4 * sizeof(double));
+        if (rc) return rc;
+    }
+    LBW_CK(launch_moments_soa(d->msrc.pull, d->buf[d->msrc.buf], d->g, d->msrc.fv, 1.0,
+                              d->macro_dense, d->stream));
+    d->msrc.kind = MS_DENSE;
+    return LBW_OK;
+}
+
+int lbw_domain_upload_pdf(lbw_domain* d, const double* f_aos) {
+    LBW_REQ(d && f_aos, "null argument");
+    LBW_CK(cudaSetDevice(d->device));
+    const size_t bytes = interior_cells(d) * 27 * sizeof(double);
+    int rc = ensure_stage(d, bytes);
+    if (rc) return rc;
+    rc = freeze_macro_if(d, true, false);
+    if (rc) return rc;
+    LBW_CK(cudaMemcpyAsync(d->stage, f_aos, bytes, cudaMemcpyHostToDevice, d->stream));
+    LBW_CK(launch_aos_to_soa(d->stage, d->buf[d->cur], d->g, d->stream));
+    LBW_CK(cudaStreamSynchronize(d->stream));
+    d->state_pre = true;
+    return LBW_OK;
+}
+
+int lbw_domain_upload_pdf_device(lbw_domain* d, const double* f_aos_dev) {
+    LBW_REQ(d && f_aos_dev, "null argument");
+    LBW_CK(cudaSetDevice(d->device));
+    int rc = freeze_macro_if(d, true, false);
+    if (rc) return rc;
+    LBW_CK(launch_aos_to_soa(f_aos_dev, d->buf[d->cur], d->g, d->stream));
+    d->state_pre = true;
+    return LBW_OK;
+}
+
+int lbw_domain_download_pdf(lbw_domain* d, double* f_aos) {
+    LBW_REQ(d && f_aos, "null argument");
+    LBW_CK(cudaSetDevice(d->device));
+    const size_t bytes = interior_cells(d) * 27 * sizeof(double);
+    int rc = ensure_stage(d, bytes);
+    if (rc) return rc;
+    // post-collision state -> the reference's post-stream state (stream only)
+    LBW_CK(launch_gather_aos(!d->state_pre, d->buf[d->cur], d->g, d->stage, d->stream));
+    LBW_CK(cudaMemcpyAsync(f_aos, d->stage, bytes, cudaMemcpyDeviceToHost, d->stream));
+    LBW_CK(cudaStreamSynchronize(d->stream));
+    return LBW_OK;
+}
+
+int lbw_domain_set_force(lbw_domain* d, const double* force_aos) {
+    LBW_REQ(d, "null domain");
+    LBW_CK(cudaSetDevice(d->device));
+    int rc = freeze_macro_if(d, false, true);
+    if (rc) return rc;
+    if (!force_aos) {
+        d->user_active = false;
+        d->shown_fv = ForceView{nullptr, nullptr};
+        return LBW_OK;
+    }
+    const int64_t rows = (int64_t)d->g.nxl * d->g.ny;
+    if (!d->user.row_slot) {
+        rc = alloc_dev(d, (void**)&d->user.row_slot, rows * sizeof(int32_t));
+        if (!rc) rc = alloc_dev(d, (void**)&d->user.pool, rows * 3 * d->g.zp * sizeof(double));
+        if (rc) return rc;
+        d->user.cap = rows;
+    }
+    const size_t bytes = interior_cells(d) * 3 * sizeof(double);
+    rc = ensure_stage(d, bytes);
+    if (rc) return rc;
+    LBW_CK(cudaMemcpyAsync(d->stage, force_aos, bytes, cudaMemcpyHostToDevice, d->stream));
+    LBW_CK(launch_force_from_aos(d->stage, d->g, d->user.row_slot, d->user.pool, d->stream));
+    LBW_CK(cudaStreamSynchronize(d->stream));
+    d->user_active = true;
+    d->shown_fv = d->user.view();
+    return LBW_OK;
+}
+
+int lbw_domain_download_force(lbw_domain* d, double* force_aos) {
+    LBW_REQ(d && force_aos, "null argument");
+    LBW_CK(cudaSetDevice(d->device));
+    const size_t bytes = interior_cells(d) * 3 * sizeof(double);
+    int rc = ensure_stage(d, bytes);
+    if (rc) return rc;
+    LBW_CK(launch_force_to_aos(d->shown_fv, d->g, d->stage, d->stream));
+    LBW_CK(cudaMemcpyAsync(force_aos, d->stage, bytes, cudaMemcpyDeviceToHost, d->stream));
+    LBW_CK(cudaStreamSynchronize(d->stream));
+    return LBW_OK;
+}
+
+int lbw_domain_set_macro(lbw_domain* d, const double* macro_aos, const double* uniform4) {
+    LBW_REQ(d, "null domain");
+    LBW_CK(cudaSetDevice(d->device));
+    if (uniform4) {
+        d->msrc.kind = MS_UNIFORM;
+        for (int k = 0; k < 4; ++k) d->msrc.uniform[k] = uniform4[k];
+        return LBW_OK;
+    }
+    if (!macro_aos) return LBW_OK;
+    const size_t bytes = interior_cells(d) * 4 * sizeof(double);
+    if (!d->macro_dense) {
+        int rc = alloc_dev(d, (void**)&d->macro_dense, bytes);
+        if (rc) return rc;
+    }
+    LBW_CK(cudaMemcpyAsync(d->macro_dense, macro_aos, bytes, cudaMemcpyHostToDevice, d->stream));
+    LBW_CK(cudaStreamSynchronize(d->stream));
+    d->msrc.kind = MS_DENSE;
+    return LBW_OK;
+}
+
+int lbw_domain_download_macro(lbw_domain* d, double* macro_aos) {
+    LBW_REQ(d && macro_aos, "null argument");
+    LBW_CK(cudaSetDevice(d->device));
+    const size_t n = interior_cells(d);
+    if (d->msrc.kind == MS_UNIFORM) {
+        for (size_t c = 0; c < n; ++c)
+            for (int k = 0; k < 4; ++k) macro_aos[c * 4 + k] = d->msrc.uniform[k];
+        return LBW_OK;
+    }
+    const size_t bytes = n * 4 * sizeof(double);
+    if (d->msrc.kind == MS_DENSE) {
+        LBW_CK(cudaMemcpyAsync(macro_aos, d->macro_dense, bytes, cudaMemcpyDeviceToHost, d->stream));
+    } else {
+        int rc = ensure_stage(d, bytes);
+        if (rc) return rc;
+        LBW_CK(launch_moments_soa(d->msrc.pull, d->buf[d->msrc.buf], d->g, d->msrc.fv, 1.0,
+                                  d->stage, d->stream));
+        LBW_CK(cudaMemcpyAsync(macro_aos, d->stage, bytes, cudaMemcpyDeviceToHost, d->stream));
+    }
+    LBW_CK(cudaStreamSynchronize(d->stream));
+    return LBW_OK;
+}
+
+int lbw_domain_recompute_moments(lbw_domain* d, double* macro_aos) {
+    LBW_REQ(d, "null domain");
+    LBW_CK(cudaSetDevice(d->device));
+    const size_t bytes = interior_cells(d) * 4 * sizeof(double);
+    int rc = ensure_stage(d, bytes);
+    if (rc) return rc;
+    const ForceView fv = d->shown_fv;
+    LBW_CK(launch_moments_soa(!d->state_pre, d->buf[d->cur], d->g, fv, 1.0, d->stage, d->stream));
+    if (macro_aos)
+        LBW_CK(cudaMemcpyAsync(macro_aos, d->stage, bytes, cudaMemcpyDeviceToHost, d->stream));
+    LBW_CK(cudaStreamSynchronize(d->stream));
+    // _recompute_moments overwrites PdfField.macro (sim.py:160-165): the
+    // next actuator step samples these moments.
+    d->msrc.kind = MS_GATHER;
+    d->msrc.buf = d->cur;
+    d->msrc.pull = !d->state_pre;
+    d->msrc.fv = fv;
+    return LBW_OK;
+}
+
+int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
+    LBW_REQ(d, "null domain");
+    LBW_REQ(nsteps >= 0, "nsteps must be >= 0");
+    LBW_CK(cudaSetDevice(d->device));
+    for (int32_t s = 0; s < nsteps; ++s) {
+        ForceView fv = d->user_active ? d->user.view() : ForceView{nullptr, nullptr};
+        if (alm_active(d)) {
+            int rc = alm_before_collide(d, &fv);
+            if (rc) return rc;
+        }
+        SweepArgs a;
+        a.src = d->buf[d->cur];
+        a.dst = d->buf[1 - d->cur];
+        a.g = d->g;
+        a.fv = fv;
+        a.r = d->relax;
+        a.x_begin = 0;
+        a.x_end = d->g.nxl;
+        a.nan_key = d->d_nan;
+        a.step = d->step;
+        a.halo = d->halo[1 - d->cur];
+        const bool pull = !d->state_pre;
+        if (d->timing) {
+            while (d->ev_pool.size() < d->ev_used + 2) {
+                cudaEvent_t ev;
+                LBW_CK(cudaEventCreate(&ev));
+                d->ev_pool.push_back(ev);
+            }
+            LBW_CK(cudaEventRecord(d->ev_pool[d->ev_used], d->stream));
+        }
+        const cudaError_t e = d->desc.mode == LBW_MODE_FAST
+                                  ? launch_sweep_fast(d->desc.op, pull, a, d->stream)
+                                  : launch_sweep_exact(d->desc.op, pull, a, d->stream);
+        LBW_CK(e);
+        if (d->timing) {
+            LBW_CK(cudaEventRecord(d->ev_pool[d->ev_used + 1], d->stream));
+            d->ev_used += 2;
+        }
+        // the next step samples moments(pre-collision f, F) of this collide
+        d->msrc.kind = MS_GATHER;
+        d->msrc.buf = d->cur;
+        d->msrc.pull = pull;
+        d->msrc.fv = fv;
+        d->last_fv = fv;
+        d->shown_fv = fv;
+        d->cur = 1 - d->cur;
+        d->state_pre = false;
+        d->step += 1;
+    }
+    if (nsteps > 0) {
+        LBW_CK(cudaMemcpyAsync(d->h_nan, d->d_nan, sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, d->stream));
+        LBW_CK(cudaEventRecord(d->nan_event, d->stream));
+        d->nan_pending = true;
+    }
+    return LBW_OK;
+}
+
+int64_t lbw_domain_step_index(lbw_domain* d) { return d ? d->step : -1; }
+int lbw_domain_set_step_index(lbw_domain* d, int64_t step) {
+    LBW_REQ(d && step >= 0, "bad argument");
+    d->step = step;
+    return LBW_OK;
+}
+
+int lbw_domain_poll_nonfinite(lbw_domain* d, int wait, int64_t* step, int64_t* cell3,
+                              int32_t* field) {
+    LBW_REQ(d, "null domain");
+    LBW_CK(cudaSetDevice(d->device));
+    if (d->nan_pending) {
+        if (wait) {
+            LBW_CK(cudaEventSynchronize(d->nan_event));
+            d->nan_pending = false;
+        } else {
+            const cudaError_t q = cudaEventQuery(d->nan_event);
+            if (q == cudaSuccess) d->nan_pending = false;
+            else if (q != cudaErrorNotReady) LBW_CK(q);
+            else cudaGetLastError();
+        }
+    }
+    const unsigned long long k = *d->h_nan;
+    if (k == ~0ull) return 0;
+    const int64_t cell = (int64_t)((k >> 1) & ((1ull << 39) - 1));
+    if (step) *step = (int64_t)(k >> 40);
+    if (cell3) {
+        const int64_t ny = d->g.ny, nz = d->g.nz;
+        cell3[0] = cell / (ny * nz);
+        cell3[1] = (cell / nz) % ny;
+        cell3[2] = cell % nz;
+    }
+    if (field) *field = (k & 1ull) ? 1 : 0;
+    return 1;
+}
+
+int lbw_domain_sync(lbw_domain* d) {
+    LBW_REQ(d, "null domain");
+    LBW_CK(cudaSetDevice(d->device));
+    LBW_CK(cudaStreamSynchronize(d->stream));
+    return LBW_OK;
+}
+
+int lbw_domain_sweep_timing(lbw_domain* d, int enable) {
+    LBW_REQ(d, "null domain");
+    d->timing = enable != 0;
+    d->ev_used = 0;
+    return LBW_OK;
+}
+
+int lbw_domain_sweep_time(lbw_domain* d, double* ms_total, int64_t* launches) {
+    LBW_REQ(d && ms_total && launches, "null argument");
+    LBW_CK(cudaSetDevice(d->device));
+    LBW_CK(cudaStreamSynchronize(d->stream));
+    double total = 0.0;
+    for (size_t k = 0; k + 1 < d->ev_used; k += 2) {
+        float ms = 0.0f;
+        LBW_CK(cudaEventElapsedTime(&ms, d->ev_pool[k], d->ev_pool[k + 1]));
+        total += ms;
+    }
+    *ms_total = total;
+    *launches = (int64_t)(d->ev_used / 2);
+    return LBW_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,97 @@
+// lbw_domain.h — host-side state of one device-resident x-slab.
+#pragma once
+#include <string>
+#include <vector>
+
+#include "../../include/lbw.h"
+#include "lbw_internal.h"
+
+namespace lbw {
+
+void set_error(const std::string& msg);
+
+#define LBW_CK(call)                                                                    \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess) {                                                        \
+            ::lbw::set_error(std::string(#call) + ": " + cudaGetErrorString(e_));       \
+            return LBW_ECUDA;                                                           \
+        }                                                                               \
+    } while (0)
+
+#define LBW_REQ(cond, msg)                  \
+    do {                                    \
+        if (!(cond)) {                      \
+            ::lbw::set_error(msg);          \
+            return LBW_EINVAL;              \
+        }                                   \
+    } while (0)
+
+// A sparse force field: rows (x,y) of the slab that carry force own a slot
+// of [3][zp] doubles in the pool.
+struct ForceSet {
+    int32_t* row_slot = nullptr;   // (nxl*ny), -1 = no force
+    double* pool = nullptr;        // (cap, 3, zp)
+    int32_t* slot_row = nullptr;   // (cap) row of each used slot
+    int32_t* count = nullptr;      // device counter of used slots
+    int64_t cap = 0;
+    ForceView view() const { return ForceView{row_slot, pool}; }
+};
+
+enum MacroKind { MS_UNIFORM = 0, MS_DENSE = 1, MS_GATHER = 2 };
+struct MacroSource {
+    int kind = MS_UNIFORM;
+    double uniform[4] = {1.0, 0.0, 0.0, 0.0};
+    int buf = 0;          // MS_GATHER: population buffer
+    bool pull = false;    //            stream from it (post-collision data)
+    ForceView fv{nullptr, nullptr};
+};
+
+struct AlmState;  // lbw_alm.cu
+
+}  // namespace lbw
+
+struct lbw_domain {
+    lbw_domain_desc desc{};
+    lbw::Geom g{};
+    lbw::Relax relax{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    double* buf[2] = {nullptr, nullptr};
+    int cur = 0;             // buffer holding the current state
+    bool state_pre = true;   // buf[cur] holds pre-collision populations
+    int64_t step = 0;
+    // force
+    lbw::ForceSet user;      // dense body force set by the caller
+    bool user_active = false;
+    lbw::ForceView last_fv{nullptr, nullptr};  // force of the most recent collide
+    lbw::ForceView shown_fv{nullptr, nullptr}; // what download_force reports
+    // ALM sampling source for the next step
+    lbw::MacroSource msrc;
+    double* macro_dense = nullptr;
+    // non-finite flag
+    unsigned long long* d_nan = nullptr;
+    unsigned long long* h_nan = nullptr;
+    cudaEvent_t nan_event = nullptr;
+    bool nan_pending = false;
+    // staging for AoS transfers
+    double* stage = nullptr;
+    size_t stage_bytes = 0;
+    int64_t bytes = 0;
+    lbw::AlmState* alm = nullptr;
+    // optional sweep timing (lbw_domain_sweep_timing)
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    // multi-GPU halo targets (peer ghost planes) per buffer
+    lbw::HaloOut halo[2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    std::vector<void*> peer_mapped;
+};
+
+namespace lbw {
+// lbw_alm.cu
+int alm_before_collide(lbw_domain* d, ForceView* fv_out);
+void alm_destroy(lbw_domain* d);
+bool alm_active(const lbw_domain* d);
+int ensure_stage(lbw_domain* d, size_t bytes);
+}  // namespace lbw

@@ -1,0 +1,91 @@
+// lbw_internal.h — structures shared by the host driver and the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "lbw_cell.cuh"
+
+namespace lbw {
+
+// Source of a pulled population whose x plane lies outside the owned slab.
+enum XSource : int {
+    XS_GHOST = 0,  // ghost plane in memory, written by the neighbouring slab
+    XS_WRAP = 1,   // periodic x on one domain: the plane at the other end
+    XS_CONST = 2,  // velocity inflow: polynomial equilibrium feq_in (halo.py:151-156)
+    XS_CLAMP = 3,  // zero-gradient outflow: the adjacent interior plane (halo.py:157-160)
+    XS_ZERO = 4,   // non-periodic face without a boundary condition: never-written ghost (0)
+};
+
+// Device layout of one population buffer: planes p = 0 .. nxl+1 (p = x+1,
+// planes 0 and nxl+1 are ghosts), each plane [27][ny][zp] with z fastest.
+struct Geom {
+    int32_t nxl, ny, nz, zp;   // local x planes, y, z, z pitch
+    int64_t dir_stride;        // ny*zp
+    int64_t plane_stride;      // 27*ny*zp
+    int64_t x0, nxg;           // first global x, global x size
+    int32_t per_y, per_z;
+    int32_t lo_src, hi_src;    // XSource for x-1 at x=0 and x+1 at x=nxl-1
+    double feq_in[27];
+};
+
+__host__ __device__ inline int64_t buf_index(const Geom& g, int p, int i, int y, int z) {
+    return (int64_t)p * g.plane_stride + (int64_t)i * g.dir_stride + (int64_t)y * g.zp + z;
+}
+
+// Force density of the cells that carry one: rows (x,y) with a slot hold
+// [3][zp] doubles in the pool; every other cell has F = 0.
+struct ForceView {
+    const int32_t* row_slot;  // (nxl*ny) slot index or -1; nullptr = no force
+    const double* pool;       // [slot][3][zp]
+};
+
+struct HaloOut {
+    double* lo;  // receives dirs 0..8 of plane x=0   ([9][ny][zp]), or nullptr
+    double* hi;  // receives dirs 18..26 of plane x=nxl-1, or nullptr
+};
+
+// kernel launchers (defined in the .cu translation units)
+struct SweepArgs {
+    const double* src;
+    double* dst;
+    Geom g;
+    ForceView fv;
+    Relax r;
+    int32_t x_begin, x_end;   // local planes [x_begin, x_end)
+    unsigned long long* nan_key;
+    int64_t step;
+    HaloOut halo;
+};
+
+// exact flavour (lbw_kernels_exact.cu, -fmad=false)
+cudaError_t launch_sweep_exact(int op, bool pull, const SweepArgs& a, cudaStream_t s);
+cudaError_t launch_batch_exact(int op, double* f2, const double* F2, double* macro2, int64_t n,
+                               Relax r, cudaStream_t s);
+cudaError_t launch_block_collide_exact(int op, double* f, const double* force, double* macro,
+                                       int64_t nx, int64_t ny, int64_t nz, Relax r,
+                                       cudaStream_t s);
+// fast flavour (lbw_kernels_fast.cu)
+cudaError_t launch_sweep_fast(int op, bool pull, const SweepArgs& a, cudaStream_t s);
+cudaError_t launch_batch_fast(int op, double* f2, const double* F2, double* macro2, int64_t n,
+                              Relax r, cudaStream_t s);
+cudaError_t launch_block_collide_fast(int op, double* f, const double* force, double* macro,
+                                      int64_t nx, int64_t ny, int64_t nz, Relax r,
+                                      cudaStream_t s);
+
+// data movement / moments (lbw_kernels_exact.cu)
+cudaError_t launch_block_moments(const double* f, const double* force, double* macro, int64_t nx,
+                                 int64_t ny, int64_t nz, double dt, cudaStream_t s);
+cudaError_t launch_block_stream(const double* fsrc, double* fdst, int64_t nx, int64_t ny,
+                                int64_t nz, cudaStream_t s);
+cudaError_t launch_aos_to_soa(const double* aos, double* buf, const Geom& g, cudaStream_t s);
+cudaError_t launch_gather_aos(bool pull, const double* buf, const Geom& g, double* aos,
+                              cudaStream_t s);
+cudaError_t launch_moments_soa(bool pull, const double* buf, const Geom& g, ForceView fv,
+                               double dt, double* macro_aos, cudaStream_t s);
+cudaError_t launch_force_to_aos(ForceView fv, const Geom& g, double* aos, cudaStream_t s);
+cudaError_t launch_force_from_aos(const double* aos, const Geom& g, int32_t* row_slot,
+                                  double* pool, cudaStream_t s);
+
+void count_launch(int n = 1);
+
+}  // namespace lbw

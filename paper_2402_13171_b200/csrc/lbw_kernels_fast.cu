@@ -1,0 +1,45 @@
+// lbw_kernels_fast.cu — FMA flavour of the collide kernels (LBW_MODE_FAST).
+// Compiled with contraction enabled (default -fmad=true).
+#define LBW_FAST 1
+#include "lbw_sweep.cuh"
+
+namespace lbw {
+
+cudaError_t launch_sweep_fast(int op, bool pull, const SweepArgs& a, cudaStream_t s) {
+    const dim3 blk = sweep_block(a.g);
+    const dim3 grd((a.g.nz + blk.x - 1) / blk.x, (a.g.ny + blk.y - 1) / blk.y, a.x_end - a.x_begin);
+    if (grd.z == 0) return cudaSuccess;
+    if (op == 1) {
+        if (pull) k_sweep<1, true><<<grd, blk, 0, s>>>(a);
+        else k_sweep<1, false><<<grd, blk, 0, s>>>(a);
+    } else {
+        if (pull) k_sweep<0, true><<<grd, blk, 0, s>>>(a);
+        else k_sweep<0, false><<<grd, blk, 0, s>>>(a);
+    }
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_batch_fast(int op, double* f2, const double* F2, double* macro2, int64_t n,
+                              Relax r, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)((n + 127) / 128);
+    if (op == 1) k_batch<1><<<blocks, 128, 0, s>>>(f2, F2, macro2, n, r);
+    else k_batch<0><<<blocks, 128, 0, s>>>(f2, F2, macro2, n, r);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_block_collide_fast(int op, double* f, const double* force, double* macro,
+                                      int64_t nx, int64_t ny, int64_t nz, Relax r,
+                                      cudaStream_t s) {
+    const int64_t n = nx * ny * nz;
+    if (n == 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)((n + 127) / 128);
+    if (op == 1) k_block_collide<1><<<blocks, 128, 0, s>>>(f, force, macro, nx, ny, nz, r);
+    else k_block_collide<0><<<blocks, 128, 0, s>>>(f, force, macro, nx, ny, nz, r);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace lbw

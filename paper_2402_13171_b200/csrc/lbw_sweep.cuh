@@ -1,0 +1,199 @@
+// lbw_sweep.cuh — kernel templates shared by the exact and fast translation
+// units.  Each TU defines LBW_FAST (0/1) before including this header and
+// instantiates only its own flavour, so the exact kernels never see a
+// contracting compiler (-fmad=false is a per-TU flag).
+#pragma once
+#include "lbw_internal.h"
+
+#ifndef LBW_FAST
+#error "define LBW_FAST before including lbw_sweep.cuh"
+#endif
+
+namespace lbw {
+
+constexpr int kSweepThreads = 128;
+
+template <int OP>
+__device__ __forceinline__ Macro collide_cell(double (&f)[27], double Fx, double Fy, double Fz,
+                                              const Relax& r) {
+#if LBW_FAST
+    if constexpr (OP == 1) return cumulant_fast(f, Fx, Fy, Fz, r);
+    else return bgk_fast(f, Fx, Fy, Fz, r);
+#else
+    if constexpr (OP == 1) return cumulant_exact(f, Fx, Fy, Fz, r);
+    else return bgk_exact(f, Fx, Fy, Fz, r);
+#endif
+}
+
+// Where population i of cell (x,y,z) streams from (pull: x - c_i), with the
+// x-face rules of XSource and the y/z wrap (periodic) or zero-ghost
+// (non-periodic) rule of the reference's ghost ring (halo.py:92-160).
+struct PullSrc {
+    int64_t xoff[3];  // plane offset for cx = -1, 0, +1
+    int32_t xkind[3]; // 0 memory, 1 constant inflow, 2 zero
+    int32_t yoff[3];  // ys*zp for cy = -1, 0, +1
+    int32_t zs[3];
+    bool yok[3], zok[3];
+};
+
+__device__ __forceinline__ void x_source(const Geom& g, int x, int cx, int64_t& off, int32_t& kind) {
+    int xs = x - cx;
+    kind = 0;
+    if (xs < 0 || xs >= g.nxl) {
+        const int mode = xs < 0 ? g.lo_src : g.hi_src;
+        if (mode == XS_WRAP) xs = xs < 0 ? g.nxl - 1 : 0;
+        else if (mode == XS_CLAMP) xs = xs < 0 ? 0 : g.nxl - 1;
+        else if (mode == XS_CONST) kind = 1;
+        else if (mode == XS_ZERO) kind = 2;
+        // XS_GHOST: plane -1 / nxl are the ghost planes 0 / nxl+1
+    }
+    off = (int64_t)(xs + 1) * g.plane_stride;
+}
+
+__device__ __forceinline__ void make_pull(const Geom& g, int x, int y, int z, PullSrc& s) {
+#pragma unroll
+    for (int c = -1; c <= 1; ++c) {
+        x_source(g, x, c, s.xoff[c + 1], s.xkind[c + 1]);
+        int ys = y - c;
+        bool yok = true;
+        if (ys < 0) { if (g.per_y) ys += g.ny; else yok = false; }
+        else if (ys >= g.ny) { if (g.per_y) ys -= g.ny; else yok = false; }
+        s.yoff[c + 1] = yok ? ys * g.zp : 0;
+        s.yok[c + 1] = yok;
+        int zs = z - c;
+        bool zok = true;
+        if (zs < 0) { if (g.per_z) zs += g.nz; else zok = false; }
+        else if (zs >= g.nz) { if (g.per_z) zs -= g.nz; else zok = false; }
+        s.zs[c + 1] = zok ? zs : 0;
+        s.zok[c + 1] = zok;
+    }
+}
+
+template <bool PULL>
+__device__ __forceinline__ void load_cell(const double* __restrict__ src, const Geom& g, int x, int y,
+                                          int z, double (&f)[27]) {
+    if constexpr (!PULL) {
+        const double* p = src + buf_index(g, x + 1, 0, y, z);
+#pragma unroll
+        for (int i = 0; i < 27; ++i) f[i] = __ldg(p + (int64_t)i * g.dir_stride);
+    } else {
+        PullSrc s;
+        make_pull(g, x, y, z, s);
+#pragma unroll
+        for (int i = 0; i < 27; ++i) {
+            const int a = cx_of(i) + 1, b = cy_of(i) + 1, c = cz_of(i) + 1;
+            if (s.xkind[a] == 1) {
+                f[i] = g.feq_in[i];
+            } else if (s.xkind[a] == 2 || !s.yok[b] || !s.zok[c]) {
+                f[i] = 0.0;
+            } else {
+                f[i] = __ldg(src + s.xoff[a] + (int64_t)i * g.dir_stride + s.yoff[b] + s.zs[c]);
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void load_force(const ForceView& fv, const Geom& g, int x, int y, int z,
+                                           double& Fx, double& Fy, double& Fz) {
+    Fx = Fy = Fz = 0.0;
+    if (fv.row_slot != nullptr) {
+        const int32_t slot = fv.row_slot[(int64_t)x * g.ny + y];
+        if (slot >= 0) {
+            const double* p = fv.pool + (int64_t)slot * 3 * g.zp + z;
+            Fx = p[0];
+            Fy = p[g.zp];
+            Fz = p[2 * g.zp];
+        }
+    }
+}
+
+// Non-finite macro -> atomicMin of (step, global cell, density-ok bit)
+// (sim.py:254-262: first offending cell in C order, "density" when rho is bad).
+__device__ __forceinline__ void flag_nonfinite(unsigned long long* key, int64_t step,
+                                               int64_t cell, const Macro& m) {
+    const bool rho_ok = isfinite(m.rho);
+    if (!(rho_ok && isfinite(m.ux) && isfinite(m.uy) && isfinite(m.uz))) {
+        const unsigned long long k = ((unsigned long long)step << 40) |
+                                     ((unsigned long long)cell << 1) | (rho_ok ? 1ull : 0ull);
+        atomicMin(key, k);
+    }
+}
+
+// K1: fused pull-stream + collide (+Guo) over local planes [x_begin, x_end).
+// One thread per cell, z fastest.  PULL=false collides the stored state in
+// place position (first step after an upload of pre-collision data).
+template <int OP, bool PULL>
+__global__ void __launch_bounds__(kSweepThreads, 4) k_sweep(SweepArgs a) {
+    const Geom& g = a.g;
+    const int z = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    const int x = a.x_begin + blockIdx.z;
+    if (z >= g.nz || y >= g.ny) return;
+    double f[27];
+    load_cell<PULL>(a.src, g, x, y, z, f);
+    double Fx, Fy, Fz;
+    load_force(a.fv, g, x, y, z, Fx, Fy, Fz);
+    const Macro m = collide_cell<OP>(f, Fx, Fy, Fz, a.r);
+    flag_nonfinite(a.nan_key, a.step, ((g.x0 + x) * g.ny + y) * (int64_t)g.nz + z, m);
+    double* d = a.dst + buf_index(g, x + 1, 0, y, z);
+#pragma unroll
+    for (int i = 0; i < 27; ++i) d[(int64_t)i * g.dir_stride] = f[i];
+    if (x == 0 && a.halo.lo != nullptr) {
+        double* h = a.halo.lo + (int64_t)y * g.zp + z;
+#pragma unroll
+        for (int i = 0; i < 9; ++i) h[(int64_t)i * g.dir_stride] = f[i];
+    }
+    if (x == g.nxl - 1 && a.halo.hi != nullptr) {
+        double* h = a.halo.hi + (int64_t)y * g.zp + z;
+#pragma unroll
+        for (int i = 18; i < 27; ++i) h[(int64_t)(i - 18) * g.dir_stride] = f[i];
+    }
+}
+
+// K0: batch collide of (n,27) rows (_kernels.py:400-427)
+template <int OP>
+__global__ void __launch_bounds__(128) k_batch(double* __restrict__ f2, const double* __restrict__ F2,
+                                               double* __restrict__ macro2, int64_t n, Relax r) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    double f[27];
+#pragma unroll
+    for (int i = 0; i < 27; ++i) f[i] = f2[k * 27 + i];
+    const Macro m = collide_cell<OP>(f, F2[k * 3], F2[k * 3 + 1], F2[k * 3 + 2], r);
+#pragma unroll
+    for (int i = 0; i < 27; ++i) f2[k * 27 + i] = f[i];
+    macro2[k * 4] = m.rho;
+    macro2[k * 4 + 1] = m.ux;
+    macro2[k * 4 + 2] = m.uy;
+    macro2[k * 4 + 3] = m.uz;
+}
+
+// collide of every interior cell of a ghosted AoS block (_kernels.py:304-354)
+template <int OP>
+__global__ void __launch_bounds__(128) k_block_collide(double* __restrict__ f,
+                                                       const double* __restrict__ force,
+                                                       double* __restrict__ macro, int64_t nx,
+                                                       int64_t ny, int64_t nz, Relax r) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nx * ny * nz) return;
+    const int64_t z = t % nz + 1, y = (t / nz) % ny + 1, x = t / (nz * ny) + 1;
+    const int64_t c = (x * (ny + 2) + y) * (nz + 2) + z;
+    double fl[27];
+#pragma unroll
+    for (int i = 0; i < 27; ++i) fl[i] = f[c * 27 + i];
+    const Macro m = collide_cell<OP>(fl, force[c * 3], force[c * 3 + 1], force[c * 3 + 2], r);
+#pragma unroll
+    for (int i = 0; i < 27; ++i) f[c * 27 + i] = fl[i];
+    macro[c * 4] = m.rho;
+    macro[c * 4 + 1] = m.ux;
+    macro[c * 4 + 2] = m.uy;
+    macro[c * 4 + 3] = m.uz;
+}
+
+inline dim3 sweep_block(const Geom& g) {
+    int bz = 32;
+    while (bz < g.nz && bz < kSweepThreads) bz *= 2;
+    return dim3(bz, kSweepThreads / bz, 1);
+}
+
+}  // namespace lbw

@@ -1,0 +1,146 @@
+"""Host view of one device-resident slab (the PdfField surface of
+lbwind.fields, fields.py:22-67).
+
+The populations live on the GPU as two fp64 [x+1][27][y][z] buffers; this
+object exposes the reference's accessors on demand:
+
+    interior        (nx,ny,nz,27)  f_n, the post-stream state between steps
+    interior_force  (nx,ny,nz,3)   the force of the latest collide (or the
+                                   user-set body force)
+    interior_macro  (nx,ny,nz,4)   (rho, u) the next actuator step samples
+
+Reading downloads a fresh copy.  The returned arrays write through: any
+item assignment (``fld.interior[...] = x``, ``fld.interior_force[..., 0] =
+F``, augmented assignment) uploads the whole array back, so the
+reference's in-place idioms keep working on device state.
+"""
+
+import numpy as np
+
+from . import _lib
+from .collision import equilibrium_pdf, product_equilibrium
+
+
+class _WriteThrough(np.ndarray):
+    """ndarray whose item assignment pushes the root array to the device."""
+
+    def __array_finalize__(self, obj):
+        self._push = getattr(obj, "_push", None)
+        self._root = getattr(obj, "_root", None)
+
+    def __setitem__(self, key, value):
+        super().__setitem__(key, value)
+        if self._push is not None:
+            self._push(self._root)
+
+
+def _write_through(arr, push):
+    out = arr.view(_WriteThrough)
+    out._push = push
+    out._root = out
+    return out
+
+
+class DeviceField:
+    def __init__(self, sim, size, origin, block_id=0):
+        self._sim = sim
+        self.size = tuple(int(s) for s in size)
+        self.origin = tuple(int(o) for o in origin)
+        self.block_id = int(block_id)
+        self.dtype = np.dtype(np.float64)
+
+    # -- device handle
+    @property
+    def _d(self):
+        return self._sim._domain
+
+    def cell_count(self):
+        nx, ny, nz = self.size
+        return nx * ny * nz
+
+    # -- populations
+    def download_pdf(self):
+        out = np.empty(self.size + (27,))
+        _lib.check(_lib.load().lbw_domain_download_pdf(self._d, _lib.ptr(out)), "download")
+        return out
+
+    def upload_pdf(self, f):
+        f = np.ascontiguousarray(np.broadcast_to(np.asarray(f, dtype=np.float64),
+                                                 self.size + (27,)))
+        _lib.check(_lib.load().lbw_domain_upload_pdf(self._d, _lib.ptr(f)), "upload")
+
+    @property
+    def interior(self):
+        return _write_through(self.download_pdf(), lambda a: self.upload_pdf(np.asarray(a)))
+
+    @interior.setter
+    def interior(self, value):
+        self.upload_pdf(value)
+
+    # -- force
+    def download_force(self):
+        out = np.empty(self.size + (3,))
+        _lib.check(_lib.load().lbw_domain_download_force(self._d, _lib.ptr(out)), "force")
+        return out
+
+    def set_force(self, force):
+        if force is None:
+            _lib.check(_lib.load().lbw_domain_set_force(self._d, None), "force")
+            return
+        force = np.ascontiguousarray(np.broadcast_to(np.asarray(force, dtype=np.float64),
+                                                     self.size + (3,)))
+        _lib.check(_lib.load().lbw_domain_set_force(self._d, _lib.ptr(force)), "force")
+
+    @property
+    def interior_force(self):
+        return _write_through(self.download_force(), lambda a: self.set_force(np.asarray(a)))
+
+    @interior_force.setter
+    def interior_force(self, value):
+        self.set_force(value)
+
+    # -- macro
+    def download_macro(self):
+        out = np.empty(self.size + (4,))
+        _lib.check(_lib.load().lbw_domain_download_macro(self._d, _lib.ptr(out)), "macro")
+        return out
+
+    def set_macro(self, macro):
+        macro = np.ascontiguousarray(np.broadcast_to(np.asarray(macro, dtype=np.float64),
+                                                     self.size + (4,)))
+        _lib.check(_lib.load().lbw_domain_set_macro(self._d, _lib.ptr(macro), None), "macro")
+
+    @property
+    def interior_macro(self):
+        return _write_through(self.download_macro(), lambda a: self.set_macro(np.asarray(a)))
+
+    @interior_macro.setter
+    def interior_macro(self, value):
+        self.set_macro(value)
+
+    def initialize_equilibrium(self, rho, u, product=False):
+        """Interior populations at equilibrium of (rho, u); the sampled macro
+        becomes exactly (rho, u) and the force field is cleared
+        (fields.py:54-67).  rho scalar or (nx,ny,nz); u (3,) or (nx,ny,nz,3)."""
+        n = self.size
+        rho_arr = np.broadcast_to(np.asarray(rho, np.float64), n)
+        u_arr = np.broadcast_to(np.asarray(u, np.float64), n + (3,))
+        uniform = np.ndim(rho) == 0 and np.shape(u) == (3,)
+        if uniform:
+            # one cell's equilibrium, evaluated by the same numpy expression
+            one = (product_equilibrium if product else equilibrium_pdf)(
+                np.asarray(rho, np.float64), np.asarray(u, np.float64))
+            eq = np.broadcast_to(one, n + (27,))
+        else:
+            eq = (product_equilibrium if product else equilibrium_pdf)(rho_arr, u_arr)
+        self.set_force(None)
+        self.upload_pdf(eq)
+        lib = _lib.load()
+        if uniform:
+            u4 = np.array([float(rho), *np.asarray(u, np.float64)])
+            _lib.check(lib.lbw_domain_set_macro(self._d, None, _lib.ptr(u4)), "macro")
+        else:
+            m = np.empty(n + (4,))
+            m[..., 0] = rho_arr
+            m[..., 1:4] = u_arr
+            self.set_macro(m)

@@ -1,0 +1,393 @@
+"""Time-stepping driver on the GPU (the Simulation surface of lbwind.sim,
+/root/reference/pkg/src/lbwind/sim.py:56-400).
+
+One Simulation owns one device-resident x-slab (the whole lattice on one
+GPU, or slab ``rank`` of ``nranks`` in a multi-GPU run, see
+paper_2402_13171_b200.parallel) plus the turbine topologies.  A step keeps
+the reference's order (sim.py:5-21):
+
+  host   refresh actuator kinematics for t = n dt (vectorised, bit-identical
+         to refresh_points) and queue them (one async H2D)
+  K4     sample the previous step's macro field, blade-element forces
+  K5     zero last step's force rows, spread in ascending global id
+  K1     fused pull-stream + collide + Guo, outer boundary folded into the
+         pull, non-finite flag, edge planes pushed to the neighbour slabs
+  host   advance the topologies by dt
+
+Everything between the two host parts is queued on the domain's CUDA
+stream; the only synchronisation per step is a non-blocking poll of the
+non-finite flag.
+"""
+
+import json
+import os
+
+import numpy as np
+
+from . import _lib
+from .collision import CollisionConfig
+from .errors import ConfigError, NumericalAbort
+from .fields import DeviceField
+from .halo import BoundarySpec
+from .roofline import RunTimer, lbm_kernel_cost, lightspeed, measure_mlups, percent_table_row
+from .turbine import DiskSpec, LineSpec
+
+_EX = np.array([1.0, 0.0, 0.0])
+KIN_COLS = 15
+
+
+class BlockDescriptor:
+    def __init__(self, id, block_index, origin, size, owner=0):
+        self.id, self.block_index = id, tuple(block_index)
+        self.origin, self.size = tuple(origin), tuple(size)
+        self.owner, self.weight = owner, 1.0
+        self.neighbors = {}
+
+
+class SlabGrid:
+    """The device decomposition: x-slabs, one per GPU.  Exposes the bits of
+    lbwind.blocks.BlockGrid that callers read (blocks, global_dims,
+    periodicity, counts, owner_block_of_position)."""
+
+    def __init__(self, cells, periodicity, nranks, rank):
+        self.global_dims = tuple(int(c) for c in cells)
+        self.periodicity = tuple(bool(p) for p in periodicity)
+        self.nranks, self.rank = int(nranks), int(rank)
+        nx = self.global_dims[0]
+        self.bounds = [(r * nx) // self.nranks for r in range(self.nranks + 1)]
+        if any(self.bounds[r + 1] - self.bounds[r] < 1 for r in range(self.nranks)):
+            raise ConfigError(f"{nx} x planes cannot be split over {nranks} GPUs")
+        self.counts = (self.nranks, 1, 1)
+        self.block_dims = (self.bounds[1] - self.bounds[0],) + self.global_dims[1:]
+        x0, x1 = self.bounds[rank], self.bounds[rank + 1]
+        self.blocks = [BlockDescriptor(rank, (rank, 0, 0), (x0, 0, 0),
+                                       (x1 - x0,) + self.global_dims[1:], owner=rank)]
+
+    def __len__(self):
+        return len(self.blocks)
+
+    def owner_block_of_position(self, pos):
+        x = None
+        for k in range(3):
+            v = pos[k] % self.global_dims[k] if self.periodicity[k] else pos[k]
+            if not 0.0 <= v < self.global_dims[k]:
+                raise ConfigError(f"position component {pos[k]} outside the non-periodic domain")
+            if k == 0:
+                x = v
+        return int(np.searchsorted(self.bounds, x, side="right") - 1)
+
+
+class ActuatorPoint:
+    """One actuator point (attribute surface of lbwind.actuator.ActuatorPoint,
+    actuator.py:33-63).  Per-step state lives in the Simulation's arrays;
+    attribute reads fetch device results lazily."""
+
+    def __init__(self, sim, gid, chord=0.0, element_length=0.0, twist=0.0, polar=None,
+                 area=0.0):
+        self._sim = sim
+        self.global_id = int(gid)
+        self.chord = float(chord)
+        self.element_length = float(element_length)
+        self.twist = float(twist)
+        self.polar = polar
+        self.area = float(area)
+        self.owner_block = -1
+
+    def _k(self, a, b):
+        return self._sim._kin[self.global_id, a:b].copy()
+
+    position = property(lambda s: s._sim._pos_m[s.global_id].copy())
+    position_lat = property(lambda s: s._k(0, 3))
+    velocity = property(lambda s: s._k(3, 6))
+    e_chord = property(lambda s: s._k(6, 9))
+    e_normal = property(lambda s: s._k(9, 12))
+    e_span = property(lambda s: s._k(12, 15))
+    sampled_rho = property(lambda s: float(s._sim._alm_results()[0][s.global_id]))
+    sampled_u = property(lambda s: s._sim._alm_results()[1][s.global_id].copy())
+    blade_force = property(lambda s: s._sim._alm_results()[2][s.global_id].copy())
+    fluid_force = property(lambda s: -s._sim._alm_results()[2][s.global_id])
+
+
+class Simulation:
+    def __init__(self, cfg, rank=0, nranks=1, device=None):
+        self.cfg = cfg
+        self.units = cfg.units
+        lib = _lib.require_gpu()
+        self.grid = SlabGrid(cfg.cells, cfg.periodicity, nranks, rank)
+        desc = self.grid.blocks[0]
+        self.collision = CollisionConfig(cfg.operator, self.units.omega,
+                                         cfg.higher_order_rates).validate()
+        wind_lat = self.units.velocity_to_lattice(np.asarray(cfg.wind, dtype=np.float64))
+        self.boundary = BoundarySpec(cfg.boundary_kind, u_in_lat=wind_lat)
+        if cfg.precision != "double":
+            raise ConfigError("run.precision: the device build computes and stores fp64 "
+                              "(precision: single is not supported yet)")
+        self.device = cfg.device if device is None else int(device)
+        self._domain = self._create_domain(lib, desc, rank, nranks)
+        self.fields = [DeviceField(self, desc.size, desc.origin, desc.id)]
+        self.fields[0].initialize_equilibrium(1.0, wind_lat,
+                                              product=(cfg.operator == "cumulant"))
+        self._build_points()
+        self.timer = RunTimer(int(np.prod(cfg.cells)))
+        self.step_index = 0
+        self._macro_fresh = False
+        self._avg = {}
+        self._results = None
+        self._warned = set()
+
+    # ----------------------------------------------------------- setup
+    def _create_domain(self, lib, desc, rank, nranks):
+        cfg = self.cfg
+        d = _lib.DomainDesc()
+        for k in range(3):
+            d.cells[k] = cfg.cells[k]
+            d.periodic[k] = int(cfg.periodicity[k])
+        d.slab_x0, d.slab_nx = desc.origin[0], desc.size[0]
+        d.op = _lib.OP_CUMULANT if cfg.operator == "cumulant" else _lib.OP_BGK
+        d.mode = _lib.MODE_FAST if cfg.arithmetic == "fast" else _lib.MODE_EXACT
+        d.boundary = (_lib.BC_INFLOW_OUTFLOW if cfg.boundary_kind == "velocity_inflow_outflow"
+                      else _lib.BC_PERIODIC)
+        d.device = self.device
+        d.omega = float(self.units.omega)
+        for k in range(4):
+            d.rates[k] = float(cfg.higher_order_rates[k])
+        for k in range(3):
+            d.u_in[k] = float(self.boundary.u_in_lat[k])
+        d.rank, d.nranks = rank, nranks
+        d.feq_in_given = 1
+        feq = self.boundary.inflow_populations()
+        for i in range(27):
+            d.feq_in[i] = float(feq[i])
+        handle = _lib.ctypes.c_void_p()
+        _lib.check(lib.lbw_domain_create(_lib.ctypes.byref(d), _lib.ctypes.byref(handle)),
+                   "domain")
+        return handle
+
+    def _build_points(self):
+        """Global ids in topology -> component -> point order (sim.py:113-143)."""
+        cfg = self.cfg
+        self.points, self._line_groups, self._disk_groups = [], [], []
+        polar_ids = sorted(cfg.polars)
+        gid = 0
+        for topo in cfg.topologies:
+            for comp in topo.components:
+                spec = comp.discretization
+                if isinstance(spec, LineSpec):
+                    start = gid
+                    for pi in range(spec.n_points):
+                        pid = spec.polar[pi]
+                        self.points.append(ActuatorPoint(
+                            self, gid, spec.chord[pi], spec.element_length[pi], spec.twist[pi],
+                            cfg.polars.get(pid) if pid is not None else None))
+                        gid += 1
+                    self._line_groups.append((comp, spec, slice(start, gid)))
+                elif isinstance(spec, DiskSpec):
+                    raise ConfigError(
+                        f"component {comp.name!r}: actuator disks are not on the device path "
+                        "yet (SURVEY.md section 8 row f2)")
+        P = len(self.points)
+        self._kin = np.zeros((P, KIN_COLS))
+        self._pos_m = np.zeros((P, 3))
+        if P == 0:
+            return
+        # static point data + concatenated polar tables -> device
+        index_of = {pid: k for k, pid in enumerate(polar_ids)}
+        self._polar_list = [cfg.polars[pid] for pid in polar_ids]
+        pidx = np.full(P, -1, dtype=np.int32)
+        for p in self.points:
+            if p.polar is not None:
+                pidx[p.global_id] = index_of[p.polar.id]
+        rows = np.array([t.alpha.size for t in self._polar_list] or [0], dtype=np.int32)
+        offs = np.concatenate([[0], np.cumsum(rows)[:-1]]).astype(np.int32)
+        cat = (lambda attr: np.ascontiguousarray(np.concatenate(
+            [getattr(t, attr) for t in self._polar_list]) if self._polar_list else np.zeros(1)))
+        self._alm_static = dict(
+            chord=np.array([p.chord for p in self.points]),
+            elen=np.array([p.element_length for p in self.points]),
+            twist=np.array([p.twist for p in self.points]), pidx=pidx, rows=rows, offs=offs,
+            alpha=cat("alpha"), cl=cat("cl"), cd=cat("cd"))
+        s = self._alm_static
+        D = _lib.ctypes.POINTER(_lib.ctypes.c_double)
+        I = _lib.ctypes.POINTER(_lib.ctypes.c_int32)
+        a = _lib.AlmDesc()
+        a.n_points = P
+        a.chord = s["chord"].ctypes.data_as(D)
+        a.element_length = s["elen"].ctypes.data_as(D)
+        a.twist = s["twist"].ctypes.data_as(D)
+        a.polar_index = s["pidx"].ctypes.data_as(I)
+        a.n_polars = len(self._polar_list)
+        a.polar_offset = s["offs"].ctypes.data_as(I)
+        a.polar_rows = s["rows"].ctypes.data_as(I)
+        a.polar_alpha = s["alpha"].ctypes.data_as(D)
+        a.polar_cl = s["cl"].ctypes.data_as(D)
+        a.polar_cd = s["cd"].ctypes.data_as(D)
+        a.velocity_scale = self.units.velocity_scale
+        a.rho_ref = self.units.rho_ref
+        a.force_dt2 = self.units.force_dt2
+        a.force_den = self.units.force_den
+        _lib.check(_lib.load().lbw_alm_configure(self._domain, _lib.ctypes.byref(a)), "ALM")
+
+    # ------------------------------------------------------- per step
+    def refresh_points(self):
+        """Positions, velocities and frames from the topology state
+        (sim.py:167-191), stacked: identical doubles, O(1) numpy calls per
+        line."""
+        kin = self._kin
+        for comp, spec, sl in self._line_groups:
+            frames = comp.point_frames_arr
+            n = spec.n_points
+            self._pos_m[sl] = comp.point_positions_arr
+            kin[sl, 3:6] = comp.point_velocities
+            for col, v in ((6, spec.chord_local), (9, spec.normal_local), (12, spec.span_local)):
+                kin[sl, col:col + 3] = np.matmul(
+                    frames, np.broadcast_to(v, (n, 3))[:, :, None])[:, :, 0]
+        if self._line_groups:
+            L = np.asarray(self.grid.global_dims, dtype=np.float64)
+            periodic = np.asarray(self.grid.periodicity, dtype=bool)
+            lat = self._pos_m / self.units.dx
+            lat = np.where(periodic, np.mod(lat, L), lat)
+            bad = (~periodic) & ((lat < 0.0) | (lat >= L))
+            if np.any(bad):
+                p, k = np.argwhere(bad)[0]
+                raise ConfigError(
+                    f"position component {lat[p, k]} outside the non-periodic domain")
+            kin[:, 0:3] = lat
+
+    def _alm_results(self):
+        if self._results is None:
+            P = len(self.points)
+            rho, u, blade = np.zeros(P), np.zeros((P, 3)), np.zeros((P, 3))
+            if P:
+                rc = _lib.load().lbw_alm_get(self._domain, _lib.ptr(rho), _lib.ptr(u),
+                                             _lib.ptr(blade))
+                if rc == _lib.LBW_EINVAL:
+                    raise ValueError(_lib.last_error())
+                _lib.check(rc, "ALM results")
+            self._results = (rho, u, blade)
+        return self._results
+
+    def _poll(self, wait):
+        step, field = _lib.ctypes.c_int64(), _lib.ctypes.c_int32()
+        cell = (_lib.ctypes.c_int64 * 3)()
+        rc = _lib.load().lbw_domain_poll_nonfinite(self._domain, int(wait),
+                                                   _lib.ctypes.byref(step), cell,
+                                                   _lib.ctypes.byref(field))
+        if rc < 0:
+            _lib.check(rc, "poll")
+        if rc == 1:
+            raise NumericalAbort(int(step.value), tuple(int(c) for c in cell),
+                                 "density" if field.value == 0 else "velocity")
+
+    def _warn_clamps(self):
+        if not self.points or not self._polar_list:
+            return
+        flags = np.zeros(len(self._polar_list), dtype=np.int32)
+        _lib.check(_lib.load().lbw_alm_clamp_flags(
+            self._domain, flags.ctypes.data_as(_lib.ctypes.POINTER(_lib.ctypes.c_int32))))
+        for k in np.nonzero(flags)[0]:
+            self._polar_list[k].warn_clamp()
+
+    def step(self):
+        lib = _lib.load()
+        t = self.timer
+        if self.points:
+            t.start_phase("turbine")
+            self.refresh_points()
+            _lib.check(lib.lbw_alm_set_kinematics(self._domain, _lib.ptr(self._kin)), "ALM")
+            t.stop_phase()
+        t.start_phase("collide")
+        _lib.check(lib.lbw_domain_step(self._domain, 1), "step")
+        t.stop_phase()
+        self._results = None
+        self._poll(wait=False)
+        if self.cfg.topologies:
+            t.start_phase("turbine")
+            for topo in self.cfg.topologies:
+                topo.advance(self.units.dt)
+            t.stop_phase()
+        t.count_step()
+        self.step_index += 1
+        self._macro_fresh = False
+
+    def synchronize(self):
+        _lib.check(_lib.load().lbw_domain_sync(self._domain), "sync")
+        self._poll(wait=True)
+        self._warn_clamps()
+
+    # ---------------------------------------------------------- output
+    def _recompute_moments(self):
+        """moments of the current populations with the current force; they
+        also become the next actuator sampling source (sim.py:160-165)."""
+        self._poll(wait=True)
+        _lib.check(_lib.load().lbw_domain_recompute_moments(self._domain, None), "moments")
+        self._macro_fresh = True
+
+    def _probe_tick(self):
+        from . import output
+        output.probe_tick(self)
+
+    def run(self):
+        cfg = self.cfg
+        self.timer.start()
+        for _ in range(cfg.steps):
+            self.step()
+            if cfg.cadence > 0 and self.step_index % cfg.cadence == 0:
+                self.synchronize()
+                self.timer.stop()
+                self._probe_tick()
+                self.timer.start()
+        self.synchronize()
+        self.timer.stop()
+        if cfg.cadence == 0 and (cfg.probes or cfg.vtk):
+            self._probe_tick()
+        report = self.report()
+        os.makedirs(cfg.output_dir, exist_ok=True)
+        with open(os.path.join(cfg.output_dir, "report.json"), "w") as fh:
+            json.dump(report, fh, indent=2, sort_keys=True)
+        return report
+
+    def report(self):
+        cfg = self.cfg
+        cost = lbm_kernel_cost(precision_bytes=np.dtype(cfg.dtype).itemsize,
+                               n_f=cfg.kernel_flops())
+        u = self.units
+        out = {"config": cfg.echo(),
+               "units": {"dx_m": u.dx, "dt_s": u.dt, "u_lat": u.u_lat, "nu_lat": u.nu_lat,
+                         "tau": u.tau, "omega": u.omega},
+               "grid": {"cells": list(cfg.cells), "blocks": self.grid.nranks,
+                        "block_dims": list(self.grid.block_dims), "workers": cfg.workers,
+                        "actuator_points": len(self.points), "devices": self.grid.nranks},
+               "kernel": dict(cost.to_dict(), operator=cfg.operator, precision=cfg.precision,
+                              arithmetic=cfg.arithmetic),
+               "performance": dict(self.timer.to_dict(),
+                                   phase_fractions=self.timer.phase_fractions())}
+        if self.timer.steps > 0 and self.timer.wall_seconds > 0.0:
+            mlups, _ = measure_mlups(self.timer)
+            out["performance"]["mlups"] = mlups
+            if cfg.machine is not None:
+                out["performance"].update(percent_table_row(mlups, cfg.machine, cost))
+        if cfg.machine is not None:
+            out["machine"] = cfg.machine.to_dict()
+            ls = lightspeed(cfg.machine, cost)
+            if ls is not None:
+                out["machine"]["lightspeed"] = ls
+        return out
+
+    def close(self):
+        if getattr(self, "_domain", None):
+            _lib.load().lbw_domain_destroy(self._domain)
+            self._domain = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_simulation(cfg):
+    sim = Simulation(cfg)
+    try:
+        return sim.run()
+    finally:
+        sim.close()

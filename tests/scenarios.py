@@ -1,0 +1,93 @@
+"""Shared test scenarios: configs for the product and matching oracles."""
+
+import os
+import tempfile
+
+import numpy as np
+
+ROTOR_YAML = """
+name: alm
+components:
+  - name: tower
+    position: [0.0, 0.0, 0.0]
+  - name: nacelle
+    parent: tower
+    position: [0.0, 0.0, 0.8]
+  - name: hub
+    parent: nacelle
+    position: [-0.05, 0.0, 0.0]
+    rotation: {axis: [1.0, 0.0, 0.0], rate_rad_per_s: 96.0}
+  - name: blade1
+    parent: hub
+    discretization: {type: line, points: 6, r_start: 0.06, r_end: 0.48,
+                     chord: 0.08, twist_deg: 8.0, polar: sym}
+  - name: blade2
+    parent: hub
+    orientation: {axis: [1.0, 0.0, 0.0], angle_deg: 120.0}
+    discretization: {type: line, points: 6, r_start: 0.06, r_end: 0.48,
+                     chord: 0.08, twist_deg: 8.0, polar: sym}
+  - name: blade3
+    parent: hub
+    orientation: {axis: [1.0, 0.0, 0.0], angle_deg: 240.0}
+    discretization: {type: line, points: 6, r_start: 0.06, r_end: 0.48,
+                     chord: 0.08, twist_deg: 8.0, polar: sym}
+"""
+
+
+def sym_polar_csv():
+    a = np.arange(-180.0, 181.0, 15.0)
+    r = np.deg2rad(a)
+    rows = ["alpha_deg,cl,cd"]
+    rows += [f"{x},{0.9 * np.sin(2 * t):.6f},{0.08 + 0.3 * (1 - np.cos(2 * t)):.6f}"
+             for x, t in zip(a, r)]
+    return "\n".join(rows) + "\n"
+
+
+def write_rotor_files(d):
+    with open(os.path.join(d, "rotor.yaml"), "w") as fh:
+        fh.write(ROTOR_YAML)
+    with open(os.path.join(d, "sym.csv"), "w") as fh:
+        fh.write(sym_polar_csv())
+
+
+def rotor_raw(cells, periodic, boundary="periodic", position=(0.9, 0.3, 0.0), steps=0,
+              arithmetic="exact", nu=0.866, cpd=8, mach=0.1, operator="cumulant"):
+    return {"domain": {"cells": list(cells), "periodicity": list(periodic)},
+            "fluid": {"kinematic_viscosity": nu, "wind": [8.0, 0.0, 0.0]},
+            "resolution": {"cells_per_diameter": cpd, "reference_diameter": 1.0, "mach": mach},
+            "run": {"steps": steps, "boundary": boundary, "arithmetic": arithmetic,
+                    "collision": {"operator": operator}},
+            "turbines": [{"file": "rotor.yaml", "position": list(position)}],
+            "polars": [{"id": "sym", "file": "sym.csv"}]}
+
+
+def rotor_config(cells=(12, 12, 12), periodic=(True, True, True), boundary="periodic",
+                 position=(0.9, 0.3, 0.0), steps=0, arithmetic="exact", **kw):
+    """(RunConfig, TemporaryDirectory) for the golden-style rotor."""
+    from paper_2402_13171_b200 import parse_config
+    tmp = tempfile.TemporaryDirectory()
+    write_rotor_files(tmp.name)
+    cfg = parse_config(rotor_raw(cells, periodic, boundary, position, steps, arithmetic, **kw),
+                       base_dir=tmp.name)
+    return cfg, tmp
+
+
+def oracle_for(sim):
+    """OracleSim with the parameters and initial state of a product
+    Simulation (uniform wind product equilibrium)."""
+    from oracle import oracle as orc
+    cfg, u = sim.cfg, sim.units
+    points = None
+    if sim.points:
+        points = {"chord": np.array([p.chord for p in sim.points]),
+                  "element_length": np.array([p.element_length for p in sim.points]),
+                  "twist": np.array([p.twist for p in sim.points]),
+                  "polar": [None if p.polar is None else (p.polar.alpha, p.polar.cl, p.polar.cd)
+                            for p in sim.points],
+                  "vscale": u.velocity_scale, "rho_ref": u.rho_ref, "dt2": u.dt ** 2,
+                  "den": u.rho_ref * u.dx ** 4}
+    ref = orc.OracleSim(cfg.cells, periodic=cfg.periodicity, op=cfg.operator, omega=u.omega,
+                        rates=cfg.higher_order_rates, boundary=cfg.boundary_kind,
+                        u_in=sim.boundary.u_in_lat, points=points)
+    ref.initialize_equilibrium(1.0, sim.boundary.u_in_lat, product=(cfg.operator == "cumulant"))
+    return ref
