@@ -9,7 +9,18 @@
 #error "define LBW_FAST before including lbw_sweep.cuh"
 #endif
 
+// Kernels get a per-flavour namespace: identical template kernels in two
+// translation units would share one weak host stub, and the runtime would
+// launch whichever TU's cubin registered that stub (an ODR trap that once
+// ran the FMA kernel for LBW_MODE_EXACT).
+#if LBW_FAST
+#define LBW_FLAVOR fast
+#else
+#define LBW_FLAVOR exact
+#endif
+
 namespace lbw {
+namespace LBW_FLAVOR {
 
 constexpr int kSweepThreads = 128;
 
@@ -196,4 +207,6 @@ inline dim3 sweep_block(const Geom& g) {
     return dim3(bz, kSweepThreads / bz, 1);
 }
 
+}  // namespace LBW_FLAVOR
+using namespace LBW_FLAVOR;
 }  // namespace lbw
