@@ -360,7 +360,7 @@ class _HostOnlySim:
                             polar=cfg.polars.get(pid) if pid is not None else None))())
                     self._line_groups.append((comp, spec, slice(gid, gid + spec.n_points)))
                     gid += spec.n_points
-        self._kin = np.zeros((gid, 15))
+        self._kin = np.zeros((gid, 18))
         self._pos_m = np.zeros((gid, 3))
         self.refresh_points = Simulation.refresh_points.__get__(self)
 

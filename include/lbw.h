@@ -209,8 +209,37 @@ typedef struct lbw_alm_desc {
 } lbw_alm_desc;
 
 int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc);
-/* kin: (P, 15) = lattice position (wrapped, sim.py:188-191), velocity m/s,
- * e_chord, e_normal, e_span (sim.py:176-181).  Queued for the next step. */
+
+/* Device-side turbine kinematics (replaces TurbineTopology.advance +
+ * Simulation.refresh_points, turbine.py:227-311 / sim.py:167-191, with a
+ * one-CTA kernel per step).  Components in pre-order (parent < child),
+ * all turbines concatenated; every actuator point belongs to exactly one
+ * line component, numbered by global id. */
+typedef struct lbw_kin_desc {
+    int32_t n_components;
+    const int32_t* parent;          /* (C) parent index, -1 for a root          */
+    const double* rel_p;            /* (C,3) relative position                  */
+    const double* rel_T;            /* (C,3,3) relative orientation             */
+    const double* axis;             /* (C,3) unit rotation axis (any if rate 0) */
+    const double* rate;             /* (C) rad/s                                */
+    const double* step_rotation;    /* (C,3,3) rotation_matrix(axis, rate*dt)   */
+    const double* spin;             /* (C,3,3) accumulated spin now             */
+    const int32_t* line_first;      /* (C) first point id of the line, or -1    */
+    const int32_t* line_count;      /* (C) points of the line                   */
+    const double* offsets;          /* (P,3) line offsets from the start point  */
+    const double* orientations;     /* (P,3,3) per-point orientations           */
+    const double* local_frames;     /* (P,3,3) rows chord, normal, span (local) */
+    double dx;                      /* m per cell                               */
+    int32_t advance_first;          /* 1: advance by dt before the first step  */
+    int64_t reserved[8];
+} lbw_kin_desc;
+int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* desc);
+/* current device kinematics: kin (P,18) as in set_kinematics, spin
+ * (C,3,3), per-component world state (C,49) — any may be NULL. */
+int lbw_alm_download_kinematics(lbw_domain* d, double* kin, double* spin, double* comp_state);
+/* kin: (P, 18) = lattice position (wrapped, sim.py:188-191), velocity m/s,
+ * e_chord, e_normal, e_span (sim.py:176-181), position m.  Queued for the
+ * next step. */
 int lbw_alm_set_kinematics(lbw_domain* d, const double* kin);
 /* Results of the most recent actuator step (host arrays, may be NULL):
  * sampled rho (P,), sampled u lattice (P,3), blade force N (P,3).  Blocks

@@ -78,6 +78,27 @@ class AlmDesc(ctypes.Structure):
     ]
 
 
+class KinDesc(ctypes.Structure):
+    _fields_ = [
+        ("n_components", ctypes.c_int32),
+        ("parent", _c_i32_p),
+        ("rel_p", _c_double_p),
+        ("rel_T", _c_double_p),
+        ("axis", _c_double_p),
+        ("rate", _c_double_p),
+        ("step_rotation", _c_double_p),
+        ("spin", _c_double_p),
+        ("line_first", _c_i32_p),
+        ("line_count", _c_i32_p),
+        ("offsets", _c_double_p),
+        ("orientations", _c_double_p),
+        ("local_frames", _c_double_p),
+        ("dx", ctypes.c_double),
+        ("advance_first", ctypes.c_int32),
+        ("reserved", ctypes.c_int64 * 8),
+    ]
+
+
 # name -> (restype, argtypes); exactly the declarations of include/lbw.h
 _VP = ctypes.c_void_p
 _I = ctypes.c_int
@@ -116,6 +137,8 @@ SIGNATURES = {
     "lbw_domain_sweep_timing": (_I, [_VP, _I]),
     "lbw_domain_sweep_time": (_I, [_VP, _c_double_p, _c_i64_p]),
     "lbw_alm_configure": (_I, [_VP, ctypes.POINTER(AlmDesc)]),
+    "lbw_alm_configure_kinematics": (_I, [_VP, ctypes.POINTER(KinDesc)]),
+    "lbw_alm_download_kinematics": (_I, [_VP, _VP, _VP, _VP]),
     "lbw_alm_set_kinematics": (_I, [_VP, _VP]),
     "lbw_alm_get": (_I, [_VP, _VP, _VP, _VP]),
     "lbw_alm_clamp_flags": (_I, [_VP, _c_i32_p]),
@@ -184,6 +207,16 @@ def ptr(a):
     if not a.flags["C_CONTIGUOUS"]:
         raise ValueError("array must be C-contiguous")
     return ctypes.c_void_p(a.ctypes.data)
+
+
+def dptr(a):
+    """ctypes double* of a C-contiguous float64 array."""
+    return a.ctypes.data_as(_c_double_p)
+
+
+def iptr(a):
+    """ctypes int32* of a C-contiguous int32 array."""
+    return a.ctypes.data_as(_c_i32_p)
 
 
 def kernel_launches():

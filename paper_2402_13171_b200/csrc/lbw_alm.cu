@@ -1,22 +1,28 @@
 // lbw_alm.cu — actuator-line coupling on the device (compiled with
-// -fmad=false, like the exact sweep: the per-point arithmetic follows the
-// reference expression order).
+// -fmad=false like the exact sweep: the per-point arithmetic follows the
+// reference expression order).  Per step, three small launches precede
+// the sweep:
 //
-//   K4  k_alm_sample_force   one thread per point: trilinear sampling of the
-//                            previous step's macro field (recomputed from the
-//                            retained population buffer, App. A.7 of
-//                            SURVEY.md), angle of attack, polar lookup,
-//                            blade-element force, lattice force
-//                            (actuator.py:70-146, polars.py:65-80,
-//                            sim.py:210-235, units.py:69-70)
-//   K5a k_alm_clear          forget the rows used two steps ago
-//   K5b k_alm_mark           per point: Roma weights per axis with periodic
-//                            images (actuator.py:100-110, 190-195, 297-341);
-//                            claim a pool slot for every touched (x,y) row
-//   K5c k_alm_fill           one CTA per touched row: per cell, sum
-//                            (wx*wy)*wz*F over the points in ascending
-//                            global id starting from 0.0 (actuator.py:204-247)
-//                            — deterministic, no float atomics.
+//   KK  k_kinematics       (device kinematics mode) one CTA: advance every
+//                          component's spin by R(axis, rate dt), compose the
+//                          world frames down the tree, then every point's
+//                          position, velocity and chord/normal/span frame
+//                          (turbine.py:227-311, sim.py:167-191)
+//   K4  k_alm_points       one warp per point: lanes 0-7 recompute the
+//                          previous step's macro at the 8 sampling-cube cells
+//                          from the retained population buffer (SURVEY.md
+//                          App. A.7); lane 0 interpolates, evaluates angle of
+//                          attack, polar and blade-element force
+//                          (actuator.py:70-146, polars.py:65-80,
+//                          sim.py:210-235); lanes 0-2 build the per-axis Roma
+//                          deposit lists with periodic images
+//                          (actuator.py:100-110, 190-195, 297-341); lane 0
+//                          claims a pool slot for every touched (x,y) row
+//   K5  k_alm_fill         one CTA per claimed row: per cell, the sum of
+//                          (wx*wy)*wz*F over the points in ascending global id
+//                          from 0.0 (actuator.py:204-247) — deterministic, no
+//                          float atomics.  CTA 0 also clears the other force
+//                          set (last read by this step's K4) for the next step.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -29,8 +35,13 @@
 
 namespace lbw {
 
-constexpr int kKin = 15;  // pos_lat(3) vel(3) e_chord(3) e_normal(3) e_span(3)
+constexpr int kKin = 18;  // pos_lat(3) vel(3) e_chord(3) e_normal(3) e_span(3) pos_m(3)
 constexpr int kRing = 8;
+// per-component device state: world p(3) T(9) v(3) w(3) spin_axis(3) has_axis(1)
+// start_p(3) start_T(9) v_start(3) w_start(3) R(9)
+constexpr int kCS = 49;
+enum { CS_P = 0, CS_T = 3, CS_V = 12, CS_W = 15, CS_AX = 18, CS_HAX = 21, CS_SP = 22,
+       CS_ST = 25, CS_VS = 34, CS_WS = 37, CS_R = 40 };
 
 struct AlmDev {
     int32_t n;
@@ -44,14 +55,33 @@ struct AlmDev {
     const double* p_cl;
     const double* p_cd;
     double vscale, rho_ref, dt2, den;
-    const double* kin;     // (P,15)
+    double* kin;           // (P,18)
     double* samples;       // (P,4)
     double* blade;         // (P,3)
     double* flat;          // (P,3) lattice force on the fluid
     int32_t* dep_cell;     // (P,3 axes,3) global cell or -1
     double* dep_w;         // (P,3,3)
     int32_t* clamp_flags;  // (n_polars)
-    int32_t* error_flags;  // bit 0: non-positive sampled density
+    int32_t* error_flags;  // bit 0: non-positive density, bit 1: point outside domain
+};
+
+struct KinDev {
+    int32_t nc;
+    const int32_t* parent;
+    const double* rel_p;
+    const double* rel_T;
+    const double* axis;
+    const double* rate;
+    const double* rstep;
+    double* spin;
+    const int32_t* line_first;
+    const int32_t* line_count;
+    const int32_t* point_comp;
+    const double* off;
+    const double* orient;
+    const double* lframe;
+    double* cs;
+    double dx;
 };
 
 struct AlmState {
@@ -66,13 +96,25 @@ struct AlmState {
     int32_t *clamp_flags = nullptr, *error_flags = nullptr;
     double vscale = 0, rho_ref = 0, dt2 = 0, den = 0;
     ForceSet set[2];
-    double* h_ring = nullptr;   // pinned (kRing, P, 15)
+    double* h_ring = nullptr;   // pinned (kRing, P, 18)
     cudaEvent_t ring_ev[kRing] = {};
     int ring_pos = 0;
     bool kin_queued = false;
     bool stepped = false;       // apply_outer_boundary has run at least once
     int flip = 0;               // force set written by the next actuator step
+    size_t fill_smem = 0;
+    // device kinematics
+    bool kin_device = false;
+    int32_t nc = 0;
+    int32_t *k_parent = nullptr, *k_line_first = nullptr, *k_line_count = nullptr;
+    int32_t* k_point_comp = nullptr;
+    double *k_rel_p = nullptr, *k_rel_T = nullptr, *k_axis = nullptr, *k_rate = nullptr;
+    double *k_rstep = nullptr, *k_spin = nullptr, *k_off = nullptr, *k_orient = nullptr;
+    double *k_lframe = nullptr, *k_cs = nullptr;
+    double k_dx = 1.0;
+    bool k_advance = false;     // advance the tree before the next evaluation
     std::vector<void*> allocs;
+
     AlmDev dev() const {
         AlmDev a;
         a.n = n;
@@ -99,6 +141,26 @@ struct AlmState {
         a.error_flags = error_flags;
         return a;
     }
+    KinDev kdev() const {
+        KinDev k;
+        k.nc = nc;
+        k.parent = k_parent;
+        k.rel_p = k_rel_p;
+        k.rel_T = k_rel_T;
+        k.axis = k_axis;
+        k.rate = k_rate;
+        k.rstep = k_rstep;
+        k.spin = k_spin;
+        k.line_first = k_line_first;
+        k.line_count = k_line_count;
+        k.point_comp = k_point_comp;
+        k.off = k_off;
+        k.orient = k_orient;
+        k.lframe = k_lframe;
+        k.cs = k_cs;
+        k.dx = k_dx;
+        return k;
+    }
 };
 
 // How the macro field sampled at this step is obtained (MacroSource).
@@ -116,6 +178,162 @@ struct MacroDev {
 };
 
 namespace {
+
+// ------------------------------------------------------------ 3x3 algebra
+// row-major 3x3; C = A B with a fixed (a0 b0 + a1 b1) + a2 b2 order
+__device__ void mm3(const double* A, const double* B, double* C) {
+    double t[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            t[i * 3 + j] = A[i * 3] * B[j] + A[i * 3 + 1] * B[3 + j] + A[i * 3 + 2] * B[6 + j];
+    for (int k = 0; k < 9; ++k) C[k] = t[k];
+}
+__device__ void mv3(const double* A, const double* v, double* out) {
+    double t[3];
+    for (int i = 0; i < 3; ++i) t[i] = A[i * 3] * v[0] + A[i * 3 + 1] * v[1] + A[i * 3 + 2] * v[2];
+    for (int i = 0; i < 3; ++i) out[i] = t[i];
+}
+__device__ void cross3(const double* a, const double* b, double* out) {
+    const double c0 = a[1] * b[2] - a[2] * b[1];
+    const double c1 = a[2] * b[0] - a[0] * b[2];
+    const double c2 = a[0] * b[1] - a[1] * b[0];
+    out[0] = c0;
+    out[1] = c1;
+    out[2] = c2;
+}
+// max |T^T T - I| > 1e-12 (turbine.py:_DRIFT_TOL)
+__device__ bool drifted(const double* T) {
+    double m = 0.0;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = T[i] * T[j] + T[3 + i] * T[3 + j] + T[6 + i] * T[6 + j];
+            if (i == j) s -= 1.0;
+            m = fmax(m, fabs(s));
+        }
+    return m > 1e-12;
+}
+// Gram-Schmidt on the columns (turbine.py:83-90)
+__device__ void reorth(double* T) {
+    double c0[3] = {T[0], T[3], T[6]}, c1[3] = {T[1], T[4], T[7]};
+    const double n0 = sqrt(c0[0] * c0[0] + c0[1] * c0[1] + c0[2] * c0[2]);
+    for (int i = 0; i < 3; ++i) c0[i] /= n0;
+    const double d = c0[0] * c1[0] + c0[1] * c1[1] + c0[2] * c1[2];
+    for (int i = 0; i < 3; ++i) c1[i] = c1[i] - d * c0[i];
+    const double n1 = sqrt(c1[0] * c1[0] + c1[1] * c1[1] + c1[2] * c1[2]);
+    for (int i = 0; i < 3; ++i) c1[i] /= n1;
+    double c2[3];
+    cross3(c0, c1, c2);
+    for (int i = 0; i < 3; ++i) {
+        T[i * 3] = c0[i];
+        T[i * 3 + 1] = c1[i];
+        T[i * 3 + 2] = c2[i];
+    }
+}
+// numpy float remainder (npy_divmod): result takes the divisor's sign
+__device__ double np_mod(double a, double b) {
+    double m = fmod(a, b);
+    if (m != 0.0) {
+        if ((b < 0) != (m < 0)) m += b;
+    } else {
+        m = copysign(0.0, b);
+    }
+    return m;
+}
+
+// KK: tree walk + point kinematics, one CTA
+__global__ void k_kinematics(KinDev k, AlmDev a, Geom g, int per_x, int advance) {
+    if (threadIdx.x == 0) {
+        for (int c = 0; c < k.nc; ++c) {
+            double* s = k.cs + (int64_t)c * kCS;
+            const int par = k.parent[c];
+            const double I3[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+            const double zero3[3] = {0, 0, 0};
+            const double* Pp = par >= 0 ? k.cs + (int64_t)par * kCS + CS_P : zero3;
+            const double* PT = par >= 0 ? k.cs + (int64_t)par * kCS + CS_T : I3;
+            const double* Pv = par >= 0 ? k.cs + (int64_t)par * kCS + CS_V : zero3;
+            const double* Pw = par >= 0 ? k.cs + (int64_t)par * kCS + CS_W : zero3;
+            double* spin = k.spin + c * 9;
+            const double rate = k.rate[c];
+            if (advance && rate != 0.0) {
+                mm3(spin, k.rstep + c * 9, spin);
+                if (drifted(spin)) reorth(spin);
+            }
+            double Tp_rp[3], Tp_Tr[9];
+            mv3(PT, k.rel_p + c * 3, Tp_rp);
+            mm3(PT, k.rel_T + c * 9, Tp_Tr);
+            for (int i = 0; i < 3; ++i) s[CS_P + i] = Pp[i] + Tp_rp[i];
+            mm3(Tp_Tr, spin, s + CS_T);
+            if (drifted(s + CS_T)) reorth(s + CS_T);
+            double cr[3];
+            cross3(Pw, Tp_rp, cr);
+            for (int i = 0; i < 3; ++i) s[CS_V + i] = Pv[i] + cr[i];
+            for (int i = 0; i < 3; ++i) s[CS_W + i] = Pw[i];
+            if (par >= 0) {
+                const double* ps = k.cs + (int64_t)par * kCS;
+                for (int i = 0; i < 3; ++i) s[CS_AX + i] = ps[CS_AX + i];
+                s[CS_HAX] = ps[CS_HAX];
+            } else {
+                s[CS_AX] = s[CS_AX + 1] = s[CS_AX + 2] = 0.0;
+                s[CS_HAX] = 0.0;
+            }
+            if (rate != 0.0) {
+                mv3(Tp_Tr, k.axis + c * 3, s + CS_AX);
+                s[CS_HAX] = 1.0;
+                for (int i = 0; i < 3; ++i) s[CS_W + i] = s[CS_W + i] + s[CS_AX + i] * rate;
+            }
+            for (int i = 0; i < 9; ++i) s[CS_R + i] = spin[i];
+            const int first = k.line_first[c];
+            if (first >= 0) {
+                const double* W = s + CS_T;
+                double Tp_o0[3], Tp_O0[9];
+                mv3(W, k.off + (int64_t)first * 3, Tp_o0);
+                for (int i = 0; i < 3; ++i) s[CS_SP + i] = s[CS_P + i] + Tp_o0[i];
+                mm3(W, k.orient + (int64_t)first * 9, Tp_O0);
+                mm3(Tp_O0, spin, s + CS_ST);
+                cross3(s + CS_W, Tp_o0, cr);
+                for (int i = 0; i < 3; ++i) s[CS_VS + i] = s[CS_V + i] + cr[i];
+                for (int i = 0; i < 3; ++i) s[CS_WS + i] = s[CS_W + i];
+                if (rate != 0.0) {
+                    double ax[3];
+                    mv3(Tp_O0, k.axis + c * 3, ax);
+                    for (int i = 0; i < 3; ++i) s[CS_WS + i] = s[CS_WS + i] + ax[i] * rate;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const int64_t dims[3] = {g.nxg, g.ny, g.nz};
+    const int per[3] = {per_x, g.per_y, g.per_z};
+    for (int p = threadIdx.x; p < a.n; p += blockDim.x) {
+        const int c = k.point_comp[p];
+        const double* s = k.cs + (int64_t)c * kCS;
+        const int kk = p - k.line_first[c];
+        double pos[3], fr[9], vel[3];
+        if (kk == 0) {
+            for (int i = 0; i < 3; ++i) pos[i] = s[CS_SP + i];
+            for (int i = 0; i < 9; ++i) fr[i] = s[CS_ST + i];
+            for (int i = 0; i < 3; ++i) vel[i] = s[CS_VS + i];
+        } else {
+            double rel[3], tmp[9], cr[3];
+            mv3(s + CS_ST, k.off + (int64_t)p * 3, rel);
+            for (int i = 0; i < 3; ++i) pos[i] = s[CS_SP + i] + rel[i];
+            mm3(s + CS_ST, k.orient + (int64_t)p * 9, tmp);
+            mm3(tmp, s + CS_R, fr);
+            cross3(s + CS_WS, rel, cr);
+            for (int i = 0; i < 3; ++i) vel[i] = s[CS_VS + i] + cr[i];
+        }
+        double* out = a.kin + (int64_t)p * kKin;
+        for (int i = 0; i < 3; ++i) {
+            double lat = pos[i] / k.dx;
+            if (per[i]) lat = np_mod(lat, (double)dims[i]);
+            else if (!(lat >= 0.0 && lat < (double)dims[i])) atomicOr(a.error_flags, 2);
+            out[i] = lat;
+            out[3 + i] = vel[i];
+            out[15 + i] = pos[i];
+        }
+        for (int f = 0; f < 3; ++f) mv3(fr, k.lframe + (int64_t)p * 9 + f * 3, out + 6 + 3 * f);
+    }
+}
 
 // Macro (rho, u) of global cell (gx,gy,gz), following the ghost semantics
 // of PdfField.macro (fields.py:35-36, halo.py:144-160).  Returns false when
@@ -185,7 +403,6 @@ __device__ __forceinline__ double dot3(const double* a, const double* b) {
 // np.interp on one value (numpy compiled_base.c arr_interp semantics)
 __device__ double interp1(double x, const double* xp, const double* fp, int n) {
     if (isnan(x)) return x;
-    int j;
     if (x < xp[0]) return fp[0];
     if (x > xp[n - 1]) return fp[n - 1];
     if (x == xp[n - 1]) return fp[n - 1];
@@ -195,7 +412,7 @@ __device__ double interp1(double x, const double* xp, const double* fp, int n) {
         if (xp[mid] <= x) lo = mid;
         else hi = mid;
     }
-    j = lo;
+    const int j = lo;
     if (xp[j] == x) return fp[j];
     const double slope = (fp[j + 1] - fp[j]) / (xp[j + 1] - xp[j]);
     double r = slope * (x - xp[j]) + fp[j];
@@ -217,11 +434,75 @@ __device__ __forceinline__ double roma(double r) {
     return 0.0;
 }
 
-__global__ void k_alm_sample_force(AlmDev a, Geom g, MacroDev m) {
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= a.n) return;
+// blade-element force on the BLADE (actuator.py:117-146, sim.py:218-235)
+__device__ void blade_force(const AlmDev& a, int p, const double* kin, const double* acc,
+                            double* blade) {
+    blade[0] = blade[1] = blade[2] = 0.0;
+    const int pid = a.polar_index[p];
+    if (pid < 0) return;
+    const double* vel = kin + 3;
+    const double* ec = kin + 6;
+    const double* en = kin + 9;
+    const double* es = kin + 12;
+    double urel[3];
+    for (int c = 0; c < 3; ++c) urel[c] = acc[1 + c] * a.vscale - vel[c];
+    const double along = dot3(urel, es);
+    double up[3];
+    for (int c = 0; c < 3; ++c) up[c] = urel[c] - along * es[c];
+    const double speed = sqrt(dot3(up, up));
+    if (!(speed >= 1e-12)) return;  // DEGENERATE_SPEED (actuator.py:30)
+    const double phi = atan2(dot3(up, en), dot3(up, ec));
+    double alpha = phi - a.twist[p];
+    double ed[3], el[3];
+    for (int c = 0; c < 3; ++c) ed[c] = up[c] / speed;
+    cross3(es, ed, el);
+    const int off = a.polar_offset[pid], rows = a.polar_rows[pid];
+    const double* xp = a.p_alpha + off;
+    if (alpha < xp[0] || alpha > xp[rows - 1]) {
+        atomicOr(&a.clamp_flags[pid], 1);
+        alpha = fmin(fmax(alpha, xp[0]), xp[rows - 1]);
+    }
+    const double cl = interp1(alpha, xp, a.p_cl + off, rows);
+    const double cd = interp1(alpha, xp, a.p_cd + off, rows);
+    const double rho_phys = acc[0] * a.rho_ref;
+    if (!(rho_phys > 0.0)) atomicOr(a.error_flags, 1);
+    const double scale = 0.5 * rho_phys * speed * speed * a.chord[p] * a.elen[p];
+    for (int c = 0; c < 3; ++c) blade[c] = scale * (cl * el[c] + cd * ed[c]);
+}
+
+// per-axis deposit cells + weights, images across periodic faces computed
+// from the shifted position pos - w*L (actuator.py:190-195, 330-332)
+__device__ void deposit_axis(double x, int64_t L, int periodic, int32_t* dc, double* dw) {
+    int cnt = 0;
+    for (int q = 0; q < 3; ++q) {
+        dc[q] = -1;
+        dw[q] = 0.0;
+    }
+    const int nimg = periodic ? 3 : 1;
+    for (int im = 0; im < nimg; ++im) {
+        const double w = im == 0 ? 0.0 : (im == 1 ? 1.0 : -1.0);
+        const double xs = im == 0 ? x : x - w * (double)L;
+        const double n0f = floor(xs);
+        const int64_t n0 = (int64_t)n0f;
+        const double r[3] = {xs - (n0f - 0.5), xs - (n0f + 0.5), xs - (n0f + 1.5)};
+        for (int q = 0; q < 3; ++q) {
+            const int64_t c = n0 - 1 + q;
+            if (c < 0 || c >= L) continue;
+            const double wt = roma(r[q]);
+            if (wt == 0.0 || cnt >= 3) continue;
+            dc[cnt] = (int32_t)c;
+            dw[cnt] = wt;
+            ++cnt;
+        }
+    }
+}
+
+// K4: one warp per point
+__global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s) {
+    const int p = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (p >= a.n) return;  // uniform per warp
     const double* kin = a.kin + (int64_t)p * kKin;
-    // --- trilinear sampling (actuator.py:77-93)
     int64_t j0[3];
     double t[3];
     for (int k = 0; k < 3; ++k) {
@@ -229,125 +510,66 @@ __global__ void k_alm_sample_force(AlmDev a, Geom g, MacroDev m) {
         j0[k] = (int64_t)fl;
         t[k] = kin[k] - 0.5 - fl;
     }
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    if (lane < 8)
+        macro_at(g, m, j0[0] + ((lane >> 2) & 1), j0[1] + ((lane >> 1) & 1), j0[2] + (lane & 1), v);
+    // lane 0: trilinear sum in (dx,dy,dz) lexicographic order (actuator.py:88-92)
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int dx = 0; dx < 2; ++dx) {
-        const double wx = dx ? t[0] : 1.0 - t[0];
-        for (int dy = 0; dy < 2; ++dy) {
-            const double wy = dy ? t[1] : 1.0 - t[1];
-            for (int dz = 0; dz < 2; ++dz) {
-                const double wz = dz ? t[2] : 1.0 - t[2];
-                const double w = wx * wy * wz;
-                double v[4];
-                macro_at(g, m, j0[0] + dx, j0[1] + dy, j0[2] + dz, v);
-                for (int c = 0; c < 4; ++c) acc[c] += w * v[c];
-            }
-        }
+    for (int c = 0; c < 8; ++c) {
+        double vc[4];
+        for (int q = 0; q < 4; ++q) vc[q] = __shfl_sync(0xffffffffu, v[q], c);
+        const double wx = (c >> 2) & 1 ? t[0] : 1.0 - t[0];
+        const double wy = (c >> 1) & 1 ? t[1] : 1.0 - t[1];
+        const double wz = c & 1 ? t[2] : 1.0 - t[2];
+        const double w = wx * wy * wz;
+        for (int q = 0; q < 4; ++q) acc[q] += w * vc[q];
     }
-    for (int c = 0; c < 4; ++c) a.samples[p * 4 + c] = acc[c];
-
-    // --- blade element (actuator.py:117-146, sim.py:218-235)
-    double blade[3] = {0.0, 0.0, 0.0};
-    const int pid = a.polar_index[p];
-    if (pid >= 0) {
-        const double* vel = kin + 3;
-        const double* ec = kin + 6;
-        const double* en = kin + 9;
-        const double* es = kin + 12;
-        double urel[3];
-        for (int c = 0; c < 3; ++c) urel[c] = acc[1 + c] * a.vscale - vel[c];
-        const double along = dot3(urel, es);
-        double up[3];
-        for (int c = 0; c < 3; ++c) up[c] = urel[c] - along * es[c];
-        const double speed = sqrt(dot3(up, up));
-        if (speed >= 1e-12) {  // DEGENERATE_SPEED (actuator.py:30)
-            const double phi = atan2(dot3(up, en), dot3(up, ec));
-            double alpha = phi - a.twist[p];
-            double ed[3], el[3];
-            for (int c = 0; c < 3; ++c) ed[c] = up[c] / speed;
-            el[0] = es[1] * ed[2] - es[2] * ed[1];
-            el[1] = es[2] * ed[0] - es[0] * ed[2];
-            el[2] = es[0] * ed[1] - es[1] * ed[0];
-            const int off = a.polar_offset[pid], rows = a.polar_rows[pid];
-            const double* xp = a.p_alpha + off;
-            if (alpha < xp[0] || alpha > xp[rows - 1]) {
-                atomicOr(&a.clamp_flags[pid], 1);
-                alpha = fmin(fmax(alpha, xp[0]), xp[rows - 1]);
-            }
-            const double cl = interp1(alpha, xp, a.p_cl + off, rows);
-            const double cd = interp1(alpha, xp, a.p_cd + off, rows);
-            const double rho_phys = acc[0] * a.rho_ref;
-            if (!(rho_phys > 0.0)) atomicOr(a.error_flags, 1);
-            const double scale = 0.5 * rho_phys * speed * speed * a.chord[p] * a.elen[p];
-            for (int c = 0; c < 3; ++c) blade[c] = scale * (cl * el[c] + cd * ed[c]);
-        }
-    }
-    for (int c = 0; c < 3; ++c) {
-        a.blade[p * 3 + c] = blade[c];
-        // fluid force = -blade, to lattice units (units.py:69)
-        a.flat[p * 3 + c] = -blade[c] * a.dt2 / a.den;
-    }
-}
-
-__global__ void k_alm_clear(ForceSet s) {
-    const int32_t n = *s.count;
-    for (int32_t i = threadIdx.x; i < n; i += blockDim.x) s.row_slot[s.slot_row[i]] = -1;
-    __syncthreads();
-    if (threadIdx.x == 0) *s.count = 0;
-}
-
-// per point: deposit cells + Roma weights per axis, images across periodic
-// faces computed from the shifted position pos - w*L (actuator.py:330-332)
-__global__ void k_alm_mark(AlmDev a, Geom g, int per_x, ForceSet s) {
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= a.n) return;
-    const double* kin = a.kin + (int64_t)p * kKin;
-    const int64_t dims[3] = {g.nxg, g.ny, g.nz};
-    const int per[3] = {per_x, g.per_y, g.per_z};
     int32_t* dc = a.dep_cell + (int64_t)p * 9;
     double* dw = a.dep_w + (int64_t)p * 9;
-    for (int k = 0; k < 3; ++k) {
-        int cnt = 0;
-        for (int q = 0; q < 3; ++q) { dc[k * 3 + q] = -1; dw[k * 3 + q] = 0.0; }
-        const int nimg = per[k] ? 3 : 1;
-        for (int im = 0; im < nimg; ++im) {
-            const double w = im == 0 ? 0.0 : (im == 1 ? 1.0 : -1.0);
-            const double x = im == 0 ? kin[k] : kin[k] - w * (double)dims[k];
-            const double n0f = floor(x);
-            const int64_t n0 = (int64_t)n0f;
-            const double r[3] = {x - (n0f - 0.5), x - (n0f + 0.5), x - (n0f + 1.5)};
-            for (int q = 0; q < 3; ++q) {
-                const int64_t c = n0 - 1 + q;
-                if (c < 0 || c >= dims[k]) continue;
-                const double wt = roma(r[q]);
-                if (wt == 0.0 || cnt >= 3) continue;
-                dc[k * 3 + cnt] = (int32_t)c;
-                dw[k * 3 + cnt] = wt;
-                ++cnt;
-            }
+    if (lane == 0) {
+        for (int q = 0; q < 4; ++q) a.samples[p * 4 + q] = acc[q];
+        double blade[3];
+        blade_force(a, p, kin, acc, blade);
+        for (int c = 0; c < 3; ++c) {
+            a.blade[p * 3 + c] = blade[c];
+            a.flat[p * 3 + c] = -blade[c] * a.dt2 / a.den;  // units.py:69
         }
+    } else if (lane >= 1 && lane <= 3) {
+        const int k = lane - 1;
+        const int64_t L = k == 0 ? g.nxg : (k == 1 ? g.ny : g.nz);
+        const int per = k == 0 ? m.per_x : (k == 1 ? g.per_y : g.per_z);
+        deposit_axis(kin[k], L, per, dc + 3 * k, dw + 3 * k);
     }
-    // claim the (x,y) rows of this slab
-    for (int i = 0; i < 3; ++i) {
-        const int32_t cxg = dc[i];
-        if (cxg < 0) continue;
-        const int64_t x = cxg - g.x0;
-        if (x < 0 || x >= g.nxl) continue;
-        for (int j = 0; j < 3; ++j) {
-            const int32_t cy = dc[3 + j];
-            if (cy < 0) continue;
-            const int64_t row = x * g.ny + cy;
-            if (atomicCAS(&s.row_slot[row], -1, -2) == -1) {
-                const int32_t slot = atomicAdd(s.count, 1);
-                s.slot_row[slot] = (int32_t)row;
-                s.row_slot[row] = slot;
+    __syncwarp();
+    if (lane == 0) {
+        for (int i = 0; i < 3; ++i) {
+            const int32_t cxg = dc[i];
+            if (cxg < 0) continue;
+            const int64_t x = cxg - g.x0;
+            if (x < 0 || x >= g.nxl) continue;
+            for (int j = 0; j < 3; ++j) {
+                const int32_t cy = dc[3 + j];
+                if (cy < 0) continue;
+                const int64_t row = x * g.ny + cy;
+                if (atomicCAS(&s.row_slot[row], -1, -2) == -1) {
+                    const int32_t slot = atomicAdd(s.count, 1);
+                    s.slot_row[slot] = (int32_t)row;
+                    s.row_slot[row] = slot;
+                }
             }
         }
     }
 }
 
-// one CTA per used slot; dynamic shared memory holds (point, wxy) pairs
-__global__ void k_alm_fill(AlmDev a, Geom g, ForceSet s) {
+// K5: one CTA per used slot of set s; CTA 0 first clears set `old`.
+__global__ void k_alm_fill(AlmDev a, Geom g, ForceSet s, ForceSet old) {
     extern __shared__ unsigned char smem[];
+    if (blockIdx.x == 0) {
+        const int32_t n = *old.count;
+        for (int32_t i = threadIdx.x; i < n; i += blockDim.x) old.row_slot[old.slot_row[i]] = -1;
+        __syncthreads();
+        if (threadIdx.x == 0) *old.count = 0;
+    }
     const int32_t slot = blockIdx.x;
     if (slot >= *s.count) return;
     const int32_t row = s.slot_row[slot];
@@ -360,7 +582,7 @@ __global__ void k_alm_fill(AlmDev a, Geom g, ForceSet s) {
     if (threadIdx.x == 0) base = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-    // ordered compaction of the points touching row (xg, y)
+    // ordered compaction of the points touching row (xg, y), ascending id
     for (int c0 = 0; c0 < a.n; c0 += blockDim.x) {
         const int p = c0 + threadIdx.x;
         bool hit = false;
@@ -444,12 +666,19 @@ void alm_destroy(lbw_domain* d) {
 
 int alm_before_collide(lbw_domain* d, ForceView* fv_out) {
     AlmState* s = d->alm;
-    if (!s->kin_queued) {
+    const Geom& g = d->g;
+    const AlmDev a = s->dev();
+    const int per_x = d->desc.periodic[0] ? 1 : 0;
+    if (s->kin_device) {
+        k_kinematics<<<1, 256, 0, d->stream>>>(s->kdev(), a, g, per_x, s->k_advance ? 1 : 0);
+        count_launch();
+        LBW_CK(cudaGetLastError());
+        s->k_advance = true;
+    } else if (!s->kin_queued) {
         set_error("actuator step without kinematics: call lbw_alm_set_kinematics first");
         return LBW_ESTATE;
     }
     s->kin_queued = false;
-    const Geom& g = d->g;
     MacroDev m{};
     m.kind = d->msrc.kind;
     for (int k = 0; k < 4; ++k) m.uniform[k] = d->msrc.uniform[k];
@@ -460,20 +689,15 @@ int alm_before_collide(lbw_domain* d, ForceView* fv_out) {
     m.bc_set = s->stepped ? 1 : 0;
     for (int k = 0; k < 3; ++k) m.u_in[k] = d->desc.u_in[k];
     m.inflow = d->desc.boundary == LBW_BC_INFLOW_OUTFLOW ? 1 : 0;
-    m.per_x = d->desc.periodic[0] ? 1 : 0;
-    const AlmDev a = s->dev();
-    const int threads = 64;
-    const unsigned blocks = (unsigned)((s->n + threads - 1) / threads);
-    k_alm_sample_force<<<blocks, threads, 0, d->stream>>>(a, g, m);
-    count_launch();
-    LBW_CK(cudaGetLastError());
+    m.per_x = per_x;
     ForceSet& fs = s->set[s->flip];
+    ForceSet& old = s->set[s->flip ^ 1];
     s->flip ^= 1;
-    k_alm_clear<<<1, 256, 0, d->stream>>>(fs);
-    k_alm_mark<<<blocks, threads, 0, d->stream>>>(a, g, m.per_x, fs);
-    const size_t shm = ((size_t)(s->n * 4 + 15) / 16) * 16 + (size_t)s->n * 8;
-    k_alm_fill<<<(unsigned)fs.cap, 128, shm, d->stream>>>(a, g, fs);
-    count_launch(3);
+    const int threads = 128;
+    const unsigned blocks = (unsigned)((s->n * 32 + threads - 1) / threads);
+    k_alm_points<<<blocks, threads, 0, d->stream>>>(a, g, m, fs);
+    k_alm_fill<<<(unsigned)fs.cap, 128, s->fill_smem, d->stream>>>(a, g, fs, old);
+    count_launch(2);
     LBW_CK(cudaGetLastError());
     s->stepped = true;
     *fv_out = fs.view();
@@ -511,6 +735,16 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     s->rho_ref = desc->rho_ref;
     s->dt2 = desc->force_dt2;
     s->den = desc->force_den;
+    s->fill_smem = ((size_t)(P * 4 + 15) / 16) * 16 + (size_t)P * 8;
+    if (s->fill_smem > 48 * 1024) {
+        if (cudaFuncSetAttribute(k_alm_fill, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)s->fill_smem) != cudaSuccess) {
+            cudaGetLastError();
+            alm_destroy(d);
+            set_error("too many actuator points for one CTA's point list");
+            return LBW_EINVAL;
+        }
+    }
     int rc = LBW_OK;
     auto A = [&](auto** p, size_t n) {
         if (rc == LBW_OK) rc = dev_alloc(d, s, p, n);
@@ -595,10 +829,94 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     return LBW_OK;
 }
 
+int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
+    LBW_REQ(d && kd, "null argument");
+    LBW_REQ(alm_active(d), "configure the actuator points first");
+    AlmState* s = d->alm;
+    const int C = kd->n_components, P = s->n;
+    LBW_REQ(C >= 1, "need at least one component");
+    LBW_REQ(kd->dx > 0.0, "dx must be positive");
+    for (int c = 0; c < C; ++c) {
+        LBW_REQ(kd->parent[c] >= -1 && kd->parent[c] < c, "components must be in pre-order");
+        LBW_REQ(kd->line_first[c] >= -1 && kd->line_first[c] + kd->line_count[c] <= P,
+                "line point range out of bounds");
+    }
+    LBW_CK(cudaSetDevice(d->device));
+    LBW_CK(cudaStreamSynchronize(d->stream));
+    std::vector<int32_t> point_comp(P, -1);
+    for (int c = 0; c < C; ++c)
+        for (int k = 0; k < kd->line_count[c]; ++k) point_comp[kd->line_first[c] + k] = c;
+    for (int p = 0; p < P; ++p) LBW_REQ(point_comp[p] >= 0, "point without a line component");
+    int rc = LBW_OK;
+    auto A = [&](auto** p, size_t n) {
+        if (rc == LBW_OK) rc = dev_alloc(d, s, p, n);
+    };
+    A(&s->k_parent, C);
+    A(&s->k_line_first, C);
+    A(&s->k_line_count, C);
+    A(&s->k_point_comp, P);
+    A(&s->k_rel_p, (size_t)C * 3);
+    A(&s->k_rel_T, (size_t)C * 9);
+    A(&s->k_axis, (size_t)C * 3);
+    A(&s->k_rate, C);
+    A(&s->k_rstep, (size_t)C * 9);
+    A(&s->k_spin, (size_t)C * 9);
+    A(&s->k_off, (size_t)P * 3);
+    A(&s->k_orient, (size_t)P * 9);
+    A(&s->k_lframe, (size_t)P * 9);
+    A(&s->k_cs, (size_t)C * kCS);
+    if (rc) return rc;
+    auto H = [&](void* dst, const void* src, size_t bytes) {
+        if (rc == LBW_OK && cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("kinematics upload failed");
+            rc = LBW_ECUDA;
+        }
+    };
+    H(s->k_parent, kd->parent, C * 4);
+    H(s->k_line_first, kd->line_first, C * 4);
+    H(s->k_line_count, kd->line_count, C * 4);
+    H(s->k_point_comp, point_comp.data(), P * 4);
+    H(s->k_rel_p, kd->rel_p, C * 24);
+    H(s->k_rel_T, kd->rel_T, C * 72);
+    H(s->k_axis, kd->axis, C * 24);
+    H(s->k_rate, kd->rate, C * 8);
+    H(s->k_rstep, kd->step_rotation, C * 72);
+    H(s->k_spin, kd->spin, C * 72);
+    H(s->k_off, kd->offsets, (size_t)P * 24);
+    H(s->k_orient, kd->orientations, (size_t)P * 72);
+    H(s->k_lframe, kd->local_frames, (size_t)P * 72);
+    if (rc) return rc;
+    s->nc = C;
+    s->k_dx = kd->dx;
+    s->kin_device = true;
+    s->k_advance = kd->advance_first != 0;
+    return LBW_OK;
+}
+
+int lbw_alm_download_kinematics(lbw_domain* d, double* kin, double* spin, double* comp_state) {
+    LBW_REQ(d, "null domain");
+    LBW_REQ(alm_active(d), "no actuator points configured");
+    AlmState* s = d->alm;
+    LBW_CK(cudaSetDevice(d->device));
+    if (kin)
+        LBW_CK(cudaMemcpyAsync(kin, s->kin, (size_t)s->n * kKin * 8, cudaMemcpyDeviceToHost,
+                               d->stream));
+    if (spin && s->kin_device)
+        LBW_CK(cudaMemcpyAsync(spin, s->k_spin, (size_t)s->nc * 72, cudaMemcpyDeviceToHost,
+                               d->stream));
+    if (comp_state && s->kin_device)
+        LBW_CK(cudaMemcpyAsync(comp_state, s->k_cs, (size_t)s->nc * kCS * 8,
+                               cudaMemcpyDeviceToHost, d->stream));
+    LBW_CK(cudaStreamSynchronize(d->stream));
+    return LBW_OK;
+}
+
 int lbw_alm_set_kinematics(lbw_domain* d, const double* kin) {
     LBW_REQ(d && kin, "null argument");
     LBW_REQ(alm_active(d), "no actuator points configured");
     AlmState* s = d->alm;
+    LBW_REQ(!s->kin_device, "kinematics are computed on the device for this domain");
     LBW_CK(cudaSetDevice(d->device));
     const int slot = s->ring_pos;
     s->ring_pos = (s->ring_pos + 1) % kRing;
@@ -629,6 +947,10 @@ int lbw_alm_get(lbw_domain* d, double* rho, double* u, double* blade_force) {
         if (u)
             for (int c = 0; c < 3; ++c) u[p * 3 + c] = smp[p * 4 + 1 + c];
     }
+    if (err & 2) {
+        set_error("actuator point outside the non-periodic domain");
+        return LBW_EINVAL;
+    }
     if (err & 1) {
         set_error("density must be positive at an actuator point");
         return LBW_EINVAL;
@@ -638,13 +960,11 @@ int lbw_alm_get(lbw_domain* d, double* rho, double* u, double* blade_force) {
 
 int lbw_alm_clamp_flags(lbw_domain* d, int32_t* per_polar) {
     LBW_REQ(d && per_polar, "null argument");
-    if (!alm_active(d)) return LBW_OK;
+    if (!alm_active(d) || d->alm->n_polars == 0) return LBW_OK;
     LBW_CK(cudaSetDevice(d->device));
-    const int n = std::max(1, d->alm->n_polars);
     LBW_CK(cudaMemcpyAsync(per_polar, d->alm->clamp_flags, d->alm->n_polars * 4,
                            cudaMemcpyDeviceToHost, d->stream));
     LBW_CK(cudaStreamSynchronize(d->stream));
-    (void)n;
     return LBW_OK;
 }
 

@@ -33,7 +33,7 @@ from .roofline import RunTimer, lbm_kernel_cost, lightspeed, measure_mlups, perc
 from .turbine import DiskSpec, LineSpec
 
 _EX = np.array([1.0, 0.0, 0.0])
-KIN_COLS = 15
+KIN_COLS = 18   # lattice pos, velocity, e_chord, e_normal, e_span, position m
 
 
 class BlockDescriptor:
@@ -94,9 +94,9 @@ class ActuatorPoint:
         self.owner_block = -1
 
     def _k(self, a, b):
-        return self._sim._kin[self.global_id, a:b].copy()
+        return self._sim._kin_view()[self.global_id, a:b].copy()
 
-    position = property(lambda s: s._sim._pos_m[s.global_id].copy())
+    position = property(lambda s: s._k(15, 18))
     position_lat = property(lambda s: s._k(0, 3))
     velocity = property(lambda s: s._k(3, 6))
     e_chord = property(lambda s: s._k(6, 9))
@@ -109,9 +109,19 @@ class ActuatorPoint:
 
 
 class Simulation:
-    def __init__(self, cfg, rank=0, nranks=1, device=None):
+    """kinematics: "host" replays the reference's numpy kinematics exactly
+    and uploads them each step; "device" advances the turbine trees on the
+    GPU (no per-step host work or H2D).  Default: host for arithmetic
+    "exact" (bit-identical kinematics), device for "fast"."""
+
+    def __init__(self, cfg, rank=0, nranks=1, device=None, kinematics=None):
         self.cfg = cfg
         self.units = cfg.units
+        if kinematics is None:
+            kinematics = "device" if cfg.arithmetic == "fast" else "host"
+        if kinematics not in ("host", "device"):
+            raise ConfigError(f"kinematics must be host or device, got {kinematics!r}")
+        self.kinematics = kinematics
         lib = _lib.require_gpu()
         self.grid = SlabGrid(cfg.cells, cfg.periodicity, nranks, rank)
         desc = self.grid.blocks[0]
@@ -188,7 +198,11 @@ class Simulation:
         P = len(self.points)
         self._kin = np.zeros((P, KIN_COLS))
         self._pos_m = np.zeros((P, 3))
+        self._kin_stale = False
+        self._topo_pending = False
+        self._polar_list = []
         if P == 0:
+            self.kinematics = "host"
             return
         # static point data + concatenated polar tables -> device
         index_of = {pid: k for k, pid in enumerate(polar_ids)}
@@ -226,6 +240,94 @@ class Simulation:
         a.force_dt2 = self.units.force_dt2
         a.force_den = self.units.force_den
         _lib.check(_lib.load().lbw_alm_configure(self._domain, _lib.ctypes.byref(a)), "ALM")
+        self._kin_stale = False
+        self._topo_pending = False
+        if self.kinematics == "device":
+            self._configure_device_kinematics()
+
+    def _flat_components(self):
+        comps, parent = [], []
+        for topo in self.cfg.topologies:
+            base = len(comps)
+            index = {id(c): base + k for k, c in enumerate(topo.components)}
+            for c in topo.components:
+                comps.append(c)
+                parent.append(-1)
+            for c in topo.components:
+                for ch in c.children:
+                    parent[index[id(ch)]] = index[id(c)]
+        return comps, parent
+
+    def _configure_device_kinematics(self):
+        """Flatten the turbine trees for the device walk (lbw_kin_desc)."""
+        from .turbine import rotation_matrix
+        comps, parent = self._flat_components()
+        C, P = len(comps), len(self.points)
+        dt = self.units.dt
+        first = {id(comp): sl.start for comp, spec, sl in self._line_groups}
+        arr = {k: np.zeros(s) for k, s in (("rel_p", (C, 3)), ("rel_T", (C, 3, 3)),
+                                            ("axis", (C, 3)), ("rate", (C,)),
+                                            ("rstep", (C, 3, 3)), ("spin", (C, 3, 3)),
+                                            ("off", (P, 3)), ("orient", (P, 3, 3)),
+                                            ("lframe", (P, 3, 3)))}
+        line_first = np.full(C, -1, dtype=np.int32)
+        line_count = np.zeros(C, dtype=np.int32)
+        for c, comp in enumerate(comps):
+            arr["rel_p"][c] = comp.relative.p
+            arr["rel_T"][c] = comp.relative.T
+            arr["rate"][c] = comp.rate
+            arr["spin"][c] = comp.spin
+            arr["rstep"][c] = np.eye(3)
+            if comp.axis is not None:
+                arr["axis"][c] = comp.axis
+                if comp.rate != 0.0 and dt != 0.0:
+                    arr["rstep"][c] = rotation_matrix(comp.axis, comp.rate * dt)
+            if id(comp) in first:
+                spec = comp.discretization
+                g0 = first[id(comp)]
+                line_first[c], line_count[c] = g0, spec.n_points
+                arr["off"][g0:g0 + spec.n_points] = spec.offsets
+                arr["orient"][g0:g0 + spec.n_points] = spec.orientations
+                arr["lframe"][g0:g0 + spec.n_points] = spec.frames_local()
+        par = np.asarray(parent, dtype=np.int32)
+        self._kin_arrays = (arr, line_first, line_count, par)   # keep alive for the call
+        k = _lib.KinDesc()
+        k.n_components = C
+        k.parent = _lib.iptr(par)
+        k.rel_p, k.rel_T = _lib.dptr(arr["rel_p"]), _lib.dptr(arr["rel_T"])
+        k.axis, k.rate = _lib.dptr(arr["axis"]), _lib.dptr(arr["rate"])
+        k.step_rotation, k.spin = _lib.dptr(arr["rstep"]), _lib.dptr(arr["spin"])
+        k.line_first, k.line_count = _lib.iptr(line_first), _lib.iptr(line_count)
+        k.offsets, k.orientations = _lib.dptr(arr["off"]), _lib.dptr(arr["orient"])
+        k.local_frames = _lib.dptr(arr["lframe"])
+        k.dx = self.units.dx
+        k.advance_first = 0
+        _lib.check(_lib.load().lbw_alm_configure_kinematics(self._domain, _lib.ctypes.byref(k)),
+                   "kinematics")
+        self._flat = comps
+
+    def _kin_view(self):
+        """(P,15) kinematics of the latest step (downloaded in device mode)."""
+        if self.kinematics == "device" and self._kin_stale and len(self.points):
+            _lib.check(_lib.load().lbw_alm_download_kinematics(
+                self._domain, _lib.ptr(self._kin), None, None), "kinematics")
+            self._kin_stale = False
+        return self._kin
+
+    def sync_topologies(self):
+        """Bring the host turbine objects to the device state: spins from the
+        device, then the host walk advances them to t = step_index * dt, as
+        the reference's per-step advance would have."""
+        if self.kinematics != "device" or not self._topo_pending:
+            return
+        spin = np.zeros((len(self._flat), 3, 3))
+        _lib.check(_lib.load().lbw_alm_download_kinematics(self._domain, None, _lib.ptr(spin),
+                                                           None), "kinematics")
+        for c, comp in enumerate(self._flat):
+            comp.spin = spin[c].copy()
+        for topo in self.cfg.topologies:
+            topo.advance(self.units.dt)
+        self._topo_pending = False
 
     # ------------------------------------------------------- per step
     def refresh_points(self):
@@ -252,6 +354,7 @@ class Simulation:
                 raise ConfigError(
                     f"position component {lat[p, k]} outside the non-periodic domain")
             kin[:, 0:3] = lat
+            kin[:, 15:18] = self._pos_m
 
     def _alm_results(self):
         if self._results is None:
@@ -290,7 +393,8 @@ class Simulation:
     def step(self):
         lib = _lib.load()
         t = self.timer
-        if self.points:
+        host_kin = self.kinematics == "host"
+        if self.points and host_kin:
             t.start_phase("turbine")
             self.refresh_points()
             _lib.check(lib.lbw_alm_set_kinematics(self._domain, _lib.ptr(self._kin)), "ALM")
@@ -301,10 +405,14 @@ class Simulation:
         self._results = None
         self._poll(wait=False)
         if self.cfg.topologies:
-            t.start_phase("turbine")
-            for topo in self.cfg.topologies:
-                topo.advance(self.units.dt)
-            t.stop_phase()
+            if host_kin or not self.points:
+                t.start_phase("turbine")
+                for topo in self.cfg.topologies:
+                    topo.advance(self.units.dt)
+                t.stop_phase()
+            else:
+                self._kin_stale = True
+                self._topo_pending = True
         t.count_step()
         self.step_index += 1
         self._macro_fresh = False
@@ -313,6 +421,7 @@ class Simulation:
         _lib.check(_lib.load().lbw_domain_sync(self._domain), "sync")
         self._poll(wait=True)
         self._warn_clamps()
+        self.sync_topologies()
 
     # ---------------------------------------------------------- output
     def _recompute_moments(self):

@@ -215,16 +215,21 @@ def test_large_domain_properties(gpu):
 
 # ----------------------------------------------------------- actuator line
 
+@pytest.mark.parametrize("kinematics", ["host", "device"])
 @pytest.mark.parametrize("tag", ["periodic", "inflow"])
-def test_rotor_vs_reference(gpu, golden, tag):
+def test_rotor_vs_reference(gpu, golden, tag, kinematics):
     g = golden(f"rotor_{tag}.npz")
     cfg, tmp = rotor_config(cells=tuple(int(c) for c in g["cells"]),
                             periodic=tuple(bool(p) for p in g["periodicity"]),
                             boundary=str(g["boundary"]), position=tuple(g["position"]))
-    sim = Simulation(cfg)
+    sim = Simulation(cfg, kinematics=kinematics)
     for n in range(g["kin"].shape[0]):
         sim.step()
-        assert np.array_equal(sim._kin, g["kin"][n])
+        kin = sim._kin_view()[:, :15]
+        if kinematics == "host":
+            assert np.array_equal(kin, g["kin"][n])
+        else:
+            np.testing.assert_allclose(kin, g["kin"][n], rtol=1e-13, atol=1e-14)
         rho, u, blade = sim._alm_results()
         np.testing.assert_allclose(rho, g["samples"][n, :, 0], rtol=1e-12)
         np.testing.assert_allclose(u, g["samples"][n, :, 1:], rtol=1e-11, atol=1e-16)
@@ -234,6 +239,27 @@ def test_rotor_vs_reference(gpu, golden, tag):
                                atol=1e-18)
     sim.close()
     tmp.cleanup()
+
+
+def test_device_kinematics_long_run(gpu):
+    """600 steps of device kinematics stay on the host (reference-identical)
+    kinematics to 1e-12 m, and sync_topologies restores the host objects."""
+    cfgs = [rotor_config(cells=(12, 12, 12))[0] for _ in range(2)]
+    host_topo = cfgs[0].topologies[0]
+    sim = Simulation(cfgs[1], kinematics="device")
+    for n in range(600):
+        sim.step()
+        if n < 599:
+            host_topo.advance(cfgs[0].units.dt)
+    sim.synchronize()
+    # host topology advanced 599 times = state used by step 599; device's
+    # last kinematics are those of step 599
+    pos_host = host_topo.point_positions()
+    np.testing.assert_allclose(sim._kin_view()[:, 15:18], pos_host, rtol=0, atol=1e-12)
+    host_topo.advance(cfgs[0].units.dt)
+    np.testing.assert_allclose(cfgs[1].topologies[0].point_positions(),
+                               host_topo.point_positions(), rtol=0, atol=1e-12)
+    sim.close()
 
 
 def test_rotor_spreading_matches_oracle_bitwise_given_forces(gpu):
