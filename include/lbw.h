@@ -237,6 +237,9 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* desc);
 /* current device kinematics: kin (P,18) as in set_kinematics, spin
  * (C,3,3), per-component world state (C,49) — any may be NULL. */
 int lbw_alm_download_kinematics(lbw_domain* d, double* kin, double* spin, double* comp_state);
+/* step whose kinematics the device spin state represents (the next step's
+ * once its actuator chain has been queued ahead of time), or -1 */
+int64_t lbw_alm_kinematics_step(lbw_domain* d);
 /* kin: (P, 18) = lattice position (wrapped, sim.py:188-191), velocity m/s,
  * e_chord, e_normal, e_span (sim.py:176-181), position m.  Queued for the
  * next step. */

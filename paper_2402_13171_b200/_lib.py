@@ -139,6 +139,7 @@ SIGNATURES = {
     "lbw_alm_configure": (_I, [_VP, ctypes.POINTER(AlmDesc)]),
     "lbw_alm_configure_kinematics": (_I, [_VP, ctypes.POINTER(KinDesc)]),
     "lbw_alm_download_kinematics": (_I, [_VP, _VP, _VP, _VP]),
+    "lbw_alm_kinematics_step": (_I64, [_VP]),
     "lbw_alm_set_kinematics": (_I, [_VP, _VP]),
     "lbw_alm_get": (_I, [_VP, _VP, _VP, _VP]),
     "lbw_alm_clamp_flags": (_I, [_VP, _c_i32_p]),

@@ -89,8 +89,10 @@ struct AlmState {
     double *chord = nullptr, *elen = nullptr, *twist = nullptr;
     int32_t *polar_index = nullptr, *polar_offset = nullptr, *polar_rows = nullptr;
     double *p_alpha = nullptr, *p_cl = nullptr, *p_cd = nullptr;
-    double* kin = nullptr;
-    double *samples = nullptr, *blade = nullptr, *flat = nullptr;
+    double* kin = nullptr;       // (2,P,18): per step parity
+    double *samples = nullptr;   // (2,P,4)
+    double *blade = nullptr;     // (2,P,3)
+    double *flat = nullptr;      // (P,3)
     int32_t* dep_cell = nullptr;
     double* dep_w = nullptr;
     int32_t *clamp_flags = nullptr, *error_flags = nullptr;
@@ -99,9 +101,8 @@ struct AlmState {
     double* h_ring = nullptr;   // pinned (kRing, P, 18)
     cudaEvent_t ring_ev[kRing] = {};
     int ring_pos = 0;
-    bool kin_queued = false;
-    bool stepped = false;       // apply_outer_boundary has run at least once
-    int flip = 0;               // force set written by the next actuator step
+    int64_t kin_queued_step = -1;  // host kinematics uploaded for this step
+    int64_t ready_step = -1;       // step whose actuator chain is queued and valid
     size_t fill_smem = 0;
     // device kinematics
     bool kin_device = false;
@@ -112,10 +113,10 @@ struct AlmState {
     double *k_rstep = nullptr, *k_spin = nullptr, *k_off = nullptr, *k_orient = nullptr;
     double *k_lframe = nullptr, *k_cs = nullptr;
     double k_dx = 1.0;
-    bool k_advance = false;     // advance the tree before the next evaluation
+    int64_t kin_state_step = 0;  // step whose kinematics the device spins represent
     std::vector<void*> allocs;
 
-    AlmDev dev() const {
+    AlmDev dev(int parity) const {
         AlmDev a;
         a.n = n;
         a.chord = chord;
@@ -131,9 +132,9 @@ struct AlmState {
         a.rho_ref = rho_ref;
         a.dt2 = dt2;
         a.den = den;
-        a.kin = kin;
-        a.samples = samples;
-        a.blade = blade;
+        a.kin = kin + (size_t)parity * n * kKin;
+        a.samples = samples + (size_t)parity * n * 4;
+        a.blade = blade + (size_t)parity * n * 3;
         a.flat = flat;
         a.dep_cell = dep_cell;
         a.dep_w = dep_w;
@@ -240,27 +241,49 @@ __device__ double np_mod(double a, double b) {
     return m;
 }
 
-// KK: tree walk + point kinematics, one CTA
+// KK: tree walk + point kinematics, one CTA.  The component parameters and
+// state are staged in shared memory (the walk itself is one thread: a chain
+// of dependent 3x3 products down the tree); points are then evaluated in
+// parallel.  Layout per component in smem: params[kKP] then state[kCS].
+constexpr int kKP = 36;  // rel_p 3, rel_T 9, axis 3, rate 1, rstep 9, spin 9, parent 1, first 1
 __global__ void k_kinematics(KinDev k, AlmDev a, Geom g, int per_x, int advance) {
+    extern __shared__ double ksm[];
+    double* prm = ksm;                         // (nc, kKP)
+    double* cs = ksm + (size_t)k.nc * kKP;     // (nc, kCS)
+    for (int i = threadIdx.x; i < k.nc * kKP; i += blockDim.x) {
+        const int c = i / kKP, j = i % kKP;
+        double v;
+        if (j < 3) v = k.rel_p[c * 3 + j];
+        else if (j < 12) v = k.rel_T[c * 9 + j - 3];
+        else if (j < 15) v = k.axis[c * 3 + j - 12];
+        else if (j < 16) v = k.rate[c];
+        else if (j < 25) v = k.rstep[c * 9 + j - 16];
+        else if (j < 34) v = k.spin[c * 9 + j - 25];
+        else if (j < 35) v = (double)k.parent[c];
+        else v = (double)k.line_first[c];
+        prm[i] = v;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
+        const double I3[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+        const double zero3[3] = {0, 0, 0};
         for (int c = 0; c < k.nc; ++c) {
-            double* s = k.cs + (int64_t)c * kCS;
-            const int par = k.parent[c];
-            const double I3[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
-            const double zero3[3] = {0, 0, 0};
-            const double* Pp = par >= 0 ? k.cs + (int64_t)par * kCS + CS_P : zero3;
-            const double* PT = par >= 0 ? k.cs + (int64_t)par * kCS + CS_T : I3;
-            const double* Pv = par >= 0 ? k.cs + (int64_t)par * kCS + CS_V : zero3;
-            const double* Pw = par >= 0 ? k.cs + (int64_t)par * kCS + CS_W : zero3;
-            double* spin = k.spin + c * 9;
-            const double rate = k.rate[c];
+            double* q = prm + c * kKP;
+            double* s = cs + c * kCS;
+            const int par = (int)q[34];
+            const double* Pp = par >= 0 ? cs + par * kCS + CS_P : zero3;
+            const double* PT = par >= 0 ? cs + par * kCS + CS_T : I3;
+            const double* Pv = par >= 0 ? cs + par * kCS + CS_V : zero3;
+            const double* Pw = par >= 0 ? cs + par * kCS + CS_W : zero3;
+            double* spin = q + 25;
+            const double rate = q[15];
             if (advance && rate != 0.0) {
-                mm3(spin, k.rstep + c * 9, spin);
+                mm3(spin, q + 16, spin);
                 if (drifted(spin)) reorth(spin);
             }
             double Tp_rp[3], Tp_Tr[9];
-            mv3(PT, k.rel_p + c * 3, Tp_rp);
-            mm3(PT, k.rel_T + c * 9, Tp_Tr);
+            mv3(PT, q, Tp_rp);
+            mm3(PT, q + 3, Tp_Tr);
             for (int i = 0; i < 3; ++i) s[CS_P + i] = Pp[i] + Tp_rp[i];
             mm3(Tp_Tr, spin, s + CS_T);
             if (drifted(s + CS_T)) reorth(s + CS_T);
@@ -269,44 +292,49 @@ __global__ void k_kinematics(KinDev k, AlmDev a, Geom g, int per_x, int advance)
             for (int i = 0; i < 3; ++i) s[CS_V + i] = Pv[i] + cr[i];
             for (int i = 0; i < 3; ++i) s[CS_W + i] = Pw[i];
             if (par >= 0) {
-                const double* ps = k.cs + (int64_t)par * kCS;
-                for (int i = 0; i < 3; ++i) s[CS_AX + i] = ps[CS_AX + i];
-                s[CS_HAX] = ps[CS_HAX];
+                for (int i = 0; i < 3; ++i) s[CS_AX + i] = cs[par * kCS + CS_AX + i];
+                s[CS_HAX] = cs[par * kCS + CS_HAX];
             } else {
                 s[CS_AX] = s[CS_AX + 1] = s[CS_AX + 2] = 0.0;
                 s[CS_HAX] = 0.0;
             }
             if (rate != 0.0) {
-                mv3(Tp_Tr, k.axis + c * 3, s + CS_AX);
+                mv3(Tp_Tr, q + 12, s + CS_AX);
                 s[CS_HAX] = 1.0;
                 for (int i = 0; i < 3; ++i) s[CS_W + i] = s[CS_W + i] + s[CS_AX + i] * rate;
             }
             for (int i = 0; i < 9; ++i) s[CS_R + i] = spin[i];
-            const int first = k.line_first[c];
+            const int first = (int)q[35];
             if (first >= 0) {
                 const double* W = s + CS_T;
-                double Tp_o0[3], Tp_O0[9];
-                mv3(W, k.off + (int64_t)first * 3, Tp_o0);
+                double Tp_o0[3], Tp_O0[9], o0[3], O0[9];
+                for (int i = 0; i < 3; ++i) o0[i] = k.off[(int64_t)first * 3 + i];
+                for (int i = 0; i < 9; ++i) O0[i] = k.orient[(int64_t)first * 9 + i];
+                mv3(W, o0, Tp_o0);
                 for (int i = 0; i < 3; ++i) s[CS_SP + i] = s[CS_P + i] + Tp_o0[i];
-                mm3(W, k.orient + (int64_t)first * 9, Tp_O0);
+                mm3(W, O0, Tp_O0);
                 mm3(Tp_O0, spin, s + CS_ST);
                 cross3(s + CS_W, Tp_o0, cr);
                 for (int i = 0; i < 3; ++i) s[CS_VS + i] = s[CS_V + i] + cr[i];
                 for (int i = 0; i < 3; ++i) s[CS_WS + i] = s[CS_W + i];
                 if (rate != 0.0) {
                     double ax[3];
-                    mv3(Tp_O0, k.axis + c * 3, ax);
+                    mv3(Tp_O0, q + 12, ax);
                     for (int i = 0; i < 3; ++i) s[CS_WS + i] = s[CS_WS + i] + ax[i] * rate;
                 }
             }
         }
     }
     __syncthreads();
+    // persist spin + component state (downloadable), evaluate the points
+    for (int i = threadIdx.x; i < k.nc * 9; i += blockDim.x)
+        k.spin[i] = prm[(i / 9) * kKP + 25 + i % 9];
+    for (int i = threadIdx.x; i < k.nc * kCS; i += blockDim.x) k.cs[i] = cs[i];
     const int64_t dims[3] = {g.nxg, g.ny, g.nz};
     const int per[3] = {per_x, g.per_y, g.per_z};
     for (int p = threadIdx.x; p < a.n; p += blockDim.x) {
         const int c = k.point_comp[p];
-        const double* s = k.cs + (int64_t)c * kCS;
+        const double* s = cs + c * kCS;
         const int kk = p - k.line_first[c];
         double pos[3], fr[9], vel[3];
         if (kk == 0) {
@@ -541,35 +569,23 @@ __global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s) {
         deposit_axis(kin[k], L, per, dc + 3 * k, dw + 3 * k);
     }
     __syncwarp();
-    if (lane == 0) {
-        for (int i = 0; i < 3; ++i) {
-            const int32_t cxg = dc[i];
-            if (cxg < 0) continue;
-            const int64_t x = cxg - g.x0;
-            if (x < 0 || x >= g.nxl) continue;
-            for (int j = 0; j < 3; ++j) {
-                const int32_t cy = dc[3 + j];
-                if (cy < 0) continue;
-                const int64_t row = x * g.ny + cy;
-                if (atomicCAS(&s.row_slot[row], -1, -2) == -1) {
-                    const int32_t slot = atomicAdd(s.count, 1);
-                    s.slot_row[slot] = (int32_t)row;
-                    s.row_slot[row] = slot;
-                }
+    if (lane < 9) {  // one (x,y) row per lane
+        const int32_t cxg = dc[lane / 3], cy = dc[3 + lane % 3];
+        const int64_t x = (int64_t)cxg - g.x0;
+        if (cxg >= 0 && cy >= 0 && x >= 0 && x < g.nxl) {
+            const int64_t row = x * g.ny + cy;
+            if (atomicCAS(&s.row_slot[row], -1, -2) == -1) {
+                const int32_t slot = atomicAdd(s.count, 1);
+                s.slot_row[slot] = (int32_t)row;
+                s.row_slot[row] = slot;
             }
         }
     }
 }
 
-// K5: one CTA per used slot of set s; CTA 0 first clears set `old`.
-__global__ void k_alm_fill(AlmDev a, Geom g, ForceSet s, ForceSet old) {
+// K5: one CTA per used slot of set s.
+__global__ void k_alm_fill(AlmDev a, Geom g, ForceSet s) {
     extern __shared__ unsigned char smem[];
-    if (blockIdx.x == 0) {
-        const int32_t n = *old.count;
-        for (int32_t i = threadIdx.x; i < n; i += blockDim.x) old.row_slot[old.slot_row[i]] = -1;
-        __syncthreads();
-        if (threadIdx.x == 0) *old.count = 0;
-    }
     const int32_t slot = blockIdx.x;
     if (slot >= *s.count) return;
     const int32_t row = s.slot_row[slot];
@@ -664,43 +680,64 @@ void alm_destroy(lbw_domain* d) {
     d->alm = nullptr;
 }
 
-int alm_before_collide(lbw_domain* d, ForceView* fv_out) {
+bool alm_ready(const lbw_domain* d, int64_t m) { return d->alm->ready_step == m; }
+
+bool alm_can_prelaunch(const lbw_domain* d) { return d->prelaunch && d->alm->kin_device; }
+
+ForceView alm_force_view(const lbw_domain* d, int64_t m) { return d->alm->set[m & 1].view(); }
+
+int alm_invalidate(lbw_domain* d) {
+    if (!alm_active(d)) return LBW_OK;
+    LBW_CK(cudaStreamSynchronize(d->alm_stream));
+    d->alm->ready_step = -1;
+    return LBW_OK;
+}
+
+int alm_launch(lbw_domain* d, int64_t m) {
     AlmState* s = d->alm;
     const Geom& g = d->g;
-    const AlmDev a = s->dev();
+    cudaStream_t st = d->alm_stream;
+    const int par = (int)(m & 1);
+    const AlmDev a = s->dev(par);
     const int per_x = d->desc.periodic[0] ? 1 : 0;
+    ForceSet& fs = s->set[par];
+    // forget the rows of step m-2 (its sweep and the sampling of step m-1
+    // are ordered before this point by the caller's stream waits)
+    LBW_CK(cudaMemsetAsync(fs.row_slot, 0xff, (size_t)g.nxl * g.ny * sizeof(int32_t), st));
+    LBW_CK(cudaMemsetAsync(fs.count, 0, sizeof(int32_t), st));
     if (s->kin_device) {
-        k_kinematics<<<1, 256, 0, d->stream>>>(s->kdev(), a, g, per_x, s->k_advance ? 1 : 0);
+        if (m < s->kin_state_step || m > s->kin_state_step + 1) {
+            set_error("device kinematics can only advance one step at a time");
+            return LBW_ESTATE;
+        }
+        const size_t ksm = (size_t)s->nc * (kKP + kCS) * sizeof(double);
+        k_kinematics<<<1, 256, ksm, st>>>(s->kdev(), a, g, per_x, m > s->kin_state_step ? 1 : 0);
         count_launch();
         LBW_CK(cudaGetLastError());
-        s->k_advance = true;
-    } else if (!s->kin_queued) {
+        s->kin_state_step = m;
+    } else if (s->kin_queued_step != m) {
         set_error("actuator step without kinematics: call lbw_alm_set_kinematics first");
         return LBW_ESTATE;
     }
-    s->kin_queued = false;
-    MacroDev m{};
-    m.kind = d->msrc.kind;
-    for (int k = 0; k < 4; ++k) m.uniform[k] = d->msrc.uniform[k];
-    m.buf = d->buf[d->msrc.buf];
-    m.pull = d->msrc.pull ? 1 : 0;
-    m.fv = d->msrc.fv;
-    m.dense = d->macro_dense;
-    m.bc_set = s->stepped ? 1 : 0;
-    for (int k = 0; k < 3; ++k) m.u_in[k] = d->desc.u_in[k];
-    m.inflow = d->desc.boundary == LBW_BC_INFLOW_OUTFLOW ? 1 : 0;
-    m.per_x = per_x;
-    ForceSet& fs = s->set[s->flip];
-    ForceSet& old = s->set[s->flip ^ 1];
-    s->flip ^= 1;
+    MacroDev md{};
+    md.kind = d->msrc.kind;
+    for (int k = 0; k < 4; ++k) md.uniform[k] = d->msrc.uniform[k];
+    md.buf = d->buf[d->msrc.buf];
+    md.pull = d->msrc.pull ? 1 : 0;
+    md.fv = d->msrc.fv;
+    md.dense = d->macro_dense;
+    md.bc_set = d->steps_done > 0 ? 1 : 0;
+    for (int k = 0; k < 3; ++k) md.u_in[k] = d->desc.u_in[k];
+    md.inflow = d->desc.boundary == LBW_BC_INFLOW_OUTFLOW ? 1 : 0;
+    md.per_x = per_x;
     const int threads = 128;
     const unsigned blocks = (unsigned)((s->n * 32 + threads - 1) / threads);
-    k_alm_points<<<blocks, threads, 0, d->stream>>>(a, g, m, fs);
-    k_alm_fill<<<(unsigned)fs.cap, 128, s->fill_smem, d->stream>>>(a, g, fs, old);
+    k_alm_points<<<blocks, threads, 0, st>>>(a, g, md, fs);
+    k_alm_fill<<<(unsigned)fs.cap, 128, s->fill_smem, st>>>(a, g, fs);
     count_launch(2);
     LBW_CK(cudaGetLastError());
-    s->stepped = true;
-    *fv_out = fs.view();
+    LBW_CK(cudaEventRecord(d->ev_alm_done, st));
+    s->ready_step = m;
     return LBW_OK;
 }
 
@@ -716,6 +753,7 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     LBW_REQ(desc->n_polars >= 0, "n_polars must be >= 0");
     LBW_CK(cudaSetDevice(d->device));
     LBW_CK(cudaStreamSynchronize(d->stream));
+    LBW_CK(cudaStreamSynchronize(d->alm_stream));
     alm_destroy(d);
     const int P = desc->n_points;
     if (P == 0) return LBW_OK;
@@ -758,9 +796,9 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     A(&s->p_alpha, std::max<int64_t>(1, total_rows));
     A(&s->p_cl, std::max<int64_t>(1, total_rows));
     A(&s->p_cd, std::max<int64_t>(1, total_rows));
-    A(&s->kin, (size_t)P * kKin);
-    A(&s->samples, (size_t)P * 4);
-    A(&s->blade, (size_t)P * 3);
+    A(&s->kin, (size_t)2 * P * kKin);
+    A(&s->samples, (size_t)2 * P * 4);
+    A(&s->blade, (size_t)2 * P * 3);
     A(&s->flat, (size_t)P * 3);
     A(&s->dep_cell, (size_t)P * 9);
     A(&s->dep_w, (size_t)P * 9);
@@ -809,8 +847,9 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
         }
         if (cudaMemset(s->clamp_flags, 0, std::max(1, desc->n_polars) * 4) != cudaSuccess ||
             cudaMemset(s->error_flags, 0, 4) != cudaSuccess ||
-            cudaMemset(s->samples, 0, (size_t)P * 32) != cudaSuccess ||
-            cudaMemset(s->blade, 0, (size_t)P * 24) != cudaSuccess ||
+            cudaMemset(s->samples, 0, (size_t)2 * P * 32) != cudaSuccess ||
+            cudaMemset(s->blade, 0, (size_t)2 * P * 24) != cudaSuccess ||
+            cudaMemset(s->kin, 0, (size_t)2 * P * kKin * 8) != cudaSuccess ||
             cudaMallocHost(&s->h_ring, (size_t)kRing * P * kKin * 8) != cudaSuccess) {
             cudaGetLastError();
             set_error("ALM initialisation failed");
@@ -834,7 +873,7 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
     LBW_REQ(alm_active(d), "configure the actuator points first");
     AlmState* s = d->alm;
     const int C = kd->n_components, P = s->n;
-    LBW_REQ(C >= 1, "need at least one component");
+    LBW_REQ(C >= 1 && C <= 256, "need 1..256 turbine components");
     LBW_REQ(kd->dx > 0.0, "dx must be positive");
     for (int c = 0; c < C; ++c) {
         LBW_REQ(kd->parent[c] >= -1 && kd->parent[c] < c, "components must be in pre-order");
@@ -843,6 +882,7 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
     }
     LBW_CK(cudaSetDevice(d->device));
     LBW_CK(cudaStreamSynchronize(d->stream));
+    LBW_CK(cudaStreamSynchronize(d->alm_stream));
     std::vector<int32_t> point_comp(P, -1);
     for (int c = 0; c < C; ++c)
         for (int k = 0; k < kd->line_count[c]; ++k) point_comp[kd->line_first[c] + k] = c;
@@ -887,29 +927,45 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
     H(s->k_orient, kd->orientations, (size_t)P * 72);
     H(s->k_lframe, kd->local_frames, (size_t)P * 72);
     if (rc) return rc;
+    const size_t ksm = (size_t)C * (kKP + kCS) * sizeof(double);
+    if (ksm > 48 * 1024 &&
+        cudaFuncSetAttribute(k_kinematics, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)ksm) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("too many turbine components for the kinematics CTA");
+        return LBW_EINVAL;
+    }
     s->nc = C;
     s->k_dx = kd->dx;
     s->kin_device = true;
-    s->k_advance = kd->advance_first != 0;
+    s->kin_state_step = d->step - (kd->advance_first ? 1 : 0);
+    s->ready_step = -1;
     return LBW_OK;
 }
+
+// parity of the most recent step's actuator outputs
+static int last_parity(const lbw_domain* d) { return d->step > 0 ? (int)((d->step - 1) & 1) : 0; }
 
 int lbw_alm_download_kinematics(lbw_domain* d, double* kin, double* spin, double* comp_state) {
     LBW_REQ(d, "null domain");
     LBW_REQ(alm_active(d), "no actuator points configured");
     AlmState* s = d->alm;
     LBW_CK(cudaSetDevice(d->device));
-    if (kin)
-        LBW_CK(cudaMemcpyAsync(kin, s->kin, (size_t)s->n * kKin * 8, cudaMemcpyDeviceToHost,
-                               d->stream));
-    if (spin && s->kin_device)
-        LBW_CK(cudaMemcpyAsync(spin, s->k_spin, (size_t)s->nc * 72, cudaMemcpyDeviceToHost,
-                               d->stream));
-    if (comp_state && s->kin_device)
-        LBW_CK(cudaMemcpyAsync(comp_state, s->k_cs, (size_t)s->nc * kCS * 8,
-                               cudaMemcpyDeviceToHost, d->stream));
     LBW_CK(cudaStreamSynchronize(d->stream));
+    LBW_CK(cudaStreamSynchronize(d->alm_stream));
+    if (kin)
+        LBW_CK(cudaMemcpy(kin, s->kin + (size_t)last_parity(d) * s->n * kKin,
+                          (size_t)s->n * kKin * 8, cudaMemcpyDeviceToHost));
+    if (spin && s->kin_device)
+        LBW_CK(cudaMemcpy(spin, s->k_spin, (size_t)s->nc * 72, cudaMemcpyDeviceToHost));
+    if (comp_state && s->kin_device)
+        LBW_CK(cudaMemcpy(comp_state, s->k_cs, (size_t)s->nc * kCS * 8, cudaMemcpyDeviceToHost));
     return LBW_OK;
+}
+
+int64_t lbw_alm_kinematics_step(lbw_domain* d) {
+    if (!d || !alm_active(d) || !d->alm->kin_device) return -1;
+    return d->alm->kin_state_step;
 }
 
 int lbw_alm_set_kinematics(lbw_domain* d, const double* kin) {
@@ -923,9 +979,12 @@ int lbw_alm_set_kinematics(lbw_domain* d, const double* kin) {
     LBW_CK(cudaEventSynchronize(s->ring_ev[slot]));
     double* h = s->h_ring + (size_t)slot * s->n * kKin;
     std::memcpy(h, kin, (size_t)s->n * kKin * 8);
-    LBW_CK(cudaMemcpyAsync(s->kin, h, (size_t)s->n * kKin * 8, cudaMemcpyHostToDevice, d->stream));
-    LBW_CK(cudaEventRecord(s->ring_ev[slot], d->stream));
-    s->kin_queued = true;
+    const int64_t m = d->step;
+    LBW_CK(cudaMemcpyAsync(s->kin + (size_t)(m & 1) * s->n * kKin, h, (size_t)s->n * kKin * 8,
+                           cudaMemcpyHostToDevice, d->alm_stream));
+    LBW_CK(cudaEventRecord(s->ring_ev[slot], d->alm_stream));
+    s->kin_queued_step = m;
+    s->ready_step = -1;
     return LBW_OK;
 }
 
@@ -934,14 +993,16 @@ int lbw_alm_get(lbw_domain* d, double* rho, double* u, double* blade_force) {
     LBW_REQ(alm_active(d), "no actuator points configured");
     AlmState* s = d->alm;
     LBW_CK(cudaSetDevice(d->device));
-    std::vector<double> smp((size_t)s->n * 4);
-    LBW_CK(cudaMemcpyAsync(smp.data(), s->samples, smp.size() * 8, cudaMemcpyDeviceToHost, d->stream));
-    if (blade_force)
-        LBW_CK(cudaMemcpyAsync(blade_force, s->blade, (size_t)s->n * 24, cudaMemcpyDeviceToHost,
-                               d->stream));
-    int32_t err = 0;
-    LBW_CK(cudaMemcpyAsync(&err, s->error_flags, 4, cudaMemcpyDeviceToHost, d->stream));
     LBW_CK(cudaStreamSynchronize(d->stream));
+    const int par = last_parity(d);
+    std::vector<double> smp((size_t)s->n * 4);
+    LBW_CK(cudaMemcpy(smp.data(), s->samples + (size_t)par * s->n * 4, smp.size() * 8,
+                      cudaMemcpyDeviceToHost));
+    if (blade_force)
+        LBW_CK(cudaMemcpy(blade_force, s->blade + (size_t)par * s->n * 3, (size_t)s->n * 24,
+                          cudaMemcpyDeviceToHost));
+    int32_t err = 0;
+    LBW_CK(cudaMemcpy(&err, s->error_flags, 4, cudaMemcpyDeviceToHost));
     for (int p = 0; p < s->n; ++p) {
         if (rho) rho[p] = smp[p * 4];
         if (u)
@@ -962,9 +1023,9 @@ int lbw_alm_clamp_flags(lbw_domain* d, int32_t* per_polar) {
     LBW_REQ(d && per_polar, "null argument");
     if (!alm_active(d) || d->alm->n_polars == 0) return LBW_OK;
     LBW_CK(cudaSetDevice(d->device));
-    LBW_CK(cudaMemcpyAsync(per_polar, d->alm->clamp_flags, d->alm->n_polars * 4,
-                           cudaMemcpyDeviceToHost, d->stream));
     LBW_CK(cudaStreamSynchronize(d->stream));
+    LBW_CK(cudaMemcpy(per_polar, d->alm->clamp_flags, d->alm->n_polars * 4,
+                      cudaMemcpyDeviceToHost));
     return LBW_OK;
 }
 

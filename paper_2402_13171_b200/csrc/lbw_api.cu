@@ -192,6 +192,7 @@ static void free_domain(lbw_domain* d) {
     if (!d) return;
     cudaSetDevice(d->device);
     if (d->stream) cudaStreamSynchronize(d->stream);
+    if (d->alm_stream) cudaStreamSynchronize(d->alm_stream);
     alm_destroy(d);
     for (void* p : d->peer_mapped) cudaIpcCloseMemHandle(p);
     for (double*& b : d->buf)
@@ -204,6 +205,9 @@ static void free_domain(lbw_domain* d) {
     if (d->nan_event) cudaEventDestroy(d->nan_event);
     if (d->stage) cudaFree(d->stage);
     for (cudaEvent_t ev : d->ev_pool) cudaEventDestroy(ev);
+    for (cudaEvent_t ev : {d->ev_main, d->ev_alm_done, d->ev_sweep[0], d->ev_sweep[1]})
+        if (ev) cudaEventDestroy(ev);
+    if (d->alm_stream) cudaStreamDestroy(d->alm_stream);
     if (d->stream) cudaStreamDestroy(d->stream);
     delete d;
 }
@@ -279,10 +283,15 @@ int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out) {
 
     int rc = LBW_OK;
     const size_t buf_bytes = (size_t)(g.nxl + 2) * g.plane_stride * sizeof(double);
-    if (cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    if (cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&d->alm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d->ev_main, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d->ev_alm_done, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d->ev_sweep[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d->ev_sweep[1], cudaEventDisableTiming) != cudaSuccess) {
         cudaGetLastError();
         free_domain(d);
-        set_error("cudaStreamCreate failed");
+        set_error("stream/event creation failed");
         return LBW_ECUDA;
     }
     for (int b = 0; b < 2 && rc == LBW_OK; ++b) rc = alloc_dev(d, (void**)&d->buf[b], buf_bytes);
@@ -346,6 +355,10 @@ static int freeze_macro_if(lbw_domain* d, bool touches_buf_cur, bool touches_use
 int lbw_domain_upload_pdf(lbw_domain* d, const double* f_aos) {
     LBW_REQ(d && f_aos, "null argument");
     LBW_CK(cudaSetDevice(d->device));
+    {
+        int rc_ = alm_invalidate(d);
+        if (rc_) return rc_;
+    }
     const size_t bytes = interior_cells(d) * 27 * sizeof(double);
     int rc = ensure_stage(d, bytes);
     if (rc) return rc;
@@ -361,6 +374,10 @@ int lbw_domain_upload_pdf(lbw_domain* d, const double* f_aos) {
 int lbw_domain_upload_pdf_device(lbw_domain* d, const double* f_aos_dev) {
     LBW_REQ(d && f_aos_dev, "null argument");
     LBW_CK(cudaSetDevice(d->device));
+    {
+        int rc_ = alm_invalidate(d);
+        if (rc_) return rc_;
+    }
     int rc = freeze_macro_if(d, true, false);
     if (rc) return rc;
     LBW_CK(launch_aos_to_soa(f_aos_dev, d->buf[d->cur], d->g, d->stream));
@@ -384,6 +401,10 @@ int lbw_domain_download_pdf(lbw_domain* d, double* f_aos) {
 int lbw_domain_set_force(lbw_domain* d, const double* force_aos) {
     LBW_REQ(d, "null domain");
     LBW_CK(cudaSetDevice(d->device));
+    {
+        int rc_ = alm_invalidate(d);
+        if (rc_) return rc_;
+    }
     int rc = freeze_macro_if(d, false, true);
     if (rc) return rc;
     if (!force_aos) {
@@ -424,6 +445,10 @@ int lbw_domain_download_force(lbw_domain* d, double* force_aos) {
 int lbw_domain_set_macro(lbw_domain* d, const double* macro_aos, const double* uniform4) {
     LBW_REQ(d, "null domain");
     LBW_CK(cudaSetDevice(d->device));
+    {
+        int rc_ = alm_invalidate(d);
+        if (rc_) return rc_;
+    }
     if (uniform4) {
         d->msrc.kind = MS_UNIFORM;
         for (int k = 0; k < 4; ++k) d->msrc.uniform[k] = uniform4[k];
@@ -467,6 +492,10 @@ int lbw_domain_download_macro(lbw_domain* d, double* macro_aos) {
 int lbw_domain_recompute_moments(lbw_domain* d, double* macro_aos) {
     LBW_REQ(d, "null domain");
     LBW_CK(cudaSetDevice(d->device));
+    {
+        int rc_ = alm_invalidate(d);
+        if (rc_) return rc_;
+    }
     const size_t bytes = interior_cells(d) * 4 * sizeof(double);
     int rc = ensure_stage(d, bytes);
     if (rc) return rc;
@@ -491,8 +520,17 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
     for (int32_t s = 0; s < nsteps; ++s) {
         ForceView fv = d->user_active ? d->user.view() : ForceView{nullptr, nullptr};
         if (alm_active(d)) {
-            int rc = alm_before_collide(d, &fv);
-            if (rc) return rc;
+            // The actuator chain of this step normally was queued on the
+            // actuator stream while the previous sweep ran; otherwise queue
+            // it now behind everything already on the main stream.
+            if (!alm_ready(d, d->step)) {
+                LBW_CK(cudaEventRecord(d->ev_main, d->stream));
+                LBW_CK(cudaStreamWaitEvent(d->alm_stream, d->ev_main, 0));
+                int rc = alm_launch(d, d->step);
+                if (rc) return rc;
+            }
+            LBW_CK(cudaStreamWaitEvent(d->stream, d->ev_alm_done, 0));
+            fv = alm_force_view(d, d->step);
         }
         SweepArgs a;
         a.src = d->buf[d->cur];
@@ -529,9 +567,20 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
         d->msrc.fv = fv;
         d->last_fv = fv;
         d->shown_fv = fv;
+        LBW_CK(cudaEventRecord(d->ev_sweep[d->step & 1], d->stream));
         d->cur = 1 - d->cur;
         d->state_pre = false;
         d->step += 1;
+        d->steps_done += 1;
+        // Queue the next step's actuator chain now: it reads only this
+        // sweep's source buffer and force set (both read-only during the
+        // sweep) and rewrites the force set of the sweep before, so it
+        // waits for that one and then overlaps this sweep.
+        if (alm_active(d) && alm_can_prelaunch(d)) {
+            LBW_CK(cudaStreamWaitEvent(d->alm_stream, d->ev_sweep[(d->step - 2) & 1], 0));
+            int rc = alm_launch(d, d->step);
+            if (rc) return rc;
+        }
     }
     if (nsteps > 0) {
         LBW_CK(cudaMemcpyAsync(d->h_nan, d->d_nan, sizeof(unsigned long long),
@@ -545,6 +594,11 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
 int64_t lbw_domain_step_index(lbw_domain* d) { return d ? d->step : -1; }
 int lbw_domain_set_step_index(lbw_domain* d, int64_t step) {
     LBW_REQ(d && step >= 0, "bad argument");
+    LBW_CK(cudaSetDevice(d->device));
+    int rc = alm_invalidate(d);
+    if (rc) return rc;
+    LBW_REQ(!alm_active(d) || step == d->step,
+            "the step index of a domain with actuator points cannot be changed");
     d->step = step;
     return LBW_OK;
 }
@@ -582,6 +636,7 @@ int lbw_domain_sync(lbw_domain* d) {
     LBW_REQ(d, "null domain");
     LBW_CK(cudaSetDevice(d->device));
     LBW_CK(cudaStreamSynchronize(d->stream));
+    LBW_CK(cudaStreamSynchronize(d->alm_stream));
     return LBW_OK;
 }
 

@@ -79,6 +79,12 @@ struct lbw_domain {
     size_t stage_bytes = 0;
     int64_t bytes = 0;
     lbw::AlmState* alm = nullptr;
+    // actuator work runs on its own stream so the next step's sampling /
+    // forces / spreading overlap the current sweep (see lbw_domain_step)
+    cudaStream_t alm_stream = nullptr;
+    cudaEvent_t ev_main = nullptr, ev_alm_done = nullptr, ev_sweep[2] = {nullptr, nullptr};
+    int64_t steps_done = 0;   // sweeps executed in this domain's lifetime
+    bool prelaunch = true;
     // optional sweep timing (lbw_domain_sweep_timing)
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -90,7 +96,16 @@ struct lbw_domain {
 
 namespace lbw {
 // lbw_alm.cu
-int alm_before_collide(lbw_domain* d, ForceView* fv_out);
+// Launch the actuator chain of step m on d->alm_stream (clear set m&1,
+// kinematics, sample/force/mark, fill); records d->ev_alm_done.
+int alm_launch(lbw_domain* d, int64_t m);
+// Step m's chain already queued and still valid?
+bool alm_ready(const lbw_domain* d, int64_t m);
+bool alm_can_prelaunch(const lbw_domain* d);
+ForceView alm_force_view(const lbw_domain* d, int64_t m);
+// Wait for queued actuator work and forget any prelaunched step (the
+// caller is about to change state it reads).
+int alm_invalidate(lbw_domain* d);
 void alm_destroy(lbw_domain* d);
 bool alm_active(const lbw_domain* d);
 int ensure_stage(lbw_domain* d, size_t bytes);

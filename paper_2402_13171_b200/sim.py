@@ -320,13 +320,15 @@ class Simulation:
         the reference's per-step advance would have."""
         if self.kinematics != "device" or not self._topo_pending:
             return
+        lib = _lib.load()
         spin = np.zeros((len(self._flat), 3, 3))
-        _lib.check(_lib.load().lbw_alm_download_kinematics(self._domain, None, _lib.ptr(spin),
-                                                           None), "kinematics")
+        _lib.check(lib.lbw_alm_download_kinematics(self._domain, None, _lib.ptr(spin), None),
+                   "kinematics")
+        behind = self.step_index - int(lib.lbw_alm_kinematics_step(self._domain))
         for c, comp in enumerate(self._flat):
             comp.spin = spin[c].copy()
         for topo in self.cfg.topologies:
-            topo.advance(self.units.dt)
+            topo.advance(self.units.dt if behind > 0 else 0.0)
         self._topo_pending = False
 
     # ------------------------------------------------------- per step

@@ -262,6 +262,34 @@ def test_device_kinematics_long_run(gpu):
     sim.close()
 
 
+def test_prelaunched_actuator_chain_survives_state_changes(gpu):
+    """Device kinematics queue step n+1's actuator chain during sweep n.
+    Mutating the state between steps (moments recompute, new populations)
+    must invalidate it: the run must track a run without prelaunch."""
+    sims = []
+    for kin in ("host", "device"):
+        cfg, tmp = rotor_config(cells=(16, 12, 12))
+        sims.append((Simulation(cfg, kinematics=kin), tmp))
+    rng = np.random.default_rng(5)
+    bump = 1.0 + 1e-3 * rng.uniform(-1, 1, (16, 12, 12, 27))
+    for sim, _ in sims:
+        for _ in range(3):
+            sim.step()
+        sim._recompute_moments()
+        for _ in range(2):
+            sim.step()
+        sim.fields[0].interior = sim.fields[0].interior * bump
+        for _ in range(3):
+            sim.step()
+    (a, ta), (b, tb) = sims
+    np.testing.assert_allclose(b.fields[0].interior, a.fields[0].interior, rtol=0, atol=1e-13)
+    np.testing.assert_allclose(b._alm_results()[2], a._alm_results()[2], rtol=1e-10,
+                               atol=1e-12)
+    for sim, tmp in sims:
+        sim.close()
+        tmp.cleanup()
+
+
 def test_rotor_spreading_matches_oracle_bitwise_given_forces(gpu):
     """With identical point forces the deposit is bit-identical: compare the
     device force field against the oracle fed the device's blade forces."""
