@@ -251,6 +251,20 @@ int lbw_alm_get(lbw_domain* d, double* rho, double* u, double* blade_force);
 /* 1 once any polar lookup clamped alpha (polars.py:68-77 warn-once). */
 int lbw_alm_clamp_flags(lbw_domain* d, int32_t* per_polar);
 
+/* ---------------------------------------------------------------- multi-GPU
+ * x-slab neighbours on other GPUs of the node (one process per GPU).  Each
+ * domain exports an opaque blob (CUDA IPC handles of its population
+ * buffers, actuator cube buffer and ordering flags); every rank imports its
+ * x neighbours' blobs (NULL where the slab touches a non-periodic face).
+ * lbw_domain_step then stores the nine outgoing direction planes of each
+ * edge plane straight into the neighbour's ghost plane from inside the
+ * sweep kernel, and orders steps with GPU-side waits on counters the
+ * neighbours write — no host synchronisation per step.  Configure the
+ * actuator points (lbw_alm_configure) before exporting. */
+int64_t lbw_peer_blob_bytes(void);
+int lbw_domain_export_handle(lbw_domain* d, void* blob, int64_t* blob_bytes);
+int lbw_domain_import_peers(lbw_domain* d, const void* lo_blob, const void* hi_blob);
+
 #ifdef __cplusplus
 }
 #endif

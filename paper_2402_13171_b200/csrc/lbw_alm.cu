@@ -93,6 +93,7 @@ struct AlmState {
     double *samples = nullptr;   // (2,P,4)
     double *blade = nullptr;     // (2,P,3)
     double *flat = nullptr;      // (P,3)
+    double* cube = nullptr;      // (2,P,8,4) sampled cube values (multi-slab runs)
     int32_t* dep_cell = nullptr;
     double* dep_w = nullptr;
     int32_t *clamp_flags = nullptr, *error_flags = nullptr;
@@ -364,9 +365,11 @@ __global__ void k_kinematics(KinDev k, AlmDev a, Geom g, int per_x, int advance)
 }
 
 // Macro (rho, u) of global cell (gx,gy,gz), following the ghost semantics
-// of PdfField.macro (fields.py:35-36, halo.py:144-160).  Returns false when
-// the cell belongs to another slab.
-__device__ bool macro_at(const Geom& g, const MacroDev& m, int64_t gx, int64_t gy, int64_t gz,
+// of PdfField.macro (fields.py:35-36, halo.py:144-160).  Returns MA_REMOTE
+// (nothing written) when the cell belongs to another slab, MA_OWNED for a
+// cell of this slab, MA_CONST for a ghost value every slab knows.
+enum { MA_REMOTE = 0, MA_OWNED = 1, MA_CONST = 2 };
+__device__ int macro_at(const Geom& g, const MacroDev& m, int64_t gx, int64_t gy, int64_t gz,
                          double out[4]) {
     const double ghost0[4] = {1.0, 0.0, 0.0, 0.0};
     auto put = [&](const double* v) {
@@ -384,32 +387,32 @@ __device__ bool macro_at(const Geom& g, const MacroDev& m, int64_t gx, int64_t g
             } else {
                 put(ghost0);
             }
-            return true;
+            return MA_CONST;
         } else if (m.inflow && gx >= g.nxg && m.bc_set) {
             gx = g.nxg - 1;
         } else {
             put(ghost0);
-            return true;
+            return MA_CONST;
         }
     }
     if (gy < 0 || gy >= g.ny) {
-        if (!g.per_y) { put(ghost0); return true; }
+        if (!g.per_y) { put(ghost0); return MA_CONST; }
         gy = gy < 0 ? gy + g.ny : gy - g.ny;
     }
     if (gz < 0 || gz >= g.nz) {
-        if (!g.per_z) { put(ghost0); return true; }
+        if (!g.per_z) { put(ghost0); return MA_CONST; }
         gz = gz < 0 ? gz + g.nz : gz - g.nz;
     }
     const int64_t x = gx - g.x0;
-    if (x < 0 || x >= g.nxl) return false;
+    if (x < 0 || x >= g.nxl) return MA_REMOTE;
     if (m.kind == MS_UNIFORM) {
         put(m.uniform);
-        return true;
+        return MA_OWNED;
     }
     const int64_t cell = (x * g.ny + gy) * g.nz + gz;
     if (m.kind == MS_DENSE) {
         put(m.dense + cell * 4);
-        return true;
+        return MA_OWNED;
     }
     double f[27];
     if (m.pull) load_cell<true>(m.buf, g, (int)x, (int)gy, (int)gz, f);
@@ -421,7 +424,7 @@ __device__ bool macro_at(const Geom& g, const MacroDev& m, int64_t gx, int64_t g
     out[1] = mm.ux;
     out[2] = mm.uy;
     out[3] = mm.uz;
-    return true;
+    return MA_OWNED;
 }
 
 __device__ __forceinline__ double dot3(const double* a, const double* b) {
@@ -526,7 +529,16 @@ __device__ void deposit_axis(double x, int64_t L, int periodic, int32_t* dc, dou
 }
 
 // K4: one warp per point
-__global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s) {
+// phase 0: single slab, everything in one pass.  Multi-slab: phase 1 only
+// computes the cube values of this slab's cells and stores them into the
+// local and both neighbours' cube buffers; phase 2 (after the neighbours'
+// stores are visible) continues from the cube buffer.
+struct CubeArgs {
+    double* local;   // (P,8,4) of this step's parity
+    double* peer[2];
+};
+
+__global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s, int phase, CubeArgs cube) {
     const int p = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (p >= a.n) return;  // uniform per warp
@@ -539,8 +551,23 @@ __global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s) {
         t[k] = kin[k] - 0.5 - fl;
     }
     double v[4] = {0.0, 0.0, 0.0, 0.0};
-    if (lane < 8)
-        macro_at(g, m, j0[0] + ((lane >> 2) & 1), j0[1] + ((lane >> 1) & 1), j0[2] + (lane & 1), v);
+    if (phase == 2) {
+        if (lane < 8)
+            for (int q = 0; q < 4; ++q) v[q] = cube.local[((int64_t)p * 8 + lane) * 4 + q];
+    } else if (lane < 8) {
+        const int code = macro_at(g, m, j0[0] + ((lane >> 2) & 1), j0[1] + ((lane >> 1) & 1),
+                                  j0[2] + (lane & 1), v);
+        if (phase == 1) {
+            const int64_t o = ((int64_t)p * 8 + lane) * 4;
+            if (code != MA_REMOTE)
+                for (int q = 0; q < 4; ++q) cube.local[o + q] = v[q];
+            if (code == MA_OWNED)
+                for (int side = 0; side < 2; ++side)
+                    if (cube.peer[side])
+                        for (int q = 0; q < 4; ++q) cube.peer[side][o + q] = v[q];
+        }
+    }
+    if (phase == 1) return;
     // lane 0: trilinear sum in (dx,dy,dz) lexicographic order (actuator.py:88-92)
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int c = 0; c < 8; ++c) {
@@ -555,11 +582,14 @@ __global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s) {
     int32_t* dc = a.dep_cell + (int64_t)p * 9;
     double* dw = a.dep_w + (int64_t)p * 9;
     if (lane == 0) {
-        for (int q = 0; q < 4; ++q) a.samples[p * 4 + q] = acc[q];
         double blade[3];
         blade_force(a, p, kin, acc, blade);
+        // per-point outputs are reported by the slab owning floor(x)
+        const int64_t ox = (int64_t)floor(kin[0]) - g.x0;
+        const bool owner = phase == 0 || (ox >= 0 && ox < g.nxl);
+        for (int q = 0; q < 4; ++q) a.samples[p * 4 + q] = owner ? acc[q] : 0.0;
         for (int c = 0; c < 3; ++c) {
-            a.blade[p * 3 + c] = blade[c];
+            a.blade[p * 3 + c] = owner ? blade[c] : 0.0;
             a.flat[p * 3 + c] = -blade[c] * a.dt2 / a.den;  // units.py:69
         }
     } else if (lane >= 1 && lane <= 3) {
@@ -669,6 +699,8 @@ int dev_alloc(lbw_domain* d, AlmState* s, T** p, size_t count) {
 
 bool alm_active(const lbw_domain* d) { return d->alm != nullptr && d->alm->n > 0; }
 
+double* alm_cube(const lbw_domain* d) { return alm_active(d) ? d->alm->cube : nullptr; }
+
 void alm_destroy(lbw_domain* d) {
     AlmState* s = d->alm;
     if (!s) return;
@@ -732,7 +764,24 @@ int alm_launch(lbw_domain* d, int64_t m) {
     md.per_x = per_x;
     const int threads = 128;
     const unsigned blocks = (unsigned)((s->n * 32 + threads - 1) / threads);
-    k_alm_points<<<blocks, threads, 0, st>>>(a, g, md, fs);
+    CubeArgs cube{};
+    if (d->linked) {
+        const size_t off = (size_t)par * s->n * 32;
+        cube.local = s->cube + off;
+        for (int side = 0; side < 2; ++side)
+            cube.peer[side] = d->nb_cube[side] ? d->nb_cube[side] + off : nullptr;
+        k_alm_points<<<blocks, threads, 0, st>>>(a, g, md, fs, 1, cube);
+        count_launch();
+        LBW_CK(cudaGetLastError());
+        const uint32_t epoch = (uint32_t)(d->alm_launches + 1);
+        int rc = peer_signal(d, st, 1, epoch);
+        if (!rc) rc = peer_wait(d, st, 1, epoch);
+        if (rc) return rc;
+        k_alm_points<<<blocks, threads, 0, st>>>(a, g, md, fs, 2, cube);
+    } else {
+        k_alm_points<<<blocks, threads, 0, st>>>(a, g, md, fs, 0, cube);
+    }
+    d->alm_launches += 1;
     k_alm_fill<<<(unsigned)fs.cap, 128, s->fill_smem, st>>>(a, g, fs);
     count_launch(2);
     LBW_CK(cudaGetLastError());
@@ -800,6 +849,7 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     A(&s->samples, (size_t)2 * P * 4);
     A(&s->blade, (size_t)2 * P * 3);
     A(&s->flat, (size_t)P * 3);
+    A(&s->cube, (size_t)2 * P * 32);
     A(&s->dep_cell, (size_t)P * 9);
     A(&s->dep_w, (size_t)P * 9);
     A(&s->clamp_flags, std::max(1, desc->n_polars));

@@ -194,7 +194,6 @@ static void free_domain(lbw_domain* d) {
     if (d->stream) cudaStreamSynchronize(d->stream);
     if (d->alm_stream) cudaStreamSynchronize(d->alm_stream);
     alm_destroy(d);
-    for (void* p : d->peer_mapped) cudaIpcCloseMemHandle(p);
     for (double*& b : d->buf)
         if (b) cudaFree(b);
     if (d->user.row_slot) cudaFree(d->user.row_slot);
@@ -205,7 +204,8 @@ static void free_domain(lbw_domain* d) {
     if (d->nan_event) cudaEventDestroy(d->nan_event);
     if (d->stage) cudaFree(d->stage);
     for (cudaEvent_t ev : d->ev_pool) cudaEventDestroy(ev);
-    for (cudaEvent_t ev : {d->ev_main, d->ev_alm_done, d->ev_sweep[0], d->ev_sweep[1]})
+    peer_close(d);
+    for (cudaEvent_t ev : {d->ev_main, d->ev_ready, d->ev_alm_done, d->ev_sweep[0], d->ev_sweep[1]})
         if (ev) cudaEventDestroy(ev);
     if (d->alm_stream) cudaStreamDestroy(d->alm_stream);
     if (d->stream) cudaStreamDestroy(d->stream);
@@ -286,6 +286,7 @@ int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out) {
     if (cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&d->alm_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&d->ev_main, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&d->ev_alm_done, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&d->ev_sweep[0], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&d->ev_sweep[1], cudaEventDisableTiming) != cudaSuccess) {
@@ -388,6 +389,10 @@ int lbw_domain_upload_pdf_device(lbw_domain* d, const double* f_aos_dev) {
 int lbw_domain_download_pdf(lbw_domain* d, double* f_aos) {
     LBW_REQ(d && f_aos, "null argument");
     LBW_CK(cudaSetDevice(d->device));
+    {
+        int rc_ = peer_wait(d, d->stream, 0, (uint32_t)d->steps_done);
+        if (rc_) return rc_;
+    }
     const size_t bytes = interior_cells(d) * 27 * sizeof(double);
     int rc = ensure_stage(d, bytes);
     if (rc) return rc;
@@ -469,6 +474,10 @@ int lbw_domain_set_macro(lbw_domain* d, const double* macro_aos, const double* u
 int lbw_domain_download_macro(lbw_domain* d, double* macro_aos) {
     LBW_REQ(d && macro_aos, "null argument");
     LBW_CK(cudaSetDevice(d->device));
+    {
+        int rc_ = peer_wait(d, d->stream, 0, (uint32_t)d->steps_done);
+        if (rc_) return rc_;
+    }
     const size_t n = interior_cells(d);
     if (d->msrc.kind == MS_UNIFORM) {
         for (size_t c = 0; c < n; ++c)
@@ -496,6 +505,10 @@ int lbw_domain_recompute_moments(lbw_domain* d, double* macro_aos) {
         int rc_ = alm_invalidate(d);
         if (rc_) return rc_;
     }
+    {
+        int rc_ = peer_wait(d, d->stream, 0, (uint32_t)d->steps_done);
+        if (rc_) return rc_;
+    }
     const size_t bytes = interior_cells(d) * 4 * sizeof(double);
     int rc = ensure_stage(d, bytes);
     if (rc) return rc;
@@ -519,6 +532,13 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
     LBW_CK(cudaSetDevice(d->device));
     for (int32_t s = 0; s < nsteps; ++s) {
         ForceView fv = d->user_active ? d->user.view() : ForceView{nullptr, nullptr};
+        // neighbours must have finished the previous sweep: it filled our
+        // ghost planes and stopped reading theirs (which we overwrite now)
+        {
+            int rc = peer_wait(d, d->stream, 0, (uint32_t)d->steps_done);
+            if (rc) return rc;
+        }
+        LBW_CK(cudaEventRecord(d->ev_ready, d->stream));
         if (alm_active(d)) {
             // The actuator chain of this step normally was queued on the
             // actuator stream while the previous sweep ran; otherwise queue
@@ -568,16 +588,21 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
         d->last_fv = fv;
         d->shown_fv = fv;
         LBW_CK(cudaEventRecord(d->ev_sweep[d->step & 1], d->stream));
+        {
+            int rc = peer_signal(d, d->stream, 0, (uint32_t)(d->steps_done + 1));
+            if (rc) return rc;
+        }
         d->cur = 1 - d->cur;
         d->state_pre = false;
         d->step += 1;
         d->steps_done += 1;
         // Queue the next step's actuator chain now: it reads only this
-        // sweep's source buffer and force set (both read-only during the
-        // sweep) and rewrites the force set of the sweep before, so it
-        // waits for that one and then overlaps this sweep.
+        // sweep's source buffer (ghost planes included) and force set, both
+        // read-only during the sweep, and rewrites the force set of the sweep
+        // before — exactly the preconditions of this sweep (ev_ready) — so it
+        // overlaps this sweep.
         if (alm_active(d) && alm_can_prelaunch(d)) {
-            LBW_CK(cudaStreamWaitEvent(d->alm_stream, d->ev_sweep[(d->step - 2) & 1], 0));
+            LBW_CK(cudaStreamWaitEvent(d->alm_stream, d->ev_ready, 0));
             int rc = alm_launch(d, d->step);
             if (rc) return rc;
         }

@@ -85,6 +85,18 @@ struct lbw_domain {
     cudaEvent_t ev_main = nullptr, ev_alm_done = nullptr, ev_sweep[2] = {nullptr, nullptr};
     int64_t steps_done = 0;   // sweeps executed in this domain's lifetime
     bool prelaunch = true;
+    cudaEvent_t ev_ready = nullptr;   // main stream passed the neighbour waits of a step
+    // x-slab neighbours (lbw_peer.cu): side 0 = lo (x-1), side 1 = hi (x+1)
+    bool linked = false;
+    int nb_rank[2] = {-1, -1};
+    int32_t nb_nxl[2] = {0, 0};
+    double* nb_buf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [side][buffer]
+    double* nb_cube[2] = {nullptr, nullptr};
+    uint32_t* nb_flags[2] = {nullptr, nullptr};
+    // my flags, written by the neighbours: [0] sweeps done by lo, [1] by hi,
+    // [2] cube launches done by lo, [3] by hi
+    uint32_t* flags = nullptr;
+    int64_t alm_launches = 0;
     // optional sweep timing (lbw_domain_sweep_timing)
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -108,5 +120,13 @@ ForceView alm_force_view(const lbw_domain* d, int64_t m);
 int alm_invalidate(lbw_domain* d);
 void alm_destroy(lbw_domain* d);
 bool alm_active(const lbw_domain* d);
+// device cube buffer (2, P, 8, 4) of the actuator sampling, or nullptr
+double* alm_cube(const lbw_domain* d);
+
+// lbw_peer.cu: cross-process GPU-side ordering with the slab neighbours
+// (stream memory operations on flags in peer memory; no host round trip)
+int peer_wait(lbw_domain* d, cudaStream_t s, int which, uint32_t value);    // which 0: sweeps, 1: cube
+int peer_signal(lbw_domain* d, cudaStream_t s, int which, uint32_t value);
+void peer_close(lbw_domain* d);
 int ensure_stage(lbw_domain* d, size_t bytes);
 }  // namespace lbw

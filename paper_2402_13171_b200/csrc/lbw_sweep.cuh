@@ -149,15 +149,19 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k_sweep(SweepArgs a) {
     double* d = a.dst + buf_index(g, x + 1, 0, y, z);
 #pragma unroll
     for (int i = 0; i < 27; ++i) d[(int64_t)i * g.dir_stride] = f[i];
+    // edge planes: the outgoing directions go straight into the neighbour
+    // slab's ghost plane (NVLink stores; halo pointers are peer mappings)
     if (x == 0 && a.halo.lo != nullptr) {
         double* h = a.halo.lo + (int64_t)y * g.zp + z;
 #pragma unroll
         for (int i = 0; i < 9; ++i) h[(int64_t)i * g.dir_stride] = f[i];
+        __threadfence_system();
     }
     if (x == g.nxl - 1 && a.halo.hi != nullptr) {
         double* h = a.halo.hi + (int64_t)y * g.zp + z;
 #pragma unroll
         for (int i = 18; i < 27; ++i) h[(int64_t)(i - 18) * g.dir_stride] = f[i];
+        __threadfence_system();
     }
 }
 

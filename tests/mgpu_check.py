@@ -1,0 +1,110 @@
+"""Multi-GPU transparency check, run under torchrun (one process per GPU):
+
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P tests/mgpu_check.py
+
+Every case runs the same configuration on N x-slabs (N GPUs, peer halo
+stores + GPU-side ordering) and on one GPU, and requires the gathered
+populations, force fields and actuator loads to be bit-identical (the
+reference's decomposition-transparency contract, test_acceptance.py:316-348).
+Exit code 0 = all identical.
+"""
+
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_2402_13171_b200 import Simulation, parse_config  # noqa: E402
+from paper_2402_13171_b200.parallel import SlabSimulation  # noqa: E402
+from tests.scenarios import rotor_config  # noqa: E402
+
+
+def lbm_raw(cells, periodic, boundary, op, arithmetic):
+    return {"domain": {"cells": list(cells), "periodicity": list(periodic)},
+            "fluid": {"kinematic_viscosity": 0.05, "wind": [0.02, 0.005, -0.003],
+                      "reference_velocity": 1.0},
+            "resolution": {"mach": 0.1, "cells_per_diameter": 32},
+            "run": {"boundary": boundary, "arithmetic": arithmetic,
+                    "collision": {"operator": op, "higher_order_rates": [1.1, 0.9, 1.3, 1.0]}}}
+
+
+def run_case(name, make_cfg, steps, perturb, kinematics=None):
+    rank, world = dist.get_rank(), dist.get_world_size()
+    cfg = make_cfg()
+    sim = SlabSimulation(cfg, rank, world, device=rank, kinematics=kinematics)
+    nx = cfg.cells[0]
+    f0 = None
+    if perturb:
+        rng = np.random.default_rng(11)
+        x0 = sim.grid.blocks[0].origin[0]
+        full = rng.uniform(-1, 1, (nx,) + tuple(cfg.cells[1:]) + (27,))
+        mine = sim.fields[0].interior.view(np.ndarray)
+        f0 = mine * (1.0 + 0.02 * full[x0:x0 + mine.shape[0]])
+        sim.fields[0].interior = f0
+    for _ in range(steps):
+        sim.step()
+    sim.synchronize()
+    got_f = sim.gather_interior()
+    got_F = sim.gather_force()
+    loads = sim.alm_results_global() if sim.points else None
+    sim.close()
+    ok = True
+    if rank == 0:
+        ref = Simulation(make_cfg(), device=0, kinematics=kinematics)
+        if perturb:
+            rng = np.random.default_rng(11)
+            full = rng.uniform(-1, 1, (nx,) + tuple(cfg.cells[1:]) + (27,))
+            ref.fields[0].interior = ref.fields[0].interior * (1.0 + 0.02 * full)
+        for _ in range(steps):
+            ref.step()
+        ref.synchronize()
+        want_f = ref.fields[0].interior.view(np.ndarray)
+        want_F = ref.fields[0].interior_force.view(np.ndarray)
+        ok = np.array_equal(got_f, want_f) and np.array_equal(got_F, want_F)
+        detail = f"max|df|={np.abs(got_f - want_f).max():.3e}"
+        if loads is not None:
+            rho, u, blade = ref._alm_results()
+            ok = ok and np.array_equal(loads[2], blade) and np.array_equal(loads[0], rho)
+            detail += f" max|dF_blade|={np.abs(loads[2] - blade).max():.3e}"
+        ref.close()
+        print(f"[{name}] world={world} {'OK' if ok else 'MISMATCH'} {detail}", flush=True)
+    flag = torch.tensor([0 if ok else 1])
+    dist.broadcast(flag, 0)
+    return flag.item() == 0
+
+
+def main():
+    dist.init_process_group("gloo")
+    rank = dist.get_rank()
+    torch.cuda.set_device(rank)
+    world = dist.get_world_size()
+    nx = 12 * world
+    ok = True
+    ok &= run_case("periodic-cumulant-exact",
+                   lambda: parse_config(lbm_raw((nx, 16, 13), (True, True, True), "periodic",
+                                                "cumulant", "exact")), 8, True)
+    ok &= run_case("inflow-bgk-fast",
+                   lambda: parse_config(lbm_raw((nx + 3, 10, 16), (False, True, True),
+                                                "velocity_inflow_outflow", "bgk", "fast")), 8, True)
+    ok &= run_case("nonperiodic-yz-cumulant",
+                   lambda: parse_config(lbm_raw((nx, 9, 7), (True, False, False), "periodic",
+                                                "cumulant", "fast")), 6, True)
+    # rotor plane at x = 11.6 cells: sampling cubes and Roma supports straddle
+    # the face between slabs 0 and 1; blades cross the periodic y face too
+    for arith, kin in (("exact", "host"), ("fast", "device")):
+        ok &= run_case(f"rotor-{arith}-{kin}",
+                       lambda: rotor_config(cells=(nx, 12, 12), position=(1.5, 0.3, 0.0),
+                                            arithmetic=arith)[0], 10, False, kinematics=kin)
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
