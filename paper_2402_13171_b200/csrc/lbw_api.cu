@@ -563,6 +563,14 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
         a.nan_key = d->d_nan;
         a.step = d->step;
         a.halo = d->halo[1 - d->cur];
+        if (d->linked) {
+            // the sweep itself tells the neighbours when its edge planes
+            // (halo stores included) are done: flag value = sweeps completed
+            a.halo.peer_flag[0] = d->nb_rank[0] >= 0 ? d->nb_flags[0] + 1 : nullptr;
+            a.halo.peer_flag[1] = d->nb_rank[1] >= 0 ? d->nb_flags[1] + 0 : nullptr;
+            a.halo.edge_counter = d->edge_counter;
+            a.halo.value = (uint32_t)(d->steps_done + 1);
+        }
         const bool pull = !d->state_pre;
         if (d->timing) {
             while (d->ev_pool.size() < d->ev_used + 2) {
@@ -588,10 +596,6 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
         d->last_fv = fv;
         d->shown_fv = fv;
         LBW_CK(cudaEventRecord(d->ev_sweep[d->step & 1], d->stream));
-        {
-            int rc = peer_signal(d, d->stream, 0, (uint32_t)(d->steps_done + 1));
-            if (rc) return rc;
-        }
         d->cur = 1 - d->cur;
         d->state_pre = false;
         d->step += 1;

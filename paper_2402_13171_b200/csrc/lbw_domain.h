@@ -96,6 +96,7 @@ struct lbw_domain {
     // my flags, written by the neighbours: [0] sweeps done by lo, [1] by hi,
     // [2] cube launches done by lo, [3] by hi
     uint32_t* flags = nullptr;
+    unsigned long long* edge_counter = nullptr;  // edge-CTA arrivals (in the flags allocation)
     int64_t alm_launches = 0;
     // optional sweep timing (lbw_domain_sweep_timing)
     bool timing = false;

@@ -42,6 +42,12 @@ struct ForceView {
 struct HaloOut {
     double* lo;  // receives dirs 0..8 of plane x=0   ([9][ny][zp]), or nullptr
     double* hi;  // receives dirs 18..26 of plane x=nxl-1, or nullptr
+    // in-kernel completion signal: the last CTA of the two edge planes
+    // (scheduled first) release-stores `value` into both neighbours' flags
+    uint32_t* peer_flag[2];
+    unsigned long long* edge_counter;  // local, monotonically increasing
+    uint32_t edge_ctas;                // CTAs covering planes 0 and nxl-1
+    uint32_t value;
 };
 
 // kernel launchers (defined in the .cu translation units)

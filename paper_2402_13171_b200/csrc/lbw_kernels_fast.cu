@@ -9,12 +9,14 @@ cudaError_t launch_sweep_fast(int op, bool pull, const SweepArgs& a, cudaStream_
     const dim3 blk = sweep_block(a.g);
     const dim3 grd((a.g.nz + blk.x - 1) / blk.x, (a.g.ny + blk.y - 1) / blk.y, a.x_end - a.x_begin);
     if (grd.z == 0) return cudaSuccess;
+    SweepArgs b = a;
+    b.halo.edge_ctas = grd.x * grd.y * (grd.z < 2 ? grd.z : 2u);
     if (op == 1) {
-        if (pull) k_sweep<1, true><<<grd, blk, 0, s>>>(a);
-        else k_sweep<1, false><<<grd, blk, 0, s>>>(a);
+        if (pull) k_sweep<1, true><<<grd, blk, 0, s>>>(b);
+        else k_sweep<1, false><<<grd, blk, 0, s>>>(b);
     } else {
-        if (pull) k_sweep<0, true><<<grd, blk, 0, s>>>(a);
-        else k_sweep<0, false><<<grd, blk, 0, s>>>(a);
+        if (pull) k_sweep<0, true><<<grd, blk, 0, s>>>(b);
+        else k_sweep<0, false><<<grd, blk, 0, s>>>(b);
     }
     count_launch();
     return cudaGetLastError();

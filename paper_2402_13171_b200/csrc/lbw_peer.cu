@@ -89,6 +89,7 @@ void peer_close(lbw_domain* d) {
     d->peer_mapped.clear();
     if (d->flags) cudaFree(d->flags);
     d->flags = nullptr;
+    d->edge_counter = nullptr;
     d->linked = false;
 }
 
@@ -114,6 +115,7 @@ int lbw_domain_export_handle(lbw_domain* d, void* blob, int64_t* blob_bytes) {
         }
         LBW_CK(cudaMemset(d->flags, 0, 64));
         d->bytes += 64;
+        d->edge_counter = reinterpret_cast<unsigned long long*>(d->flags + 8);
     }
     PeerBlob b;
     std::memset(&b, 0, sizeof b);

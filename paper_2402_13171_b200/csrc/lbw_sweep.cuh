@@ -130,16 +130,30 @@ __device__ __forceinline__ void flag_nonfinite(unsigned long long* key, int64_t 
     }
 }
 
-// K1: fused pull-stream + collide (+Guo) over local planes [x_begin, x_end).
-// One thread per cell, z fastest.  PULL=false collides the stored state in
-// place position (first step after an upload of pre-collision data).
+// Called by every thread of an edge-plane CTA after its halo stores: the
+// CTA's last arrival on the edge counter of this sweep publishes the
+// step's completion value to both neighbours over NVLink.  The counter
+// grows by edge_ctas per sweep, so no reset is needed.
+__device__ __forceinline__ void edge_done(const HaloOut& h) {
+    __threadfence_system();  // this thread's peer stores before the CTA's arrival
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        __threadfence_system();
+        const unsigned long long old = atomicAdd(h.edge_counter, 1ull);
+        if ((old + 1) % h.edge_ctas == 0) {
+            __threadfence_system();
+            for (int s = 0; s < 2; ++s)
+                if (h.peer_flag[s])
+                    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(h.peer_flag[s]),
+                                 "r"(h.value)
+                                 : "memory");
+        }
+    }
+}
+
 template <int OP, bool PULL>
-__global__ void __launch_bounds__(kSweepThreads, 4) k_sweep(SweepArgs a) {
+__device__ __forceinline__ void sweep_cell(const SweepArgs& a, int x, int y, int z) {
     const Geom& g = a.g;
-    const int z = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y * blockDim.y + threadIdx.y;
-    const int x = a.x_begin + blockIdx.z;
-    if (z >= g.nz || y >= g.ny) return;
     double f[27];
     load_cell<PULL>(a.src, g, x, y, z, f);
     double Fx, Fy, Fz;
@@ -155,14 +169,29 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k_sweep(SweepArgs a) {
         double* h = a.halo.lo + (int64_t)y * g.zp + z;
 #pragma unroll
         for (int i = 0; i < 9; ++i) h[(int64_t)i * g.dir_stride] = f[i];
-        __threadfence_system();
     }
     if (x == g.nxl - 1 && a.halo.hi != nullptr) {
         double* h = a.halo.hi + (int64_t)y * g.zp + z;
 #pragma unroll
         for (int i = 18; i < 27; ++i) h[(int64_t)(i - 18) * g.dir_stride] = f[i];
-        __threadfence_system();
     }
+}
+
+// K1: fused pull-stream + collide (+Guo) over local planes [x_begin, x_end).
+// One thread per cell, z fastest.  PULL=false collides the stored state in
+// place position (first step after an upload of pre-collision data).
+template <int OP, bool PULL>
+__global__ void __launch_bounds__(kSweepThreads, 4) k_sweep(SweepArgs a) {
+    const Geom& g = a.g;
+    const int z = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    // the two edge planes come first in dispatch order so their halo stores
+    // (and the completion signal) are issued at the start of the sweep
+    const int bz = (int)blockIdx.z;
+    const int x = a.x_begin + (bz == 0 ? 0 : (bz == 1 ? g.nxl - 1 : bz - 1));
+    const bool edge = bz < 2 && a.halo.edge_counter != nullptr;
+    if (z < g.nz && y < g.ny) sweep_cell<OP, PULL>(a, x, y, z);
+    if (edge) edge_done(a.halo);  // whole CTA, uniform branch
 }
 
 // K0: batch collide of (n,27) rows (_kernels.py:400-427)
