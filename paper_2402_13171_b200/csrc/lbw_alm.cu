@@ -582,11 +582,20 @@ __global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s, int phase
     int32_t* dc = a.dep_cell + (int64_t)p * 9;
     double* dw = a.dep_w + (int64_t)p * 9;
     if (lane == 0) {
-        double blade[3];
-        blade_force(a, p, kin, acc, blade);
-        // per-point outputs are reported by the slab owning floor(x)
-        const int64_t ox = (int64_t)floor(kin[0]) - g.x0;
+        // Multi-slab: only points whose Roma support reaches this slab (their
+        // sampling cube is then complete: own + neighbour cells) are
+        // evaluated; per-point outputs come from the slab owning floor(x).
+        const int64_t n0 = (int64_t)floor(kin[0]);
+        const int64_t ox = n0 - g.x0;
         const bool owner = phase == 0 || (ox >= 0 && ox < g.nxl);
+        bool relevant = phase == 0;
+        for (int dxc = -1; dxc <= 1 && !relevant; ++dxc) {
+            int64_t c = n0 + dxc;
+            if (m.per_x) c = (c % g.nxg + g.nxg) % g.nxg;
+            relevant = c - g.x0 >= 0 && c - g.x0 < g.nxl;
+        }
+        double blade[3] = {0.0, 0.0, 0.0};
+        if (relevant) blade_force(a, p, kin, acc, blade);
         for (int q = 0; q < 4; ++q) a.samples[p * 4 + q] = owner ? acc[q] : 0.0;
         for (int c = 0; c < 3; ++c) {
             a.blade[p * 3 + c] = owner ? blade[c] : 0.0;
