@@ -1,6 +1,8 @@
 // lbw_kernels_fast.cu — FMA flavour of the collide kernels (LBW_MODE_FAST).
 // Compiled with contraction enabled (default -fmad=true).
 #define LBW_FAST 1
+#include <cstdlib>
+
 #include "lbw_sweep.cuh"
 
 namespace lbw {
@@ -11,9 +13,19 @@ cudaError_t launch_sweep_fast(int op, bool pull, const SweepArgs& a, cudaStream_
     if (grd.z == 0) return cudaSuccess;
     SweepArgs b = a;
     b.halo.edge_ctas = grd.x * grd.y * (grd.z < 2 ? grd.z : 2u);
+    // occupancy variant of the hot kernel (LBW_SWEEP_MINB=4|5|6 CTAs/SM)
+    static const int minb = [] {
+        const char* e = getenv("LBW_SWEEP_MINB");
+        return e ? atoi(e) : 5;
+    }();
     if (op == 1) {
-        if (pull) k_sweep<1, true><<<grd, blk, 0, s>>>(b);
-        else k_sweep<1, false><<<grd, blk, 0, s>>>(b);
+        if (pull) {
+            if (minb == 6) k_sweep<1, true, 6><<<grd, blk, 0, s>>>(b);
+            else if (minb == 4) k_sweep<1, true, 4><<<grd, blk, 0, s>>>(b);
+            else k_sweep<1, true, 5><<<grd, blk, 0, s>>>(b);
+        } else {
+            k_sweep<1, false><<<grd, blk, 0, s>>>(b);
+        }
     } else {
         if (pull) k_sweep<0, true><<<grd, blk, 0, s>>>(b);
         else k_sweep<0, false><<<grd, blk, 0, s>>>(b);

@@ -180,8 +180,8 @@ __device__ __forceinline__ void sweep_cell(const SweepArgs& a, int x, int y, int
 // K1: fused pull-stream + collide (+Guo) over local planes [x_begin, x_end).
 // One thread per cell, z fastest.  PULL=false collides the stored state in
 // place position (first step after an upload of pre-collision data).
-template <int OP, bool PULL>
-__global__ void __launch_bounds__(kSweepThreads, 4) k_sweep(SweepArgs a) {
+template <int OP, bool PULL, int MINB = 4>
+__global__ void __launch_bounds__(kSweepThreads, MINB) k_sweep(SweepArgs a) {
     const Geom& g = a.g;
     const int z = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
