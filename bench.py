@@ -92,24 +92,31 @@ def workload(name, n_gpus):
                          "reference_velocity": 1.0},
                "resolution": {"mach": 0.02}, "run": {"collision": {"operator": "cumulant"}}}
         return raw, f"C1 TGV {64 * n_gpus}x64x64 periodic cumulant fp64, no turbine"
-    side = {"c2": (256, 128, 128), "c3": (256, 256, 256)}[name]
-    cells = [side[0] * n_gpus, side[1], side[2]]
-    pos = [2.0, 2.0, 1.2] if name == "c2" else [2.0, 4.0, 3.2]
+    if name == "c4":     # strong scaling: the global domain is fixed
+        cells, cpd, nu, pos = [1024, 512, 512], 64, 0.0866, [4.05, 4.0, 3.2]
+    else:                # weak scaling: one slab of this size per GPU
+        side = {"c2": (256, 128, 128), "c3": (256, 256, 256)}[name]
+        cells = [side[0] * n_gpus, side[1], side[2]]
+        cpd, nu = 32, 0.1732
+        pos = [2.0, 2.0, 1.2] if name == "c2" else [2.0, 4.0, 3.2]
     raw = {"domain": {"cells": cells, "periodicity": [False, True, True]},
-           "fluid": {"kinematic_viscosity": 0.1732, "wind": [8.0, 0.0, 0.0]},
-           "resolution": {"cells_per_diameter": 32, "reference_diameter": 1.0, "mach": 0.05},
+           "fluid": {"kinematic_viscosity": nu, "wind": [8.0, 0.0, 0.0]},
+           "resolution": {"cells_per_diameter": cpd, "reference_diameter": 1.0, "mach": 0.05},
            "run": {"boundary": "velocity_inflow_outflow", "collision": {"operator": "cumulant"}},
            "turbines": [{"file": "rotor.yaml", "position": pos}],
            "polars": [{"id": "sym", "file": "sym.csv"}]}
-    desc = (f"{'C2' if name == 'c2' else 'C3'} {cells[0]}x{cells[1]}x{cells[2]} cumulant fp64, "
-            "inflow/outflow x, one 3-blade ALM rotor (18 points)")
+    desc = (f"{name.upper()} {cells[0]}x{cells[1]}x{cells[2]} cumulant fp64, "
+            f"inflow/outflow x, one 3-blade ALM rotor ({3 * POINTS_PER_BLADE} points)")
     return raw, desc
+
+
+POINTS_PER_BLADE = 6
 
 
 def make_config(name, n_gpus, arithmetic, tmpdir):
     from paper_2402_13171_b200 import parse_config
     with open(os.path.join(tmpdir, "rotor.yaml"), "w") as fh:
-        fh.write(ROTOR)
+        fh.write(ROTOR.replace("points: 6", f"points: {POINTS_PER_BLADE}"))
     with open(os.path.join(tmpdir, "sym.csv"), "w") as fh:
         fh.write(polar_csv())
     raw, desc = workload(name, n_gpus)
@@ -260,7 +267,8 @@ def run_ours(args, rank, world, local_rank):
         out = {
             "metric": METRIC, "value": round(value, 2), "unit": "MLUP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True,
+            "scaling": "strong" if args.config == "c4" else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "cells": list(cfg.cells),
                        "cells_per_gpu": cells_local, "actuator_points": P,
@@ -285,7 +293,7 @@ def run_ours(args, rank, world, local_rank):
         }
     sim.close()
     tmp.cleanup()
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config != "c4":
         out["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_budget)
     if dist is not None:
         dist.destroy_process_group()
@@ -422,11 +430,14 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", choices=("c1", "c2", "c3"), default="c2")
+    ap.add_argument("--config", choices=("c1", "c2", "c3", "c4"), default="c2")
+    ap.add_argument("--points-per-blade", type=int, default=6)
     ap.add_argument("--arithmetic", choices=("exact", "fast"), default="fast")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    global POINTS_PER_BLADE
+    POINTS_PER_BLADE = args.points_per_blade
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     rank = int(os.environ.get("RANK", "0"))

@@ -140,6 +140,9 @@ int64_t lbw_domain_device_bytes(lbw_domain* d);
  * reference's post-stream state after the last step. */
 int lbw_domain_upload_pdf(lbw_domain* d, const double* f_aos);
 int lbw_domain_download_pdf(lbw_domain* d, double* f_aos);
+/* Every owned cell set to the same 27 populations (uniform initial state,
+ * fields.py:54-67 with scalar rho and (3,) u) without a host-sized array. */
+int lbw_domain_fill_uniform(lbw_domain* d, const double* f27);
 /* Same, but on device buffers already laid out AoS (no host copies). */
 int lbw_domain_upload_pdf_device(lbw_domain* d, const double* f_aos_dev);
 

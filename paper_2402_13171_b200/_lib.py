@@ -124,6 +124,7 @@ SIGNATURES = {
     "lbw_domain_upload_pdf": (_I, [_VP, _VP]),
     "lbw_domain_download_pdf": (_I, [_VP, _VP]),
     "lbw_domain_upload_pdf_device": (_I, [_VP, _VP]),
+    "lbw_domain_fill_uniform": (_I, [_VP, _VP]),
     "lbw_domain_set_force": (_I, [_VP, _VP]),
     "lbw_domain_download_force": (_I, [_VP, _VP]),
     "lbw_domain_set_macro": (_I, [_VP, _VP, _VP]),

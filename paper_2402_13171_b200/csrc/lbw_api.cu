@@ -372,6 +372,23 @@ int lbw_domain_upload_pdf(lbw_domain* d, const double* f_aos) {
     return LBW_OK;
 }
 
+int lbw_domain_fill_uniform(lbw_domain* d, const double* f27) {
+    LBW_REQ(d && f27, "null argument");
+    LBW_CK(cudaSetDevice(d->device));
+    {
+        int rc_ = alm_invalidate(d);
+        if (rc_) return rc_;
+    }
+    int rc = freeze_macro_if(d, true, false);
+    if (rc) return rc;
+    double v[27];
+    for (int i = 0; i < 27; ++i) v[i] = f27[i];
+    LBW_CK(launch_fill_uniform(v, d->buf[d->cur], d->g, d->stream));
+    LBW_CK(cudaStreamSynchronize(d->stream));
+    d->state_pre = true;
+    return LBW_OK;
+}
+
 int lbw_domain_upload_pdf_device(lbw_domain* d, const double* f_aos_dev) {
     LBW_REQ(d && f_aos_dev, "null argument");
     LBW_CK(cudaSetDevice(d->device));

@@ -84,6 +84,8 @@ cudaError_t launch_block_moments(const double* f, const double* force, double* m
 cudaError_t launch_block_stream(const double* fsrc, double* fdst, int64_t nx, int64_t ny,
                                 int64_t nz, cudaStream_t s);
 cudaError_t launch_aos_to_soa(const double* aos, double* buf, const Geom& g, cudaStream_t s);
+cudaError_t launch_fill_uniform(const double (&f27)[27], double* buf, const Geom& g,
+                                cudaStream_t s);
 cudaError_t launch_gather_aos(bool pull, const double* buf, const Geom& g, double* aos,
                               cudaStream_t s);
 cudaError_t launch_moments_soa(bool pull, const double* buf, const Geom& g, ForceView fv,

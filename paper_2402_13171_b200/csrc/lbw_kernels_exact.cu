@@ -100,6 +100,19 @@ __global__ void k_aos_to_soa(const double* __restrict__ aos, double* __restrict_
     for (int i = 0; i < 27; ++i) d[(int64_t)i * g.dir_stride] = aos[t * 27 + i];
 }
 
+struct F27 {
+    double v[27];
+};
+
+__global__ void k_fill_uniform(F27 f, double* __restrict__ buf, Geom g) {
+    int x, y, z;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (!cell_of(g, t, x, y, z)) return;
+    double* d = buf + buf_index(g, x + 1, 0, y, z);
+#pragma unroll
+    for (int i = 0; i < 27; ++i) d[(int64_t)i * g.dir_stride] = f.v[i];
+}
+
 template <bool PULL>
 __global__ void k_gather_aos(const double* __restrict__ buf, Geom g, double* __restrict__ aos) {
     int x, y, z;
@@ -185,6 +198,15 @@ cudaError_t launch_block_stream(const double* fsrc, double* fdst, int64_t nx, in
 
 cudaError_t launch_aos_to_soa(const double* aos, double* buf, const Geom& g, cudaStream_t s) {
     k_aos_to_soa<<<cells_blocks(g, 128), 128, 0, s>>>(aos, buf, g);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_uniform(const double (&f27)[27], double* buf, const Geom& g,
+                                cudaStream_t s) {
+    F27 f;
+    for (int i = 0; i < 27; ++i) f.v[i] = f27[i];
+    k_fill_uniform<<<cells_blocks(g, 128), 128, 0, s>>>(f, buf, g);
     count_launch();
     return cudaGetLastError();
 }

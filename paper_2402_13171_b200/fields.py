@@ -126,16 +126,16 @@ class DeviceField:
         rho_arr = np.broadcast_to(np.asarray(rho, np.float64), n)
         u_arr = np.broadcast_to(np.asarray(u, np.float64), n + (3,))
         uniform = np.ndim(rho) == 0 and np.shape(u) == (3,)
-        if uniform:
-            # one cell's equilibrium, evaluated by the same numpy expression
-            one = (product_equilibrium if product else equilibrium_pdf)(
-                np.asarray(rho, np.float64), np.asarray(u, np.float64))
-            eq = np.broadcast_to(one, n + (27,))
-        else:
-            eq = (product_equilibrium if product else equilibrium_pdf)(rho_arr, u_arr)
         self.set_force(None)
-        self.upload_pdf(eq)
         lib = _lib.load()
+        if uniform:
+            # one cell's equilibrium, evaluated by the same numpy expression,
+            # replicated on the device (no lattice-sized host array)
+            one = np.ascontiguousarray((product_equilibrium if product else equilibrium_pdf)(
+                np.asarray(rho, np.float64), np.asarray(u, np.float64)), dtype=np.float64)
+            _lib.check(lib.lbw_domain_fill_uniform(self._d, _lib.ptr(one)), "init")
+        else:
+            self.upload_pdf((product_equilibrium if product else equilibrium_pdf)(rho_arr, u_arr))
         if uniform:
             u4 = np.array([float(rho), *np.asarray(u, np.float64)])
             _lib.check(lib.lbw_domain_set_macro(self._d, None, _lib.ptr(u4)), "macro")
