@@ -284,7 +284,13 @@ int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out) {
     int rc = LBW_OK;
     const size_t buf_bytes = (size_t)(g.nxl + 2) * g.plane_stride * sizeof(double);
     if (cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&d->alm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        // the actuator chain runs beside the sweep: highest priority so its
+        // few CTAs are dispatched ahead of the sweep's remaining ones
+        [&] {
+            int lo = 0, hi = 0;
+            cudaDeviceGetStreamPriorityRange(&lo, &hi);
+            return cudaStreamCreateWithPriority(&d->alm_stream, cudaStreamNonBlocking, hi);
+        }() != cudaSuccess ||
         cudaEventCreateWithFlags(&d->ev_main, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&d->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&d->ev_alm_done, cudaEventDisableTiming) != cudaSuccess ||
