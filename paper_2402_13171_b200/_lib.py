@@ -14,7 +14,8 @@ import numpy as np
 
 from .errors import ConfigError, NumericalAbort
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liblbw.so")
+LIB_PATH = os.environ.get("LBW_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "liblbw.so")   # LBW_LIB: A/B builds of the library
 
 LBW_OK = 0
 LBW_EINVAL = -1

@@ -80,6 +80,28 @@ __device__ __forceinline__ void make_pull(const Geom& g, int x, int y, int z, Pu
     }
 }
 
+#ifndef LBW_STREAM_HINTS
+#define LBW_STREAM_HINTS 0
+#endif
+// Streaming cache hints for the single-use population traffic: loads skip
+// L1 allocation, stores are marked evict-first.
+__device__ __forceinline__ double ld_pop(const double* p) {
+#if LBW_STREAM_HINTS
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ void st_pop(double* p, double v) {
+#if LBW_STREAM_HINTS
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
+}
+
 template <bool PULL>
 __device__ __forceinline__ void load_cell(const double* __restrict__ src, const Geom& g, int x, int y,
                                           int z, double (&f)[27]) {
@@ -98,10 +120,45 @@ __device__ __forceinline__ void load_cell(const double* __restrict__ src, const 
             } else if (s.xkind[a] == 2 || !s.yok[b] || !s.zok[c]) {
                 f[i] = 0.0;
             } else {
-                f[i] = __ldg(src + s.xoff[a] + (int64_t)i * g.dir_stride + s.yoff[b] + s.zs[c]);
+                f[i] = ld_pop(src + s.xoff[a] + (int64_t)i * g.dir_stride + s.yoff[b] + s.zs[c]);
             }
         }
     }
+}
+
+// Pull with every source in memory (no inflow constant, no zero ghost):
+// true for all cells except those at a non-periodic y/z face or an
+// inflow / unbounded x face.  Branch-free: one 32-bit offset per
+// direction inside its source plane (a plane is < 2^31 doubles).
+__device__ __forceinline__ bool pull_is_simple(const Geom& g, int x, int y, int z) {
+    const bool xs = !((x == 0 && (g.lo_src == XS_CONST || g.lo_src == XS_ZERO)) ||
+                      (x == g.nxl - 1 && (g.hi_src == XS_CONST || g.hi_src == XS_ZERO)));
+    const bool ys = g.per_y || (y > 0 && y < g.ny - 1);
+    const bool zs = g.per_z || (z > 0 && z < g.nz - 1);
+    return xs && ys && zs;
+}
+
+__device__ __forceinline__ void load_cell_simple(const double* __restrict__ src, const Geom& g,
+                                                 int x, int y, int z, double (&f)[27]) {
+    const double* px[3];
+#pragma unroll
+    for (int c = -1; c <= 1; ++c) {
+        int64_t off;
+        int32_t kind;
+        x_source(g, x, c, off, kind);
+        px[c + 1] = src + off;
+    }
+    const int ym = (y + 1 < g.ny ? y + 1 : y + 1 - g.ny) * g.zp;  // cy = -1: y+1
+    const int y0 = y * g.zp;
+    const int yp = (y > 0 ? y - 1 : y - 1 + g.ny) * g.zp;        // cy = +1: y-1
+    const int zm = z + 1 < g.nz ? z + 1 : z + 1 - g.nz;           // cz = -1: z+1
+    const int zp = z > 0 ? z - 1 : z - 1 + g.nz;                  // cz = +1: z-1
+    const int ds = (int)g.dir_stride;
+    const int yo[3] = {ym, y0, yp};
+    const int zo[3] = {zm, z, zp};
+#pragma unroll
+    for (int i = 0; i < 27; ++i)
+        f[i] = ld_pop(px[cx_of(i) + 1] + (i * ds + yo[cy_of(i) + 1] + zo[cz_of(i) + 1]));
 }
 
 __device__ __forceinline__ void load_force(const ForceView& fv, const Geom& g, int x, int y, int z,
@@ -155,14 +212,15 @@ template <int OP, bool PULL>
 __device__ __forceinline__ void sweep_cell(const SweepArgs& a, int x, int y, int z) {
     const Geom& g = a.g;
     double f[27];
-    load_cell<PULL>(a.src, g, x, y, z, f);
+    if (PULL && pull_is_simple(g, x, y, z)) load_cell_simple(a.src, g, x, y, z, f);
+    else load_cell<PULL>(a.src, g, x, y, z, f);
     double Fx, Fy, Fz;
     load_force(a.fv, g, x, y, z, Fx, Fy, Fz);
     const Macro m = collide_cell<OP>(f, Fx, Fy, Fz, a.r);
     flag_nonfinite(a.nan_key, a.step, ((g.x0 + x) * g.ny + y) * (int64_t)g.nz + z, m);
     double* d = a.dst + buf_index(g, x + 1, 0, y, z);
 #pragma unroll
-    for (int i = 0; i < 27; ++i) d[(int64_t)i * g.dir_stride] = f[i];
+    for (int i = 0; i < 27; ++i) st_pop(d + i * (int)g.dir_stride, f[i]);
     // edge planes: the outgoing directions go straight into the neighbour
     // slab's ghost plane (NVLink stores; halo pointers are peer mappings)
     if (x == 0 && a.halo.lo != nullptr) {
