@@ -342,35 +342,13 @@ def _oracle_run(cfg, steps, sim_host):
     return time.perf_counter() - t0
 
 
-class _HostOnlySim:
-    """The host half of Simulation (kinematics, parameters) without a GPU,
+def _HostOnlySim(cfg):
+    """The host half of a Simulation (kinematics, parameters) without a GPU,
     used to drive the oracle with identical actuator kinematics."""
-
-    def __init__(self, cfg):
-        from paper_2402_13171_b200.halo import BoundarySpec
-        from paper_2402_13171_b200.sim import Simulation, SlabGrid
-        from paper_2402_13171_b200.turbine import LineSpec
-        self.cfg, self.units = cfg, cfg.units
-        self.grid = SlabGrid(cfg.cells, cfg.periodicity, 1, 0)
-        self.boundary = BoundarySpec(cfg.boundary_kind, cfg.units.velocity_to_lattice(
-            np.asarray(cfg.wind, dtype=np.float64)))
-        self.points, self._line_groups = [], []
-        gid = 0
-        for topo in cfg.topologies:
-            for comp in topo.components:
-                spec = comp.discretization
-                if isinstance(spec, LineSpec):
-                    for pi in range(spec.n_points):
-                        pid = spec.polar[pi]
-                        self.points.append(type("P", (), dict(
-                            chord=spec.chord[pi], element_length=spec.element_length[pi],
-                            twist=spec.twist[pi],
-                            polar=cfg.polars.get(pid) if pid is not None else None))())
-                    self._line_groups.append((comp, spec, slice(gid, gid + spec.n_points)))
-                    gid += spec.n_points
-        self._kin = np.zeros((gid, 18))
-        self._pos_m = np.zeros((gid, 3))
-        self.refresh_points = Simulation.refresh_points.__get__(self)
+    from paper_2402_13171_b200.sim import HostKinematics
+    host = HostKinematics(cfg)
+    host.refresh_points = host.refresh
+    return host
 
 
 def cpu_baseline(args, budget_s=20.0):

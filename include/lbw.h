@@ -208,6 +208,16 @@ typedef struct lbw_alm_desc {
     double rho_ref;                 /* units.rho_ref                            */
     double force_dt2;               /* units.dt**2         (units.py:69)        */
     double force_den;               /* units.rho_ref*dx**4 (units.py:69)        */
+    /* actuator disks (actuator.py:149-183): points of a ring share a ring
+     * id; their force is the ring's momentum-theory thrust spread by area.
+     * A disk point's kinematics row carries the disk axis (centre frame's
+     * +x, unnormalised) in the e_chord slot. */
+    const int32_t* point_ring;      /* (P,) ring id or -1 (line point); may be NULL */
+    const double* area;             /* (P,) m^2 (disk samples)                  */
+    int32_t n_rings;
+    const int32_t* ring_first;      /* (n_rings,) first point id of the ring    */
+    const int32_t* ring_count;      /* (n_rings,) sectors                        */
+    const double* ring_ct;          /* (n_rings,) thrust coefficient in [0, 1)   */
     int64_t reserved[8];
 } lbw_alm_desc;
 
@@ -234,6 +244,11 @@ typedef struct lbw_kin_desc {
     const double* local_frames;     /* (P,3,3) rows chord, normal, span (local) */
     double dx;                      /* m per cell                               */
     int32_t advance_first;          /* 1: advance by dt before the first step  */
+    /* disks: the component's disk centre transform relative to it
+     * (DiskSpec.center, turbine.py:150-193) and its sample offsets (in
+     * `offsets`, rows line_first .. line_first+line_count) */
+    const int32_t* is_disk;         /* (C) 1 for a disk component, else 0      */
+    const double* disk_center;      /* (C,12) centre p(3), T(3,3); zeros if none */
     int64_t reserved[8];
 } lbw_kin_desc;
 int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* desc);

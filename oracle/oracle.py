@@ -187,6 +187,28 @@ def blade_force(kin_row, rho_lat, u_lat, chord, elen, twist, polar, vscale, rho_
     return scale * (cl * np.asarray(e_l) + cd * np.asarray(e_d))
 
 
+def disk_forces(ct, axis_world, rho_samples, u_samples, areas, rings, sectors):
+    """actuator_disk_forces (actuator.py:149-183): per-ring momentum theory,
+    force on the FLUID per sample."""
+    axis = np.asarray(axis_world, dtype=np.float64)
+    axis = axis / np.linalg.norm(axis)
+    forces = np.zeros((rings * sectors, 3))
+    u_ax = np.asarray(u_samples) @ axis
+    for j in range(rings):
+        sl = slice(j * sectors, (j + 1) * sectors)
+        if ct[j] == 0.0:
+            continue
+        a = (1.0 - np.sqrt(1.0 - ct[j])) / 2.0
+        ring_area = areas[sl].sum()
+        u_d = float((u_ax[sl] * areas[sl]).sum() / ring_area)
+        rho = float((rho_samples[sl] * areas[sl]).sum() / ring_area)
+        u_inf = u_d / (1.0 - a)
+        thrust = 0.5 * rho * u_inf * u_inf * ct[j] * ring_area
+        direction = -np.sign(u_d) if u_d != 0.0 else 0.0
+        forces[sl] = direction * (thrust / ring_area) * areas[sl][:, None] * axis[None, :]
+    return forces
+
+
 def _support_box(pos):
     lo = np.empty(3, dtype=np.int64)
     hi = np.empty(3, dtype=np.int64)
@@ -309,10 +331,18 @@ class OracleSim:
             rho, u = interpolate(self.macro, kin[p, 0:3])
             self.samples[p, 0] = rho
             self.samples[p, 1:] = u
-            b = blade_force(kin[p], rho, u, pts["chord"][p], pts["element_length"][p],
-                            pts["twist"][p], pts["polar"][p], pts["vscale"], pts["rho_ref"])
-            self.blade[p] = b
-            records.append((p, kin[p, 0:3].copy(), -b))
+            self.blade[p] = blade_force(kin[p], rho, u, pts["chord"][p],
+                                        pts["element_length"][p], pts["twist"][p],
+                                        pts["polar"][p], pts["vscale"], pts["rho_ref"])
+        # disks: sim.py:236-244 (samples in physical units, axis = centre +x,
+        # carried in the kinematics' e_chord slot)
+        for first, rings, sectors, ct in pts.get("disks", ()):
+            sl = slice(first, first + rings * sectors)
+            f = disk_forces(ct, kin[first, 6:9], self.samples[sl, 0] * pts["rho_ref"],
+                            self.samples[sl, 1:] * pts["vscale"], pts["area"][sl], rings, sectors)
+            self.blade[sl] = -f
+        for p in range(P):
+            records.append((p, kin[p, 0:3].copy(), -self.blade[p]))
         routed = route_single_block(records, self.dims, self.periodic)
         self.force[...] = 0.0
         spread(routed, self.force, self.dims, pts["dt2"], pts["den"])

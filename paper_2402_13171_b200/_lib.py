@@ -75,6 +75,12 @@ class AlmDesc(ctypes.Structure):
         ("rho_ref", ctypes.c_double),
         ("force_dt2", ctypes.c_double),
         ("force_den", ctypes.c_double),
+        ("point_ring", _c_i32_p),
+        ("area", _c_double_p),
+        ("n_rings", ctypes.c_int32),
+        ("ring_first", _c_i32_p),
+        ("ring_count", _c_i32_p),
+        ("ring_ct", _c_double_p),
         ("reserved", ctypes.c_int64 * 8),
     ]
 
@@ -96,6 +102,8 @@ class KinDesc(ctypes.Structure):
         ("local_frames", _c_double_p),
         ("dx", ctypes.c_double),
         ("advance_first", ctypes.c_int32),
+        ("is_disk", _c_i32_p),
+        ("disk_center", _c_double_p),
         ("reserved", ctypes.c_int64 * 8),
     ]
 

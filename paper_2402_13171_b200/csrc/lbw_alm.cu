@@ -62,6 +62,12 @@ struct AlmDev {
     int32_t* dep_cell;     // (P,3 axes,3) global cell or -1
     double* dep_w;         // (P,3,3)
     int32_t* clamp_flags;  // (n_polars)
+    const int32_t* point_ring;  // (P) disk ring id or -1
+    const double* area;         // (P)
+    int32_t n_rings;
+    const int32_t* ring_first;
+    const int32_t* ring_count;
+    const double* ring_ct;
     int32_t* error_flags;  // bit 0: non-positive density, bit 1: point outside domain
 };
 
@@ -80,6 +86,8 @@ struct KinDev {
     const double* off;
     const double* orient;
     const double* lframe;
+    const int32_t* is_disk;
+    const double* disk_center;
     double* cs;
     double dx;
 };
@@ -97,6 +105,9 @@ struct AlmState {
     int32_t* dep_cell = nullptr;
     double* dep_w = nullptr;
     int32_t *clamp_flags = nullptr, *error_flags = nullptr;
+    int32_t *point_ring = nullptr, *ring_first = nullptr, *ring_count = nullptr;
+    double *area = nullptr, *ring_ct = nullptr;
+    int32_t n_rings = 0;
     double vscale = 0, rho_ref = 0, dt2 = 0, den = 0;
     ForceSet set[2];
     double* h_ring = nullptr;   // pinned (kRing, P, 18)
@@ -113,6 +124,8 @@ struct AlmState {
     double *k_rel_p = nullptr, *k_rel_T = nullptr, *k_axis = nullptr, *k_rate = nullptr;
     double *k_rstep = nullptr, *k_spin = nullptr, *k_off = nullptr, *k_orient = nullptr;
     double *k_lframe = nullptr, *k_cs = nullptr;
+    int32_t* k_is_disk = nullptr;
+    double* k_disk_center = nullptr;
     double k_dx = 1.0;
     int64_t kin_state_step = 0;  // step whose kinematics the device spins represent
     std::vector<void*> allocs;
@@ -141,6 +154,12 @@ struct AlmState {
         a.dep_w = dep_w;
         a.clamp_flags = clamp_flags;
         a.error_flags = error_flags;
+        a.point_ring = point_ring;
+        a.area = area;
+        a.n_rings = n_rings;
+        a.ring_first = ring_first;
+        a.ring_count = ring_count;
+        a.ring_ct = ring_ct;
         return a;
     }
     KinDev kdev() const {
@@ -159,6 +178,8 @@ struct AlmState {
         k.off = k_off;
         k.orient = k_orient;
         k.lframe = k_lframe;
+        k.is_disk = k_is_disk;
+        k.disk_center = k_disk_center;
         k.cs = k_cs;
         k.dx = k_dx;
         return k;
@@ -246,7 +267,8 @@ __device__ double np_mod(double a, double b) {
 // state are staged in shared memory (the walk itself is one thread: a chain
 // of dependent 3x3 products down the tree); points are then evaluated in
 // parallel.  Layout per component in smem: params[kKP] then state[kCS].
-constexpr int kKP = 36;  // rel_p 3, rel_T 9, axis 3, rate 1, rstep 9, spin 9, parent 1, first 1
+// rel_p 3, rel_T 9, axis 3, rate 1, rstep 9, spin 9, parent 1, first 1, is_disk 1, disk p 3, T 9
+constexpr int kKP = 49;
 __global__ void k_kinematics(KinDev k, AlmDev a, Geom g, int per_x, int advance) {
     extern __shared__ double ksm[];
     double* prm = ksm;                         // (nc, kKP)
@@ -261,7 +283,9 @@ __global__ void k_kinematics(KinDev k, AlmDev a, Geom g, int per_x, int advance)
         else if (j < 25) v = k.rstep[c * 9 + j - 16];
         else if (j < 34) v = k.spin[c * 9 + j - 25];
         else if (j < 35) v = (double)k.parent[c];
-        else v = (double)k.line_first[c];
+        else if (j < 36) v = (double)k.line_first[c];
+        else if (j < 37) v = (double)k.is_disk[c];
+        else v = k.disk_center[c * 12 + j - 37];
         prm[i] = v;
     }
     __syncthreads();
@@ -306,7 +330,16 @@ __global__ void k_kinematics(KinDev k, AlmDev a, Geom g, int per_x, int advance)
             }
             for (int i = 0; i < 9; ++i) s[CS_R + i] = spin[i];
             const int first = (int)q[35];
-            if (first >= 0) {
+            if (q[36] != 0.0) {
+                // disk centre (update_disk, turbine.py:237-241) and its velocity
+                double Tc_p[3], TcT[9];
+                mv3(s + CS_T, q + 37, Tc_p);
+                for (int i = 0; i < 3; ++i) s[CS_SP + i] = s[CS_P + i] + Tc_p[i];
+                mm3(s + CS_T, q + 40, TcT);
+                mm3(TcT, spin, s + CS_ST);
+                cross3(s + CS_W, Tc_p, cr);
+                for (int i = 0; i < 3; ++i) s[CS_VS + i] = s[CS_V + i] + cr[i];
+            } else if (first >= 0) {
                 const double* W = s + CS_T;
                 double Tp_o0[3], Tp_O0[9], o0[3], O0[9];
                 for (int i = 0; i < 3; ++i) o0[i] = k.off[(int64_t)first * 3 + i];
@@ -338,7 +371,17 @@ __global__ void k_kinematics(KinDev k, AlmDev a, Geom g, int per_x, int advance)
         const double* s = cs + c * kCS;
         const int kk = p - k.line_first[c];
         double pos[3], fr[9], vel[3];
-        if (kk == 0) {
+        const bool disk = prm[c * kKP + 36] != 0.0;
+        if (disk) {
+            // world = centre.p + offs @ centre.T^T (sim.py:182-187); the disk
+            // axis (centre frame +x) rides in the e_chord slot
+            double rel[3];
+            mv3(s + CS_ST, k.off + (int64_t)p * 3, rel);
+            for (int i = 0; i < 3; ++i) pos[i] = s[CS_SP + i] + rel[i];
+            for (int i = 0; i < 3; ++i) vel[i] = s[CS_VS + i];
+            const double fr_d[9] = {s[CS_ST], s[CS_ST + 3], s[CS_ST + 6], 0, 1, 0, 0, 0, 1};
+            for (int i = 0; i < 9; ++i) fr[i] = fr_d[i];
+        } else if (kk == 0) {
             for (int i = 0; i < 3; ++i) pos[i] = s[CS_SP + i];
             for (int i = 0; i < 9; ++i) fr[i] = s[CS_ST + i];
             for (int i = 0; i < 3; ++i) vel[i] = s[CS_VS + i];
@@ -360,7 +403,11 @@ __global__ void k_kinematics(KinDev k, AlmDev a, Geom g, int per_x, int advance)
             out[3 + i] = vel[i];
             out[15 + i] = pos[i];
         }
-        for (int f = 0; f < 3; ++f) mv3(fr, k.lframe + (int64_t)p * 9 + f * 3, out + 6 + 3 * f);
+        if (disk) {
+            for (int i = 0; i < 9; ++i) out[6 + i] = fr[i];
+        } else {
+            for (int f = 0; f < 3; ++f) mv3(fr, k.lframe + (int64_t)p * 9 + f * 3, out + 6 + 3 * f);
+        }
     }
 }
 
@@ -595,7 +642,8 @@ __global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s, int phase
             relevant = c - g.x0 >= 0 && c - g.x0 < g.nxl;
         }
         double blade[3] = {0.0, 0.0, 0.0};
-        if (relevant) blade_force(a, p, kin, acc, blade);
+        const bool disk = a.point_ring != nullptr && a.point_ring[p] >= 0;
+        if (relevant && !disk) blade_force(a, p, kin, acc, blade);
         for (int q = 0; q < 4; ++q) a.samples[p * 4 + q] = owner ? acc[q] : 0.0;
         for (int c = 0; c < 3; ++c) {
             a.blade[p * 3 + c] = owner ? blade[c] : 0.0;
@@ -618,6 +666,46 @@ __global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s, int phase
                 s.slot_row[slot] = (int32_t)row;
                 s.row_slot[row] = slot;
             }
+        }
+    }
+}
+
+// K4d: actuator-disk rings (actuator.py:149-183), one thread per ring, fixed
+// summation order.  Fluid force per sample = direction * thrust/area_ring *
+// area_i * axis; the blade force is its negation (sim.py:236-244).
+__global__ void k_alm_disks(AlmDev a) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= a.n_rings) return;
+    const int first = a.ring_first[r], cnt = a.ring_count[r];
+    const double ct = a.ring_ct[r];
+    const double* k0 = a.kin + (int64_t)first * kKin;
+    double axis[3] = {k0[6], k0[7], k0[8]};
+    const double nrm = sqrt(dot3(axis, axis));
+    for (int c = 0; c < 3; ++c) axis[c] = axis[c] / nrm;
+    if (ct == 0.0) return;  // forces stay zero
+    const double ind = (1.0 - sqrt(1.0 - ct)) / 2.0;
+    double ring_area = 0.0, su = 0.0, srho = 0.0;
+    for (int i = 0; i < cnt; ++i) {
+        const int p = first + i;
+        const double ar = a.area[p];
+        double up[3];
+        for (int c = 0; c < 3; ++c) up[c] = a.samples[p * 4 + 1 + c] * a.vscale;
+        ring_area += ar;
+        su += dot3(up, axis) * ar;
+        srho += a.samples[p * 4] * a.rho_ref * ar;
+    }
+    const double u_d = su / ring_area;
+    const double rho = srho / ring_area;
+    const double u_inf = u_d / (1.0 - ind);
+    const double thrust = 0.5 * rho * u_inf * u_inf * ct * ring_area;
+    const double direction = u_d != 0.0 ? (u_d > 0.0 ? -1.0 : 1.0) : 0.0;
+    const double per_area = thrust / ring_area;
+    for (int i = 0; i < cnt; ++i) {
+        const int p = first + i;
+        for (int c = 0; c < 3; ++c) {
+            const double f = direction * per_area * a.area[p] * axis[c];
+            a.blade[p * 3 + c] = -f;
+            a.flat[p * 3 + c] = f * a.dt2 / a.den;
         }
     }
 }
@@ -791,6 +879,10 @@ int alm_launch(lbw_domain* d, int64_t m) {
         k_alm_points<<<blocks, threads, 0, st>>>(a, g, md, fs, 0, cube);
     }
     d->alm_launches += 1;
+    if (s->n_rings > 0) {
+        k_alm_disks<<<(unsigned)((s->n_rings + 63) / 64), 64, 0, st>>>(a);
+        count_launch();
+    }
     k_alm_fill<<<(unsigned)fs.cap, 128, s->fill_smem, st>>>(a, g, fs);
     count_launch(2);
     LBW_CK(cudaGetLastError());
@@ -818,6 +910,16 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     for (int p = 0; p < P; ++p)
         LBW_REQ(desc->polar_index[p] >= -1 && desc->polar_index[p] < desc->n_polars,
                 "polar index out of range");
+    if (desc->point_ring) {
+        LBW_REQ(desc->area && desc->n_rings >= 0, "disk rings need areas");
+        for (int r = 0; r < desc->n_rings; ++r) {
+            LBW_REQ(desc->ring_first[r] >= 0 && desc->ring_count[r] >= 1 &&
+                        desc->ring_first[r] + desc->ring_count[r] <= P,
+                    "disk ring point range out of bounds");
+            LBW_REQ(desc->ring_ct[r] >= 0.0 && desc->ring_ct[r] < 1.0,
+                    "thrust coefficient must lie in [0, 1)");
+        }
+    }
     int64_t total_rows = 0;
     for (int k = 0; k < desc->n_polars; ++k) {
         LBW_REQ(desc->polar_rows[k] >= 2, "polar needs at least 2 rows");
@@ -863,6 +965,14 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     A(&s->dep_w, (size_t)P * 9);
     A(&s->clamp_flags, std::max(1, desc->n_polars));
     A(&s->error_flags, 1);
+    const int R = desc->point_ring ? desc->n_rings : 0;
+    if (desc->point_ring) {
+        A(&s->point_ring, P);
+        A(&s->area, P);
+        A(&s->ring_first, std::max(1, R));
+        A(&s->ring_count, std::max(1, R));
+        A(&s->ring_ct, std::max(1, R));
+    }
     // sparse force sets: a point touches at most 3x3 (x,y) rows
     const int64_t rows = (int64_t)d->g.nxl * d->g.ny;
     const int64_t cap = std::min<int64_t>(rows, (int64_t)9 * P);
@@ -889,6 +999,16 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     H(s->elen, desc->element_length, P * 8);
     H(s->twist, desc->twist, P * 8);
     H(s->polar_index, desc->polar_index, P * 4);
+    if (desc->point_ring) {
+        H(s->point_ring, desc->point_ring, P * 4);
+        H(s->area, desc->area, P * 8);
+        if (R) {
+            H(s->ring_first, desc->ring_first, R * 4);
+            H(s->ring_count, desc->ring_count, R * 4);
+            H(s->ring_ct, desc->ring_ct, R * 8);
+        }
+        s->n_rings = R;
+    }
     if (desc->n_polars) {
         H(s->polar_offset, desc->polar_offset, desc->n_polars * 4);
         H(s->polar_rows, desc->polar_rows, desc->n_polars * 4);
@@ -945,7 +1065,8 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
     std::vector<int32_t> point_comp(P, -1);
     for (int c = 0; c < C; ++c)
         for (int k = 0; k < kd->line_count[c]; ++k) point_comp[kd->line_first[c] + k] = c;
-    for (int p = 0; p < P; ++p) LBW_REQ(point_comp[p] >= 0, "point without a line component");
+    for (int p = 0; p < P; ++p)
+        LBW_REQ(point_comp[p] >= 0, "point without a line or disk component");
     int rc = LBW_OK;
     auto A = [&](auto** p, size_t n) {
         if (rc == LBW_OK) rc = dev_alloc(d, s, p, n);
@@ -964,6 +1085,8 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
     A(&s->k_orient, (size_t)P * 9);
     A(&s->k_lframe, (size_t)P * 9);
     A(&s->k_cs, (size_t)C * kCS);
+    A(&s->k_is_disk, C);
+    A(&s->k_disk_center, (size_t)C * 12);
     if (rc) return rc;
     auto H = [&](void* dst, const void* src, size_t bytes) {
         if (rc == LBW_OK && cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
@@ -985,6 +1108,17 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
     H(s->k_off, kd->offsets, (size_t)P * 24);
     H(s->k_orient, kd->orientations, (size_t)P * 72);
     H(s->k_lframe, kd->local_frames, (size_t)P * 72);
+    {
+        std::vector<int32_t> isd(C, 0);
+        std::vector<double> dcen((size_t)C * 12, 0.0);
+        for (int c = 0; c < C; ++c) {
+            if (kd->is_disk) isd[c] = kd->is_disk[c] ? 1 : 0;
+            if (kd->disk_center && isd[c])
+                for (int i = 0; i < 12; ++i) dcen[(size_t)c * 12 + i] = kd->disk_center[(size_t)c * 12 + i];
+        }
+        H(s->k_is_disk, isd.data(), C * 4);
+        H(s->k_disk_center, dcen.data(), (size_t)C * 96);
+    }
     if (rc) return rc;
     const size_t ksm = (size_t)C * (kKP + kCS) * sizeof(double);
     if (ksm > 48 * 1024 &&

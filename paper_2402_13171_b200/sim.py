@@ -83,7 +83,7 @@ class ActuatorPoint:
     attribute reads fetch device results lazily."""
 
     def __init__(self, sim, gid, chord=0.0, element_length=0.0, twist=0.0, polar=None,
-                 area=0.0):
+                 area=0.0, disk=False):
         self._sim = sim
         self.global_id = int(gid)
         self.chord = float(chord)
@@ -92,16 +92,21 @@ class ActuatorPoint:
         self.polar = polar
         self.area = float(area)
         self.owner_block = -1
+        self.is_disk_sample = bool(disk)
 
     def _k(self, a, b):
         return self._sim._kin_view()[self.global_id, a:b].copy()
 
+    def _frame(self, k):
+        # disk samples keep the identity frame of the reference (actuator.py:50-55)
+        return np.eye(3)[k].copy() if self.is_disk_sample else self._k(6 + 3 * k, 9 + 3 * k)
+
     position = property(lambda s: s._k(15, 18))
     position_lat = property(lambda s: s._k(0, 3))
     velocity = property(lambda s: s._k(3, 6))
-    e_chord = property(lambda s: s._k(6, 9))
-    e_normal = property(lambda s: s._k(9, 12))
-    e_span = property(lambda s: s._k(12, 15))
+    e_chord = property(lambda s: s._frame(0))
+    e_normal = property(lambda s: s._frame(1))
+    e_span = property(lambda s: s._frame(2))
     sampled_rho = property(lambda s: float(s._sim._alm_results()[0][s.global_id]))
     sampled_u = property(lambda s: s._sim._alm_results()[1][s.global_id].copy())
     blade_force = property(lambda s: s._sim._alm_results()[2][s.global_id].copy())
@@ -192,9 +197,12 @@ class Simulation:
                         gid += 1
                     self._line_groups.append((comp, spec, slice(start, gid)))
                 elif isinstance(spec, DiskSpec):
-                    raise ConfigError(
-                        f"component {comp.name!r}: actuator disks are not on the device path "
-                        "yet (SURVEY.md section 8 row f2)")
+                    offs, areas = spec.sample_offsets()
+                    start = gid
+                    for si in range(len(areas)):
+                        self.points.append(ActuatorPoint(self, gid, area=areas[si], disk=True))
+                        gid += 1
+                    self._disk_groups.append((comp, spec, offs, areas, slice(start, gid)))
         P = len(self.points)
         self._kin = np.zeros((P, KIN_COLS))
         self._pos_m = np.zeros((P, 3))
@@ -239,6 +247,28 @@ class Simulation:
         a.rho_ref = self.units.rho_ref
         a.force_dt2 = self.units.force_dt2
         a.force_den = self.units.force_den
+        if self._disk_groups:
+            # one ring = `sectors` consecutive samples (DiskSpec.sample_offsets)
+            ring_first, ring_count, ring_ct = [], [], []
+            point_ring = np.full(P, -1, dtype=np.int32)
+            for comp, spec, offs, areas, sl in self._disk_groups:
+                for j in range(spec.rings):
+                    first = sl.start + j * spec.sectors
+                    point_ring[first:first + spec.sectors] = len(ring_first)
+                    ring_first.append(first)
+                    ring_count.append(spec.sectors)
+                    ring_ct.append(float(spec.thrust_coefficient[j]))
+            s["point_ring"] = point_ring
+            s["area"] = np.array([p.area for p in self.points])
+            s["ring_first"] = np.array(ring_first, dtype=np.int32)
+            s["ring_count"] = np.array(ring_count, dtype=np.int32)
+            s["ring_ct"] = np.array(ring_ct, dtype=np.float64)
+            a.point_ring = s["point_ring"].ctypes.data_as(I)
+            a.area = s["area"].ctypes.data_as(D)
+            a.n_rings = len(ring_first)
+            a.ring_first = s["ring_first"].ctypes.data_as(I)
+            a.ring_count = s["ring_count"].ctypes.data_as(I)
+            a.ring_ct = s["ring_ct"].ctypes.data_as(D)
         _lib.check(_lib.load().lbw_alm_configure(self._domain, _lib.ctypes.byref(a)), "ALM")
         self._kin_stale = False
         self._topo_pending = False
@@ -272,6 +302,9 @@ class Simulation:
                                             ("lframe", (P, 3, 3)))}
         line_first = np.full(C, -1, dtype=np.int32)
         line_count = np.zeros(C, dtype=np.int32)
+        is_disk = np.zeros(C, dtype=np.int32)
+        disk_center = np.zeros((C, 12))
+        disks = {id(comp): (spec, offs, sl) for comp, spec, offs, areas, sl in self._disk_groups}
         for c, comp in enumerate(comps):
             arr["rel_p"][c] = comp.relative.p
             arr["rel_T"][c] = comp.relative.T
@@ -289,8 +322,17 @@ class Simulation:
                 arr["off"][g0:g0 + spec.n_points] = spec.offsets
                 arr["orient"][g0:g0 + spec.n_points] = spec.orientations
                 arr["lframe"][g0:g0 + spec.n_points] = spec.frames_local()
+            if id(comp) in disks:
+                spec, offs, sl = disks[id(comp)]
+                line_first[c], line_count[c] = sl.start, sl.stop - sl.start
+                is_disk[c] = 1
+                disk_center[c, :3] = spec.center.p
+                disk_center[c, 3:] = spec.center.T.ravel()
+                arr["off"][sl] = offs
+                arr["orient"][sl] = np.eye(3)
+                arr["lframe"][sl] = np.eye(3)
         par = np.asarray(parent, dtype=np.int32)
-        self._kin_arrays = (arr, line_first, line_count, par)   # keep alive for the call
+        self._kin_arrays = (arr, line_first, line_count, par, is_disk, disk_center)
         k = _lib.KinDesc()
         k.n_components = C
         k.parent = _lib.iptr(par)
@@ -302,6 +344,8 @@ class Simulation:
         k.local_frames = _lib.dptr(arr["lframe"])
         k.dx = self.units.dx
         k.advance_first = 0
+        k.is_disk = _lib.iptr(is_disk)
+        k.disk_center = _lib.dptr(disk_center)
         _lib.check(_lib.load().lbw_alm_configure_kinematics(self._domain, _lib.ctypes.byref(k)),
                    "kinematics")
         self._flat = comps
@@ -336,27 +380,8 @@ class Simulation:
         """Positions, velocities and frames from the topology state
         (sim.py:167-191), stacked: identical doubles, O(1) numpy calls per
         line."""
-        kin = self._kin
-        for comp, spec, sl in self._line_groups:
-            frames = comp.point_frames_arr
-            n = spec.n_points
-            self._pos_m[sl] = comp.point_positions_arr
-            kin[sl, 3:6] = comp.point_velocities
-            for col, v in ((6, spec.chord_local), (9, spec.normal_local), (12, spec.span_local)):
-                kin[sl, col:col + 3] = np.matmul(
-                    frames, np.broadcast_to(v, (n, 3))[:, :, None])[:, :, 0]
-        if self._line_groups:
-            L = np.asarray(self.grid.global_dims, dtype=np.float64)
-            periodic = np.asarray(self.grid.periodicity, dtype=bool)
-            lat = self._pos_m / self.units.dx
-            lat = np.where(periodic, np.mod(lat, L), lat)
-            bad = (~periodic) & ((lat < 0.0) | (lat >= L))
-            if np.any(bad):
-                p, k = np.argwhere(bad)[0]
-                raise ConfigError(
-                    f"position component {lat[p, k]} outside the non-periodic domain")
-            kin[:, 0:3] = lat
-            kin[:, 15:18] = self._pos_m
+        fill_kinematics(self._line_groups, self._disk_groups, self.grid, self.units.dx,
+                        self._kin, self._pos_m)
 
     def _alm_results(self):
         if self._results is None:
@@ -502,3 +527,84 @@ def run_simulation(cfg):
         return sim.run()
     finally:
         sim.close()
+
+
+def fill_kinematics(line_groups, disk_groups, grid, dx, kin, pos_m):
+    """Host kinematics rows (P,18) of every actuator point from the current
+    topology state (Simulation.refresh_points, sim.py:167-191)."""
+    for comp, spec, sl in line_groups:
+        frames = comp.point_frames_arr
+        n = spec.n_points
+        pos_m[sl] = comp.point_positions_arr
+        kin[sl, 3:6] = comp.point_velocities
+        for col, v in ((6, spec.chord_local), (9, spec.normal_local), (12, spec.span_local)):
+            kin[sl, col:col + 3] = np.matmul(frames, np.broadcast_to(v, (n, 3))[:, :, None])[:, :, 0]
+    for comp, spec, offs, areas, sl in disk_groups:
+        # sim.py:182-187; the disk axis (centre frame +x) rides in e_chord
+        cp, cT = comp.point_positions_arr[0], comp.point_frames_arr[0]
+        pos_m[sl] = cp[None, :] + offs @ cT.T
+        kin[sl, 3:6] = comp.point_velocities[0]
+        kin[sl, 6:9] = cT @ _EX
+        kin[sl, 9:15] = (0.0, 1.0, 0.0, 0.0, 0.0, 1.0)
+    if line_groups or disk_groups:
+        L = np.asarray(grid.global_dims, dtype=np.float64)
+        periodic = np.asarray(grid.periodicity, dtype=bool)
+        lat = pos_m / dx
+        lat = np.where(periodic, np.mod(lat, L), lat)
+        bad = (~periodic) & ((lat < 0.0) | (lat >= L))
+        if np.any(bad):
+            p, k = np.argwhere(bad)[0]
+            raise ConfigError(f"position component {lat[p, k]} outside the non-periodic domain")
+        kin[:, 0:3] = lat
+        kin[:, 15:18] = pos_m
+
+
+def point_groups(cfg):
+    """(point metadata, line groups, disk groups) in global-id order
+    (topology -> component -> point, sim.py:113-143).  Metadata rows are
+    dicts with chord, element_length, twist, polar, area, disk."""
+    meta, lines, disks = [], [], []
+    for topo in cfg.topologies:
+        for comp in topo.components:
+            spec = comp.discretization
+            if isinstance(spec, LineSpec):
+                start = len(meta)
+                for pi in range(spec.n_points):
+                    pid = spec.polar[pi]
+                    meta.append(dict(chord=spec.chord[pi], element_length=spec.element_length[pi],
+                                     twist=spec.twist[pi], area=0.0, disk=False,
+                                     polar=cfg.polars.get(pid) if pid is not None else None))
+                lines.append((comp, spec, slice(start, len(meta))))
+            elif isinstance(spec, DiskSpec):
+                offs, areas = spec.sample_offsets()
+                start = len(meta)
+                for si in range(len(areas)):
+                    meta.append(dict(chord=0.0, element_length=0.0, twist=0.0, area=areas[si],
+                                     disk=True, polar=None))
+                disks.append((comp, spec, offs, areas, slice(start, len(meta))))
+    return meta, lines, disks
+
+
+class HostKinematics:
+    """The host half of a Simulation's actuator path without a device:
+    per-step kinematics rows of a configuration (used to drive the CPU
+    oracle with the same actuator motion)."""
+
+    def __init__(self, cfg):
+        self.cfg, self.units = cfg, cfg.units
+        self.grid = SlabGrid(cfg.cells, cfg.periodicity, 1, 0)
+        wind_lat = cfg.units.velocity_to_lattice(np.asarray(cfg.wind, dtype=np.float64))
+        self.boundary = BoundarySpec(cfg.boundary_kind, u_in_lat=wind_lat)
+        meta, self._line_groups, self._disk_groups = point_groups(cfg)
+        self.points = [type("PointMeta", (), m)() for m in meta]
+        self._kin = np.zeros((len(meta), KIN_COLS))
+        self._pos_m = np.zeros((len(meta), 3))
+
+    def refresh(self):
+        fill_kinematics(self._line_groups, self._disk_groups, self.grid, self.units.dx,
+                        self._kin, self._pos_m)
+        return self._kin.copy()
+
+    def advance(self):
+        for topo in self.cfg.topologies:
+            topo.advance(self.units.dt)

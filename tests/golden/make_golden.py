@@ -232,6 +232,52 @@ def gen_rotor(tag, cells, periodicity, boundary, position, tmp):
     np.savez_compressed(os.path.join(HERE, f"rotor_{tag}.npz"), **out)
 
 
+DISK_YAML = """
+name: d
+components:
+  - name: mast
+    position: [2.0, 2.0, 2.0]
+  - name: rotor
+    parent: mast
+    discretization:
+      type: disk
+      radius: 1.0
+      rings: 2
+      sectors: 6
+      thrust_coefficient: [0.5, 0.3]
+"""
+
+
+def gen_disk(tmp):
+    """Actuator disk in the style of test_sim.py:18-31 (16^3, 2 rings x 6)."""
+    with open(os.path.join(tmp, "d.yaml"), "w") as fh:
+        fh.write(DISK_YAML)
+    raw = {"domain": {"cells": [16, 16, 16]},
+           "fluid": {"kinematic_viscosity": 5.0, "wind": [8.0, 0.0, 0.0]},
+           "resolution": {"cells_per_diameter": 8, "reference_diameter": 2.0, "mach": 0.1},
+           "run": {"steps": 0, "collision": {"operator": "cumulant"}},
+           "turbines": [{"file": "d.yaml"}]}
+    cfg = parse_config(raw, base_dir=tmp)
+    sim = Simulation(cfg)
+    P = len(sim.points)
+    nsteps = 6
+    pos = np.zeros((nsteps, P, 3))
+    samples = np.zeros((nsteps, P, 4))
+    blade = np.zeros((nsteps, P, 3))
+    for n in range(nsteps):
+        sim.step()
+        for p in sim.points:
+            pos[n, p.global_id] = p.position_lat
+            samples[n, p.global_id, 0] = p.sampled_rho
+            samples[n, p.global_id, 1:] = p.sampled_u
+            blade[n, p.global_id] = p.blade_force
+    out = {"pos": pos, "samples": samples, "blade": blade, "f_final": _gather(sim),
+           "force_final": sim.fields[0].interior_force.copy(),
+           "area": np.array([p.area for p in sim.points]), "disk_yaml": np.array(DISK_YAML)}
+    sim.close()
+    np.savez_compressed(os.path.join(HERE, "disk.npz"), **out)
+
+
 def main():
     import tempfile
     _kernels.warm_up()
@@ -244,6 +290,7 @@ def main():
                   (0.9, 0.3, 0.0), tmp)
         gen_rotor("inflow", (16, 12, 12), (False, True, True), "velocity_inflow_outflow",
                   (0.9, 0.75, 0.0), tmp)
+        gen_disk(tmp)
     print("golden vectors written to", HERE, "with lbwind", lbwind.__version__)
 
 

@@ -85,9 +85,27 @@ def oracle_for(sim):
                   "polar": [None if p.polar is None else (p.polar.alpha, p.polar.cl, p.polar.cd)
                             for p in sim.points],
                   "vscale": u.velocity_scale, "rho_ref": u.rho_ref, "dt2": u.dt ** 2,
-                  "den": u.rho_ref * u.dx ** 4}
+                  "den": u.rho_ref * u.dx ** 4,
+                  "area": np.array([p.area for p in sim.points]),
+                  "disks": [(sl.start, spec.rings, spec.sectors, spec.thrust_coefficient)
+                            for comp, spec, offs, areas, sl in sim._disk_groups]}
     ref = orc.OracleSim(cfg.cells, periodic=cfg.periodicity, op=cfg.operator, omega=u.omega,
                         rates=cfg.higher_order_rates, boundary=cfg.boundary_kind,
                         u_in=sim.boundary.u_in_lat, points=points)
     ref.initialize_equilibrium(1.0, sim.boundary.u_in_lat, product=(cfg.operator == "cumulant"))
     return ref
+
+
+def disk_config(disk_yaml):
+    """(RunConfig, TemporaryDirectory) of the golden actuator-disk run
+    (tests/golden/make_golden.py gen_disk)."""
+    from paper_2402_13171_b200 import parse_config
+    tmp = tempfile.TemporaryDirectory()
+    with open(os.path.join(tmp.name, "d.yaml"), "w") as fh:
+        fh.write(disk_yaml)
+    raw = {"domain": {"cells": [16, 16, 16]},
+           "fluid": {"kinematic_viscosity": 5.0, "wind": [8.0, 0.0, 0.0]},
+           "resolution": {"cells_per_diameter": 8, "reference_diameter": 2.0, "mach": 0.1},
+           "run": {"steps": 0, "collision": {"operator": "cumulant"}},
+           "turbines": [{"file": "d.yaml"}]}
+    return parse_config(raw, base_dir=tmp.name), tmp

@@ -147,7 +147,7 @@ def test_kinematics_bitwise_vs_reference(golden, tag):
     sim.cfg, sim.units = cfg, cfg.units
     from paper_2402_13171_b200.sim import SlabGrid
     sim.grid = SlabGrid(cfg.cells, cfg.periodicity, 1, 0)
-    sim._line_groups = []
+    sim._line_groups, sim._disk_groups = [], []
     gid = 0
     for topo in cfg.topologies:
         for comp in topo.components:

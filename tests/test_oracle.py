@@ -110,3 +110,25 @@ def test_oracle_against_live_reference(reference_lbwind):
         ref = collide(f, F, cfg)
         out, _ = orc.collide_batch(op, f, F, 1.61, (0.7, 1.5, 1.1, 1.9))
         assert np.array_equal(out, ref), op
+
+
+def test_disk_oracle_matches_reference(golden):
+    """Actuator disk (actuator.py:149-183): host kinematics bit-identical, the
+    oracle's samples / ring forces / populations match the reference."""
+    from paper_2402_13171_b200.sim import HostKinematics
+    from tests.scenarios import disk_config, oracle_for
+    g = golden("disk.npz")
+    cfg, tmp = disk_config(str(g["disk_yaml"]))
+    host = HostKinematics(cfg)
+    ref = oracle_for(host)
+    for n in range(g["pos"].shape[0]):
+        kin = host.refresh()
+        assert np.array_equal(kin[:, 0:3], g["pos"][n])
+        ref.step(kin)
+        host.advance()
+        np.testing.assert_allclose(ref.samples, g["samples"][n], rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(ref.blade, g["blade"][n], rtol=1e-10, atol=1e-13)
+    np.testing.assert_allclose(ref.interior, g["f_final"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(ref.force[1:-1, 1:-1, 1:-1], g["force_final"], rtol=1e-10,
+                               atol=1e-18)
+    tmp.cleanup()
