@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define LBW_ABI_VERSION 1
+#define LBW_ABI_VERSION 2
 
 /* status codes */
 #define LBW_OK 0
@@ -58,6 +58,11 @@ extern "C" {
 /* arithmetic flavour */
 #define LBW_MODE_EXACT 0
 #define LBW_MODE_FAST 1
+
+/* population / force storage (run.precision, config.py:30, _kernels.py:5-7):
+ * arithmetic is fp64 either way; SINGLE stores fp32 and rounds on store */
+#define LBW_PREC_DOUBLE 0
+#define LBW_PREC_SINGLE 1
 
 /* outer boundary along x (halo.py:122-141, BoundarySpec.KINDS) */
 #define LBW_BC_PERIODIC 0
@@ -124,7 +129,9 @@ typedef struct lbw_domain_desc {
     int32_t nranks;          /* number of slabs                              */
     int32_t feq_in_given;    /* 1: use feq_in below for the inflow ghost     */
     double feq_in[27];       /* equilibrium_pdf(1, u_in) as the host computed it */
-    int64_t reserved[8];
+    int32_t precision;       /* LBW_PREC_* (host arrays stay fp64 either way)  */
+    int32_t reserved32;
+    int64_t reserved[7];
 } lbw_domain_desc;
 
 int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out);

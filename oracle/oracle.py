@@ -247,8 +247,20 @@ def route_single_block(records, dims, periodic):
     return out
 
 
-def spread(records, force, dims, dt2, den):
-    """spread_forces (actuator.py:204-247) into a ghosted block at origin 0."""
+def _identity(a):
+    return a
+
+
+def round_f32(a):
+    """Value a float32 array stores for `a` (numpy assignment rounds to
+    nearest even)."""
+    return np.asarray(a, dtype=np.float64).astype(np.float32).astype(np.float64)
+
+
+def spread(records, force, dims, dt2, den, rnd=_identity):
+    """spread_forces (actuator.py:204-247) into a ghosted block at origin 0.
+    rnd models the storage dtype of `force`: `+=` on a float32 array rounds
+    after every addition."""
     nx, ny, nz = dims
     for gid, pos, f_newton in records:
         f_lat = np.asarray(f_newton, dtype=np.float64) * dt2 / den
@@ -271,7 +283,8 @@ def spread(records, force, dims, dt2, den):
                     lz = cells[2][k]
                     if not 0 <= lz < nz or ws[2][k] == 0.0:
                         continue
-                    force[lx + 1, ly + 1, lz + 1, :] += (wxy * ws[2][k]) * f_lat
+                    force[lx + 1, ly + 1, lz + 1, :] = rnd(
+                        force[lx + 1, ly + 1, lz + 1, :] + (wxy * ws[2][k]) * f_lat)
 
 
 # ------------------------------------------------------------ single block
@@ -283,12 +296,16 @@ class OracleSim:
     (alpha, cl, cd) tuples or None per point), vscale, rho_ref, dt2, den.
     step(kin) takes the (P,15) kinematics of this step (lattice position,
     velocity, e_chord, e_normal, e_span) from the caller.
+    dtype float32 models ``precision: single``: every array keeps fp64
+    arithmetic but holds float32-representable values, rounded wherever the
+    reference stores into its float32 fields (_kernels.py:5-7, 342-353).
     """
 
     def __init__(self, cells, periodic=(True, True, True), op="cumulant", omega=1.0,
                  rates=(1.0, 1.0, 1.0, 1.0), boundary="periodic", u_in=(0.0, 0.0, 0.0),
-                 points=None):
+                 points=None, dtype=np.float64):
         self.dims = tuple(int(c) for c in cells)
+        self.rnd = round_f32 if np.dtype(dtype) == np.float32 else _identity
         nx, ny, nz = self.dims
         shape = (nx + 2, ny + 2, nz + 2)
         self.periodic = tuple(bool(p) for p in periodic)
@@ -315,9 +332,9 @@ class OracleSim:
         rho_arr = np.broadcast_to(np.asarray(rho, np.float64), n)
         u_arr = np.broadcast_to(np.asarray(u, np.float64), n + (3,))
         eq = product_equilibrium(rho_arr, u_arr) if product else equilibrium_pdf(rho_arr, u_arr)
-        self.f[1:-1, 1:-1, 1:-1] = eq
-        self.macro[1:-1, 1:-1, 1:-1, 0] = rho_arr
-        self.macro[1:-1, 1:-1, 1:-1, 1:4] = u_arr
+        self.f[1:-1, 1:-1, 1:-1] = self.rnd(eq)
+        self.macro[1:-1, 1:-1, 1:-1, 0] = self.rnd(rho_arr)
+        self.macro[1:-1, 1:-1, 1:-1, 1:4] = self.rnd(u_arr)
         self.force[...] = 0.0
 
     def _actuators(self, kin):
@@ -345,12 +362,15 @@ class OracleSim:
             records.append((p, kin[p, 0:3].copy(), -self.blade[p]))
         routed = route_single_block(records, self.dims, self.periodic)
         self.force[...] = 0.0
-        spread(routed, self.force, self.dims, pts["dt2"], pts["den"])
+        spread(routed, self.force, self.dims, pts["dt2"], pts["den"], self.rnd)
 
     def step(self, kin=None):
         if self.points is not None:
             self._actuators(np.asarray(kin, dtype=np.float64))
         collide_block(self.op, self.f, self.force, self.macro, self.omega, self.rates)
+        if self.rnd is not _identity:
+            self.f[...] = self.rnd(self.f)
+            self.macro[...] = self.rnd(self.macro)
         m = self.macro[1:-1, 1:-1, 1:-1]
         if not np.all(np.isfinite(m)):
             bad = np.argwhere(~np.isfinite(m))[0]
@@ -358,11 +378,11 @@ class OracleSim:
                                       "density" if bad[3] == 0 else "velocity"))
         fill_ghosts(self.f, self.periodic)
         if self.boundary == "velocity_inflow_outflow":
-            feq_in = np.ascontiguousarray(equilibrium_pdf(1.0, self.u_in))
+            feq_in = np.ascontiguousarray(self.rnd(equilibrium_pdf(1.0, self.u_in)))
             nx, ny, nz = self.dims
             lib().orc_apply_inflow_outflow(_p(self.f), nx, ny, nz, _p(feq_in))
             self.macro[0, :, :, 0] = 1.0
-            self.macro[0, :, :, 1:4] = self.u_in
+            self.macro[0, :, :, 1:4] = self.rnd(self.u_in)
             self.force[0] = 0.0
             self.macro[-1] = self.macro[-2]
             self.force[-1] = self.force[-2]
@@ -372,4 +392,5 @@ class OracleSim:
 
     def recompute_moments(self):
         moments_block(self.f, self.force, self.macro)
+        self.macro[...] = self.rnd(self.macro)
         return self.macro[1:-1, 1:-1, 1:-1].copy()

@@ -17,6 +17,10 @@ from .errors import ConfigError, NumericalAbort
 LIB_PATH = os.environ.get("LBW_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "liblbw.so")   # LBW_LIB: A/B builds of the library
 
+ABI_VERSION = 2
+LBW_PREC_DOUBLE = 0
+LBW_PREC_SINGLE = 1
+
 LBW_OK = 0
 LBW_EINVAL = -1
 LBW_ECUDA = -2
@@ -54,7 +58,9 @@ class DomainDesc(ctypes.Structure):
         ("nranks", ctypes.c_int32),
         ("feq_in_given", ctypes.c_int32),
         ("feq_in", ctypes.c_double * 27),
-        ("reserved", ctypes.c_int64 * 8),
+        ("precision", ctypes.c_int32),
+        ("reserved32", ctypes.c_int32),
+        ("reserved", ctypes.c_int64 * 7),
     ]
 
 
@@ -181,7 +187,7 @@ def load():
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.lbw_abi_version() != 1:
+        if lib.lbw_abi_version() != ABI_VERSION:
             raise LibraryMissing("liblbw.so ABI version mismatch")
         _lib = lib
         return lib

@@ -24,6 +24,7 @@
 //                          float atomics.  CTA 0 also clears the other force
 //                          set (last read by this step's K4) for the next step.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -89,6 +90,9 @@ struct KinDev {
     const int32_t* is_disk;
     const double* disk_center;
     double* cs;
+    double* spin_hist;   // (3, nc, 9): spin state of step j in slot j % 3
+    double* cs_hist;     // (3, nc, kCS)
+    int32_t hist_slot;
     double dx;
 };
 
@@ -97,7 +101,7 @@ struct AlmState {
     double *chord = nullptr, *elen = nullptr, *twist = nullptr;
     int32_t *polar_index = nullptr, *polar_offset = nullptr, *polar_rows = nullptr;
     double *p_alpha = nullptr, *p_cl = nullptr, *p_cd = nullptr;
-    double* kin = nullptr;       // (2,P,18): per step parity
+    double* kin = nullptr;       // (3,P,18): slot m % 3 (kinematics run a step ahead)
     double *samples = nullptr;   // (2,P,4)
     double *blade = nullptr;     // (2,P,3)
     double *flat = nullptr;      // (P,3)
@@ -115,7 +119,11 @@ struct AlmState {
     int ring_pos = 0;
     int64_t kin_queued_step = -1;  // host kinematics uploaded for this step
     int64_t ready_step = -1;       // step whose actuator chain is queued and valid
-    size_t fill_smem = 0;
+    // device kinematics run on their own stream, one step ahead
+    cudaStream_t kin_stream = nullptr;
+    cudaEvent_t ev_kin_done = nullptr;
+    cudaEvent_t ev_chain_done[2] = {nullptr, nullptr};  // chain of a step parity done
+    int64_t kin_valid[3] = {-1, -1, -1};  // step whose kinematics kin[slot] holds
     // device kinematics
     bool kin_device = false;
     int32_t nc = 0;
@@ -124,13 +132,16 @@ struct AlmState {
     double *k_rel_p = nullptr, *k_rel_T = nullptr, *k_axis = nullptr, *k_rate = nullptr;
     double *k_rstep = nullptr, *k_spin = nullptr, *k_off = nullptr, *k_orient = nullptr;
     double *k_lframe = nullptr, *k_cs = nullptr;
+    double *k_spin_hist = nullptr, *k_cs_hist = nullptr;
     int32_t* k_is_disk = nullptr;
     double* k_disk_center = nullptr;
     double k_dx = 1.0;
     int64_t kin_state_step = 0;  // step whose kinematics the device spins represent
     std::vector<void*> allocs;
 
-    AlmDev dev(int parity) const {
+    // device view for step m: outputs by parity, kinematics by m % 3
+    AlmDev dev(int64_t m) const {
+        const int parity = (int)(m & 1);
         AlmDev a;
         a.n = n;
         a.chord = chord;
@@ -146,7 +157,7 @@ struct AlmState {
         a.rho_ref = rho_ref;
         a.dt2 = dt2;
         a.den = den;
-        a.kin = kin + (size_t)parity * n * kKin;
+        a.kin = kin + (size_t)(m % 3) * n * kKin;
         a.samples = samples + (size_t)parity * n * 4;
         a.blade = blade + (size_t)parity * n * 3;
         a.flat = flat;
@@ -181,6 +192,9 @@ struct AlmState {
         k.is_disk = k_is_disk;
         k.disk_center = k_disk_center;
         k.cs = k_cs;
+        k.spin_hist = k_spin_hist;
+        k.cs_hist = k_cs_hist;
+        k.hist_slot = 0;
         k.dx = k_dx;
         return k;
     }
@@ -190,7 +204,7 @@ struct AlmState {
 struct MacroDev {
     int kind;
     double uniform[4];
-    const double* buf;
+    const void* buf;   // population buffer (storage type per g.single)
     int pull;
     ForceView fv;
     const double* dense;
@@ -269,8 +283,8 @@ __device__ double np_mod(double a, double b) {
 // parallel.  Layout per component in smem: params[kKP] then state[kCS].
 // rel_p 3, rel_T 9, axis 3, rate 1, rstep 9, spin 9, parent 1, first 1, is_disk 1, disk p 3, T 9
 constexpr int kKP = 49;
-__global__ void k_kinematics(KinDev k, AlmDev a, Geom g, int per_x, int advance) {
-    extern __shared__ double ksm[];
+__device__ void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g, int per_x,
+                               int advance, double* ksm) {
     double* prm = ksm;                         // (nc, kKP)
     double* cs = ksm + (size_t)k.nc * kKP;     // (nc, kCS)
     for (int i = threadIdx.x; i < k.nc * kKP; i += blockDim.x) {
@@ -362,8 +376,10 @@ __global__ void k_kinematics(KinDev k, AlmDev a, Geom g, int per_x, int advance)
     __syncthreads();
     // persist spin + component state (downloadable), evaluate the points
     for (int i = threadIdx.x; i < k.nc * 9; i += blockDim.x)
-        k.spin[i] = prm[(i / 9) * kKP + 25 + i % 9];
-    for (int i = threadIdx.x; i < k.nc * kCS; i += blockDim.x) k.cs[i] = cs[i];
+        k.spin[i] = k.spin_hist[(int64_t)k.hist_slot * k.nc * 9 + i] =
+            prm[(i / 9) * kKP + 25 + i % 9];
+    for (int i = threadIdx.x; i < k.nc * kCS; i += blockDim.x)
+        k.cs[i] = k.cs_hist[(int64_t)k.hist_slot * k.nc * kCS + i] = cs[i];
     const int64_t dims[3] = {g.nxg, g.ny, g.nz};
     const int per[3] = {per_x, g.per_y, g.per_z};
     for (int p = threadIdx.x; p < a.n; p += blockDim.x) {
@@ -411,13 +427,28 @@ __global__ void k_kinematics(KinDev k, AlmDev a, Geom g, int per_x, int advance)
     }
 }
 
+__global__ void k_kinematics(KinDev k, AlmDev a, Geom g, int per_x, int advance) {
+    extern __shared__ double ksm[];
+    kinematics_cta(k, a, g, per_x, advance, ksm);
+}
+
 // Macro (rho, u) of global cell (gx,gy,gz), following the ghost semantics
 // of PdfField.macro (fields.py:35-36, halo.py:144-160).  Returns MA_REMOTE
 // (nothing written) when the cell belongs to another slab, MA_OWNED for a
-// cell of this slab, MA_CONST for a ghost value every slab knows.
+// cell of this slab, MA_CONST for a ghost value every slab knows.  Values
+// are those the reference's macro array of the storage dtype holds.
 enum { MA_REMOTE = 0, MA_OWNED = 1, MA_CONST = 2 };
+__device__ int macro_at_raw(const Geom& g, const MacroDev& m, int64_t gx, int64_t gy, int64_t gz,
+                            double out[4]);
 __device__ int macro_at(const Geom& g, const MacroDev& m, int64_t gx, int64_t gy, int64_t gz,
-                         double out[4]) {
+                        double out[4]) {
+    const int code = macro_at_raw(g, m, gx, gy, gz, out);
+    if (code != MA_REMOTE && g.single)
+        for (int k = 0; k < 4; ++k) out[k] = stored<float>(out[k]);
+    return code;
+}
+__device__ int macro_at_raw(const Geom& g, const MacroDev& m, int64_t gx, int64_t gy, int64_t gz,
+                            double out[4]) {
     const double ghost0[4] = {1.0, 0.0, 0.0, 0.0};
     auto put = [&](const double* v) {
         for (int k = 0; k < 4; ++k) out[k] = v[k];
@@ -462,10 +493,10 @@ __device__ int macro_at(const Geom& g, const MacroDev& m, int64_t gx, int64_t gy
         return MA_OWNED;
     }
     double f[27];
-    if (m.pull) load_cell<true>(m.buf, g, (int)x, (int)gy, (int)gz, f);
-    else load_cell<false>(m.buf, g, (int)x, (int)gy, (int)gz, f);
+    if (m.pull) load_cell_any<true>(m.buf, g, (int)x, (int)gy, (int)gz, f);
+    else load_cell_any<false>(m.buf, g, (int)x, (int)gy, (int)gz, f);
     double Fx, Fy, Fz;
-    load_force(m.fv, g, (int)x, (int)gy, (int)gz, Fx, Fy, Fz);
+    load_force_any(m.fv, g, (int)x, (int)gy, (int)gz, Fx, Fy, Fz);
     const Macro mm = moments_exact(f, Fx, Fy, Fz, 1.0);
     out[0] = mm.rho;
     out[1] = mm.ux;
@@ -479,28 +510,6 @@ __device__ __forceinline__ double dot3(const double* a, const double* b) {
 }
 
 // np.interp on one value (numpy compiled_base.c arr_interp semantics)
-__device__ double interp1(double x, const double* xp, const double* fp, int n) {
-    if (isnan(x)) return x;
-    if (x < xp[0]) return fp[0];
-    if (x > xp[n - 1]) return fp[n - 1];
-    if (x == xp[n - 1]) return fp[n - 1];
-    int lo = 0, hi = n - 1;  // xp[lo] <= x < xp[hi]
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (xp[mid] <= x) lo = mid;
-        else hi = mid;
-    }
-    const int j = lo;
-    if (xp[j] == x) return fp[j];
-    const double slope = (fp[j + 1] - fp[j]) / (xp[j + 1] - xp[j]);
-    double r = slope * (x - xp[j]) + fp[j];
-    if (isnan(r)) {
-        r = slope * (x - xp[j + 1]) + fp[j + 1];
-        if (isnan(r) && fp[j] == fp[j + 1]) r = fp[j];
-    }
-    return r;
-}
-
 // Roma 3-point kernel (actuator.py:100-110)
 __device__ __forceinline__ double roma(double r) {
     const double a = fabs(r);
@@ -512,9 +521,39 @@ __device__ __forceinline__ double roma(double r) {
     return 0.0;
 }
 
-// blade-element force on the BLADE (actuator.py:117-146, sim.py:218-235)
-__device__ void blade_force(const AlmDev& a, int p, const double* kin, const double* acc,
-                            double* blade) {
+// np.interp for a whole warp: every lane gets the same result.  The
+// bracketing index (largest j with xp[j] <= x, polars.py:65-80 tables are
+// increasing) is counted with ballots over 32-row chunks instead of a
+// binary search of dependent loads.
+__device__ int interp_index_warp(double x, const double* xp, int n, int lane) {
+    int cnt = 0;
+    for (int k0 = 0; k0 < n; k0 += 32) {
+        const int k = k0 + lane;
+        const bool le = k < n && xp[k] <= x;
+        cnt += __popc(__ballot_sync(0xffffffffu, le));
+    }
+    return cnt - 1;
+}
+__device__ double interp_at(double x, const double* xp, const double* fp, int n, int j) {
+    if (isnan(x)) return x;
+    if (x < xp[0]) return fp[0];
+    if (x > xp[n - 1]) return fp[n - 1];
+    if (x == xp[n - 1]) return fp[n - 1];
+    if (xp[j] == x) return fp[j];
+    const double slope = (fp[j + 1] - fp[j]) / (xp[j + 1] - xp[j]);
+    double r = slope * (x - xp[j]) + fp[j];
+    if (isnan(r)) {
+        r = slope * (x - xp[j + 1]) + fp[j + 1];
+        if (isnan(r) && fp[j] == fp[j + 1]) r = fp[j];
+    }
+    return r;
+}
+
+// blade-element force on the BLADE (actuator.py:117-146, sim.py:218-235),
+// evaluated by a whole warp (identical values on every lane; lane 0 raises
+// the flags): the polar lookups are one ballot round each.
+__device__ void blade_force_warp(const AlmDev& a, int p, const double* kin, const double* acc,
+                                 double* blade, int lane) {
     blade[0] = blade[1] = blade[2] = 0.0;
     const int pid = a.polar_index[p];
     if (pid < 0) return;
@@ -537,13 +576,14 @@ __device__ void blade_force(const AlmDev& a, int p, const double* kin, const dou
     const int off = a.polar_offset[pid], rows = a.polar_rows[pid];
     const double* xp = a.p_alpha + off;
     if (alpha < xp[0] || alpha > xp[rows - 1]) {
-        atomicOr(&a.clamp_flags[pid], 1);
+        if (lane == 0) atomicOr(&a.clamp_flags[pid], 1);
         alpha = fmin(fmax(alpha, xp[0]), xp[rows - 1]);
     }
-    const double cl = interp1(alpha, xp, a.p_cl + off, rows);
-    const double cd = interp1(alpha, xp, a.p_cd + off, rows);
+    const int j = isnan(alpha) ? 0 : interp_index_warp(alpha, xp, rows, lane);
+    const double cl = interp_at(alpha, xp, a.p_cl + off, rows, j < 0 ? 0 : j);
+    const double cd = interp_at(alpha, xp, a.p_cd + off, rows, j < 0 ? 0 : j);
     const double rho_phys = acc[0] * a.rho_ref;
-    if (!(rho_phys > 0.0)) atomicOr(a.error_flags, 1);
+    if (!(rho_phys > 0.0) && lane == 0) atomicOr(a.error_flags, 1);
     const double scale = 0.5 * rho_phys * speed * speed * a.chord[p] * a.elen[p];
     for (int c = 0; c < 3; ++c) blade[c] = scale * (cl * el[c] + cd * ed[c]);
 }
@@ -585,10 +625,8 @@ struct CubeArgs {
     double* peer[2];
 };
 
-__global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s, int phase, CubeArgs cube) {
-    const int p = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-    const int lane = threadIdx.x & 31;
-    if (p >= a.n) return;  // uniform per warp
+__device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, const ForceSet& s,
+                           int phase, const CubeArgs& cube, int p, int lane) {
     const double* kin = a.kin + (int64_t)p * kKin;
     int64_t j0[3];
     double t[3];
@@ -628,22 +666,22 @@ __global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s, int phase
     }
     int32_t* dc = a.dep_cell + (int64_t)p * 9;
     double* dw = a.dep_w + (int64_t)p * 9;
+    // Multi-slab: only points whose Roma support reaches this slab (their
+    // sampling cube is then complete: own + neighbour cells) are evaluated;
+    // per-point outputs come from the slab owning floor(x).  (Warp-uniform.)
+    const int64_t n0 = (int64_t)floor(kin[0]);
+    const int64_t ox = n0 - g.x0;
+    const bool owner = phase == 0 || (ox >= 0 && ox < g.nxl);
+    bool relevant = phase == 0;
+    for (int dxc = -1; dxc <= 1 && !relevant; ++dxc) {
+        int64_t c = n0 + dxc;
+        if (m.per_x) c = (c % g.nxg + g.nxg) % g.nxg;
+        relevant = c - g.x0 >= 0 && c - g.x0 < g.nxl;
+    }
+    double blade[3] = {0.0, 0.0, 0.0};
+    const bool disk = a.point_ring != nullptr && a.point_ring[p] >= 0;
+    if (relevant && !disk) blade_force_warp(a, p, kin, acc, blade, lane);
     if (lane == 0) {
-        // Multi-slab: only points whose Roma support reaches this slab (their
-        // sampling cube is then complete: own + neighbour cells) are
-        // evaluated; per-point outputs come from the slab owning floor(x).
-        const int64_t n0 = (int64_t)floor(kin[0]);
-        const int64_t ox = n0 - g.x0;
-        const bool owner = phase == 0 || (ox >= 0 && ox < g.nxl);
-        bool relevant = phase == 0;
-        for (int dxc = -1; dxc <= 1 && !relevant; ++dxc) {
-            int64_t c = n0 + dxc;
-            if (m.per_x) c = (c % g.nxg + g.nxg) % g.nxg;
-            relevant = c - g.x0 >= 0 && c - g.x0 < g.nxl;
-        }
-        double blade[3] = {0.0, 0.0, 0.0};
-        const bool disk = a.point_ring != nullptr && a.point_ring[p] >= 0;
-        if (relevant && !disk) blade_force(a, p, kin, acc, blade);
         for (int q = 0; q < 4; ++q) a.samples[p * 4 + q] = owner ? acc[q] : 0.0;
         for (int c = 0; c < 3; ++c) {
             a.blade[p * 3 + c] = owner ? blade[c] : 0.0;
@@ -661,21 +699,34 @@ __global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s, int phase
         const int64_t x = (int64_t)cxg - g.x0;
         if (cxg >= 0 && cy >= 0 && x >= 0 && x < g.nxl) {
             const int64_t row = x * g.ny + cy;
-            if (atomicCAS(&s.row_slot[row], -1, -2) == -1) {
-                const int32_t slot = atomicAdd(s.count, 1);
-                s.slot_row[slot] = (int32_t)row;
-                s.row_slot[row] = slot;
+            // claim the row for this step (tag) unless a point already did;
+            // keys of earlier steps are simply overwritten (no clearing)
+            unsigned long long* key = reinterpret_cast<unsigned long long*>(s.row_key + row);
+            unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(key);
+            while ((uint32_t)(old >> 32) != s.tag) {
+                const unsigned long long prev = atomicCAS(key, old, row_key_of(s.tag, -2));
+                if (prev == old) {
+                    const int32_t slot = atomicAdd(s.count, 1);
+                    s.slot_row[slot] = (int32_t)row;
+                    atomicExch(key, row_key_of(s.tag, slot));
+                    break;
+                }
+                old = prev;
             }
         }
     }
 }
 
+__global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s, int phase, CubeArgs cube) {
+    const int p = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    if (p >= a.n) return;  // uniform per warp
+    point_warp(a, g, m, s, phase, cube, p, threadIdx.x & 31);
+}
+
 // K4d: actuator-disk rings (actuator.py:149-183), one thread per ring, fixed
 // summation order.  Fluid force per sample = direction * thrust/area_ring *
 // area_i * axis; the blade force is its negation (sim.py:236-244).
-__global__ void k_alm_disks(AlmDev a) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= a.n_rings) return;
+__device__ void disk_ring(const AlmDev& a, int r) {
     const int first = a.ring_first[r], cnt = a.ring_count[r];
     const double ct = a.ring_ct[r];
     const double* k0 = a.kin + (int64_t)first * kKin;
@@ -710,73 +761,79 @@ __global__ void k_alm_disks(AlmDev a) {
     }
 }
 
-// K5: one CTA per used slot of set s.
-__global__ void k_alm_fill(AlmDev a, Geom g, ForceSet s) {
-    extern __shared__ unsigned char smem[];
-    const int32_t slot = blockIdx.x;
-    if (slot >= *s.count) return;
+__global__ void k_alm_disks(AlmDev a) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < a.n_rings) disk_ring(a, r);
+}
+
+// K5 for one claimed row, one warp: lanes own z = z0 + lane; the points
+// touching the row are visited in ascending id (ballot over chunks of 32),
+// so each cell's sum has the same order as K5 / the reference.
+__device__ void fill_row_warp(const AlmDev& a, const Geom& g, const ForceSet& s, int slot,
+                              int lane) {
     const int32_t row = s.slot_row[slot];
     const int64_t xg = row / g.ny + g.x0;
     const int32_t y = row % g.ny;
-    int32_t* list_p = reinterpret_cast<int32_t*>(smem);
-    double* list_w = reinterpret_cast<double*>(smem + ((a.n * 4 + 15) / 16) * 16);
-    __shared__ int32_t warp_tot[32];
-    __shared__ int32_t base;
-    if (threadIdx.x == 0) base = 0;
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-    // ordered compaction of the points touching row (xg, y), ascending id
-    for (int c0 = 0; c0 < a.n; c0 += blockDim.x) {
-        const int p = c0 + threadIdx.x;
-        bool hit = false;
-        double wxy = 0.0;
-        if (p < a.n) {
-            const int32_t* dc = a.dep_cell + (int64_t)p * 9;
-            const double* dw = a.dep_w + (int64_t)p * 9;
-            double wx = 0.0, wy = 0.0;
-            bool hx = false, hy = false;
-            for (int q = 0; q < 3; ++q) {
-                if (dc[q] == xg) { hx = true; wx = dw[q]; }
-                if (dc[3 + q] == y) { hy = true; wy = dw[3 + q]; }
-            }
-            hit = hx && hy;
-            wxy = wx * wy;
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, hit);
-        if (lane == 0) warp_tot[warp] = __popc(bal);
-        __syncthreads();
-        int off = base;
-        for (int w = 0; w < warp; ++w) off += warp_tot[w];
-        off += __popc(bal & ((1u << lane) - 1u));
-        if (hit) {
-            list_p[off] = p;
-            list_w[off] = wxy;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int tot = 0;
-            for (int w = 0; w < nwarp; ++w) tot += warp_tot[w];
-            base += tot;
-        }
-        __syncthreads();
-    }
-    const int nlist = base;
-    double* dst = s.pool + (int64_t)slot * 3 * g.zp;
-    for (int z = threadIdx.x; z < g.nz; z += blockDim.x) {
+    const int64_t row0 = (int64_t)slot * 3 * g.zp;
+    for (int z0 = 0; z0 < g.nz; z0 += 32) {
+        const int z = z0 + lane;
         double F[3] = {0.0, 0.0, 0.0};
-        for (int q = 0; q < nlist; ++q) {
-            const int p = list_p[q];
-            const int32_t* dc = a.dep_cell + (int64_t)p * 9 + 6;
-            const double* dw = a.dep_w + (int64_t)p * 9 + 6;
-            for (int k = 0; k < 3; ++k) {
-                if (dc[k] == z) {
-                    const double w = list_w[q] * dw[k];
-                    for (int c = 0; c < 3; ++c) F[c] += w * a.flat[p * 3 + c];
+        for (int c0 = 0; c0 < a.n; c0 += 32) {
+            const int pl = c0 + lane;
+            bool hit = false;
+            double wxy = 0.0;
+            if (pl < a.n) {
+                const int32_t* dc = a.dep_cell + (int64_t)pl * 9;
+                const double* dw = a.dep_w + (int64_t)pl * 9;
+                double wx = 0.0, wy = 0.0;
+                bool hx = false, hy = false;
+                for (int q = 0; q < 3; ++q) {
+                    if (dc[q] == xg) { hx = true; wx = dw[q]; }
+                    if (dc[3 + q] == y) { hy = true; wy = dw[3 + q]; }
+                }
+                hit = hx && hy;
+                wxy = wx * wy;
+            }
+            unsigned bal = __ballot_sync(0xffffffffu, hit);
+            while (bal) {
+                const int src = __ffs(bal) - 1;
+                bal &= bal - 1;
+                const double w2 = __shfl_sync(0xffffffffu, wxy, src);
+                const int p = c0 + src;
+                if (z < g.nz) {
+                    const int32_t* dc = a.dep_cell + (int64_t)p * 9 + 6;
+                    const double* dw = a.dep_w + (int64_t)p * 9 + 6;
+                    for (int k = 0; k < 3; ++k) {
+                        if (dc[k] == z) {
+                            const double w = w2 * dw[k];
+                            if (g.single)
+                                for (int c = 0; c < 3; ++c)
+                                    F[c] = stored<float>(F[c] + w * a.flat[p * 3 + c]);
+                            else
+                                for (int c = 0; c < 3; ++c) F[c] += w * a.flat[p * 3 + c];
+                        }
+                    }
                 }
             }
         }
-        for (int c = 0; c < 3; ++c) dst[(int64_t)c * g.zp + z] = F[c];
+        if (z < g.nz) {
+            if (g.single) {
+                float* dst = static_cast<float*>(s.pool) + row0;
+                for (int c = 0; c < 3; ++c) dst[(int64_t)c * g.zp + z] = (float)F[c];
+            } else {
+                double* dst = static_cast<double*>(s.pool) + row0;
+                for (int c = 0; c < 3; ++c) dst[(int64_t)c * g.zp + z] = F[c];
+            }
+        }
     }
+}
+
+// K5: one warp per claimed row of this step's set (4 rows per CTA)
+__global__ void k_alm_fill(AlmDev a, Geom g, ForceSet s) {
+    const int slot = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *s.next_count = 0;  // the set's next use
+    if (slot >= *s.count) return;  // uniform per warp
+    fill_row_warp(a, g, s, slot, threadIdx.x & 31);
 }
 
 template <class T>
@@ -801,9 +858,13 @@ double* alm_cube(const lbw_domain* d) { return alm_active(d) ? d->alm->cube : nu
 void alm_destroy(lbw_domain* d) {
     AlmState* s = d->alm;
     if (!s) return;
+    if (s->kin_stream) cudaStreamSynchronize(s->kin_stream);
     for (void* p : s->allocs) cudaFree(p);
     for (auto& e : s->ring_ev)
         if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : {s->ev_kin_done, s->ev_chain_done[0], s->ev_chain_done[1]})
+        if (e) cudaEventDestroy(e);
+    if (s->kin_stream) cudaStreamDestroy(s->kin_stream);
     if (s->h_ring) cudaFreeHost(s->h_ring);
     delete s;
     d->alm = nullptr;
@@ -813,12 +874,40 @@ bool alm_ready(const lbw_domain* d, int64_t m) { return d->alm->ready_step == m;
 
 bool alm_can_prelaunch(const lbw_domain* d) { return d->prelaunch && d->alm->kin_device; }
 
-ForceView alm_force_view(const lbw_domain* d, int64_t m) { return d->alm->set[m & 1].view(); }
+ForceView alm_force_view(const lbw_domain* d, int64_t m) {
+    return d->alm->set[m & 1].view((uint32_t)(m + 1));
+}
 
 int alm_invalidate(lbw_domain* d) {
     if (!alm_active(d)) return LBW_OK;
     LBW_CK(cudaStreamSynchronize(d->alm_stream));
+    if (d->alm->kin_stream) LBW_CK(cudaStreamSynchronize(d->alm->kin_stream));
     d->alm->ready_step = -1;
+    return LBW_OK;
+}
+
+// KK for step j on the kinematics stream.  Kinematics do not depend on the
+// flow, so step j+1's are computed while step j's chain and sweep run; the
+// buffer kin[j&1] is free once the chain of step j-2 (its last reader) is
+// done.
+static int kin_launch(lbw_domain* d, int64_t j) {
+    AlmState* s = d->alm;
+    if (j < s->kin_state_step || j > s->kin_state_step + 1) {
+        set_error("device kinematics can only advance one step at a time");
+        return LBW_ESTATE;
+    }
+    const int advance = j > s->kin_state_step ? 1 : 0;
+    LBW_CK(cudaStreamWaitEvent(s->kin_stream, s->ev_chain_done[j & 1], 0));
+    const size_t ksm = (size_t)s->nc * (kKP + kCS) * sizeof(double);
+    KinDev kd = s->kdev();
+    kd.hist_slot = (int32_t)(j % 3);
+    k_kinematics<<<1, 256, ksm, s->kin_stream>>>(kd, s->dev(j), d->g,
+                                                  d->desc.periodic[0] ? 1 : 0, advance);
+    count_launch();
+    LBW_CK(cudaGetLastError());
+    LBW_CK(cudaEventRecord(s->ev_kin_done, s->kin_stream));
+    s->kin_state_step = j;
+    s->kin_valid[j % 3] = j;
     return LBW_OK;
 }
 
@@ -827,23 +916,20 @@ int alm_launch(lbw_domain* d, int64_t m) {
     const Geom& g = d->g;
     cudaStream_t st = d->alm_stream;
     const int par = (int)(m & 1);
-    const AlmDev a = s->dev(par);
+    const AlmDev a = s->dev(m);
     const int per_x = d->desc.periodic[0] ? 1 : 0;
-    ForceSet& fs = s->set[par];
-    // forget the rows of step m-2 (its sweep and the sampling of step m-1
-    // are ordered before this point by the caller's stream waits)
-    LBW_CK(cudaMemsetAsync(fs.row_slot, 0xff, (size_t)g.nxl * g.ny * sizeof(int32_t), st));
-    LBW_CK(cudaMemsetAsync(fs.count, 0, sizeof(int32_t), st));
+    // this step's use of force set m&1: claims tagged m+1, counter by use
+    ForceSet fs = s->set[par];
+    const int use = (int)((m >> 1) & 1);
+    fs.count = fs.counts + use;
+    fs.next_count = fs.counts + (1 - use);
+    fs.tag = (uint32_t)(m + 1);
     if (s->kin_device) {
-        if (m < s->kin_state_step || m > s->kin_state_step + 1) {
-            set_error("device kinematics can only advance one step at a time");
-            return LBW_ESTATE;
+        if (s->kin_valid[m % 3] != m) {
+            int rc = kin_launch(d, m);
+            if (rc) return rc;
         }
-        const size_t ksm = (size_t)s->nc * (kKP + kCS) * sizeof(double);
-        k_kinematics<<<1, 256, ksm, st>>>(s->kdev(), a, g, per_x, m > s->kin_state_step ? 1 : 0);
-        count_launch();
-        LBW_CK(cudaGetLastError());
-        s->kin_state_step = m;
+        LBW_CK(cudaStreamWaitEvent(st, s->ev_kin_done, 0));
     } else if (s->kin_queued_step != m) {
         set_error("actuator step without kinematics: call lbw_alm_set_kinematics first");
         return LBW_ESTATE;
@@ -883,10 +969,18 @@ int alm_launch(lbw_domain* d, int64_t m) {
         k_alm_disks<<<(unsigned)((s->n_rings + 63) / 64), 64, 0, st>>>(a);
         count_launch();
     }
-    k_alm_fill<<<(unsigned)fs.cap, 128, s->fill_smem, st>>>(a, g, fs);
+    k_alm_fill<<<(unsigned)((fs.cap + 3) / 4), 128, 0, st>>>(a, g, fs);
     count_launch(2);
     LBW_CK(cudaGetLastError());
     LBW_CK(cudaEventRecord(d->ev_alm_done, st));
+    if (s->kin_device) {
+        LBW_CK(cudaEventRecord(s->ev_chain_done[par], st));
+        // prefetch the next step's kinematics while this chain and sweep run
+        if (alm_can_prelaunch(d) && s->kin_state_step == m) {
+            int rc = kin_launch(d, m + 1);
+            if (rc) return rc;
+        }
+    }
     s->ready_step = m;
     return LBW_OK;
 }
@@ -933,16 +1027,6 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     s->rho_ref = desc->rho_ref;
     s->dt2 = desc->force_dt2;
     s->den = desc->force_den;
-    s->fill_smem = ((size_t)(P * 4 + 15) / 16) * 16 + (size_t)P * 8;
-    if (s->fill_smem > 48 * 1024) {
-        if (cudaFuncSetAttribute(k_alm_fill, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)s->fill_smem) != cudaSuccess) {
-            cudaGetLastError();
-            alm_destroy(d);
-            set_error("too many actuator points for one CTA's point list");
-            return LBW_EINVAL;
-        }
-    }
     int rc = LBW_OK;
     auto A = [&](auto** p, size_t n) {
         if (rc == LBW_OK) rc = dev_alloc(d, s, p, n);
@@ -956,7 +1040,7 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     A(&s->p_alpha, std::max<int64_t>(1, total_rows));
     A(&s->p_cl, std::max<int64_t>(1, total_rows));
     A(&s->p_cd, std::max<int64_t>(1, total_rows));
-    A(&s->kin, (size_t)2 * P * kKin);
+    A(&s->kin, (size_t)3 * P * kKin);
     A(&s->samples, (size_t)2 * P * 4);
     A(&s->blade, (size_t)2 * P * 3);
     A(&s->flat, (size_t)P * 3);
@@ -977,10 +1061,12 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     const int64_t rows = (int64_t)d->g.nxl * d->g.ny;
     const int64_t cap = std::min<int64_t>(rows, (int64_t)9 * P);
     for (auto& fs : s->set) {
-        A(&fs.row_slot, rows);
-        A(&fs.pool, (size_t)cap * 3 * d->g.zp);
+        A(&fs.row_key, rows);
+        char* pool = nullptr;
+        A(&pool, (size_t)cap * 3 * d->g.zp * elem_bytes(d->g));
+        fs.pool = pool;
         A(&fs.slot_row, cap);
-        A(&fs.count, 1);
+        A(&fs.counts, 2);
         fs.cap = cap;
     }
     if (rc) {
@@ -1018,8 +1104,9 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     }
     if (rc == LBW_OK) {
         for (auto& fs : s->set) {
-            if (cudaMemset(fs.row_slot, 0xff, rows * 4) != cudaSuccess ||
-                cudaMemset(fs.count, 0, 4) != cudaSuccess) {
+            // keys with tag 0xffffffff match no step (chain tags are step+1)
+            if (cudaMemset(fs.row_key, 0xff, rows * 8) != cudaSuccess ||
+                cudaMemset(fs.counts, 0, 8) != cudaSuccess) {
                 cudaGetLastError();
                 rc = LBW_ECUDA;
             }
@@ -1028,7 +1115,7 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
             cudaMemset(s->error_flags, 0, 4) != cudaSuccess ||
             cudaMemset(s->samples, 0, (size_t)2 * P * 32) != cudaSuccess ||
             cudaMemset(s->blade, 0, (size_t)2 * P * 24) != cudaSuccess ||
-            cudaMemset(s->kin, 0, (size_t)2 * P * kKin * 8) != cudaSuccess ||
+            cudaMemset(s->kin, 0, (size_t)3 * P * kKin * 8) != cudaSuccess ||
             cudaMallocHost(&s->h_ring, (size_t)kRing * P * kKin * 8) != cudaSuccess) {
             cudaGetLastError();
             set_error("ALM initialisation failed");
@@ -1085,6 +1172,8 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
     A(&s->k_orient, (size_t)P * 9);
     A(&s->k_lframe, (size_t)P * 9);
     A(&s->k_cs, (size_t)C * kCS);
+    A(&s->k_spin_hist, (size_t)3 * C * 9);
+    A(&s->k_cs_hist, (size_t)3 * C * kCS);
     A(&s->k_is_disk, C);
     A(&s->k_disk_center, (size_t)C * 12);
     if (rc) return rc;
@@ -1128,12 +1217,32 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
         set_error("too many turbine components for the kinematics CTA");
         return LBW_EINVAL;
     }
+    if (!s->kin_stream) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (cudaStreamCreateWithPriority(&s->kin_stream, cudaStreamNonBlocking, hi) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s->ev_kin_done, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s->ev_chain_done[0], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s->ev_chain_done[1], cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("kinematics stream/event creation failed");
+            return LBW_ECUDA;
+        }
+    }
+    LBW_CK(cudaStreamSynchronize(s->kin_stream));
     s->nc = C;
     s->k_dx = kd->dx;
     s->kin_device = true;
     s->kin_state_step = d->step - (kd->advance_first ? 1 : 0);
+    s->kin_valid[0] = s->kin_valid[1] = s->kin_valid[2] = -1;
     s->ready_step = -1;
     return LBW_OK;
+}
+
+// step whose turbine state lbw_alm_download_kinematics reports: the
+// domain's step, unless the device kinematics have not reached it yet
+static int64_t kin_view_step(const lbw_domain* d) {
+    return std::min<int64_t>(d->step, d->alm->kin_state_step);
 }
 
 // parity of the most recent step's actuator outputs
@@ -1146,19 +1255,27 @@ int lbw_alm_download_kinematics(lbw_domain* d, double* kin, double* spin, double
     LBW_CK(cudaSetDevice(d->device));
     LBW_CK(cudaStreamSynchronize(d->stream));
     LBW_CK(cudaStreamSynchronize(d->alm_stream));
+    if (s->kin_stream) LBW_CK(cudaStreamSynchronize(s->kin_stream));
     if (kin)
-        LBW_CK(cudaMemcpy(kin, s->kin + (size_t)last_parity(d) * s->n * kKin,
+        LBW_CK(cudaMemcpy(kin, s->kin + (size_t)(d->step > 0 ? (d->step - 1) % 3 : 0) * s->n * kKin,
                           (size_t)s->n * kKin * 8, cudaMemcpyDeviceToHost));
+    // the turbine state of step d->step (what the host objects hold after
+    // d->step advances), even when the next step's kinematics already ran
+    const int64_t v = kin_view_step(d);
+    const bool hist = s->kin_valid[v % 3] == v;
     if (spin && s->kin_device)
-        LBW_CK(cudaMemcpy(spin, s->k_spin, (size_t)s->nc * 72, cudaMemcpyDeviceToHost));
+        LBW_CK(cudaMemcpy(spin, hist ? s->k_spin_hist + (size_t)(v % 3) * s->nc * 9 : s->k_spin,
+                          (size_t)s->nc * 72, cudaMemcpyDeviceToHost));
     if (comp_state && s->kin_device)
-        LBW_CK(cudaMemcpy(comp_state, s->k_cs, (size_t)s->nc * kCS * 8, cudaMemcpyDeviceToHost));
+        LBW_CK(cudaMemcpy(comp_state,
+                          hist ? s->k_cs_hist + (size_t)(v % 3) * s->nc * kCS : s->k_cs,
+                          (size_t)s->nc * kCS * 8, cudaMemcpyDeviceToHost));
     return LBW_OK;
 }
 
 int64_t lbw_alm_kinematics_step(lbw_domain* d) {
     if (!d || !alm_active(d) || !d->alm->kin_device) return -1;
-    return d->alm->kin_state_step;
+    return kin_view_step(d);
 }
 
 int lbw_alm_set_kinematics(lbw_domain* d, const double* kin) {
@@ -1173,7 +1290,7 @@ int lbw_alm_set_kinematics(lbw_domain* d, const double* kin) {
     double* h = s->h_ring + (size_t)slot * s->n * kKin;
     std::memcpy(h, kin, (size_t)s->n * kKin * 8);
     const int64_t m = d->step;
-    LBW_CK(cudaMemcpyAsync(s->kin + (size_t)(m & 1) * s->n * kKin, h, (size_t)s->n * kKin * 8,
+    LBW_CK(cudaMemcpyAsync(s->kin + (size_t)(m % 3) * s->n * kKin, h, (size_t)s->n * kKin * 8,
                            cudaMemcpyHostToDevice, d->alm_stream));
     LBW_CK(cudaEventRecord(s->ring_ev[slot], d->alm_stream));
     s->kin_queued_step = m;

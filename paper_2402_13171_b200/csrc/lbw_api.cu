@@ -194,9 +194,9 @@ static void free_domain(lbw_domain* d) {
     if (d->stream) cudaStreamSynchronize(d->stream);
     if (d->alm_stream) cudaStreamSynchronize(d->alm_stream);
     alm_destroy(d);
-    for (double*& b : d->buf)
+    for (void*& b : d->buf)
         if (b) cudaFree(b);
-    if (d->user.row_slot) cudaFree(d->user.row_slot);
+    if (d->user.row_key) cudaFree(d->user.row_key);
     if (d->user.pool) cudaFree(d->user.pool);
     if (d->macro_dense) cudaFree(d->macro_dense);
     if (d->d_nan) cudaFree(d->d_nan);
@@ -240,6 +240,8 @@ int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out) {
     LBW_REQ(!(s.boundary == LBW_BC_INFLOW_OUTFLOW && s.periodic[0]),
             "velocity_inflow_outflow needs a non-periodic x axis");
     LBW_REQ(s.nranks >= 1 && s.rank >= 0 && s.rank < s.nranks, "bad rank/nranks");
+    LBW_REQ(s.precision == LBW_PREC_DOUBLE || s.precision == LBW_PREC_SINGLE,
+            "unknown storage precision");
     const int ndev = lbw_device_count();
     LBW_REQ(ndev > 0, "no CUDA device visible");
     LBW_REQ(s.device >= 0 && s.device < ndev, "device ordinal out of range");
@@ -257,8 +259,10 @@ int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out) {
     g.nxl = (int32_t)s.slab_nx;
     g.ny = (int32_t)s.cells[1];
     g.nz = (int32_t)s.cells[2];
-    g.zp = (g.nz + 15) / 16 * 16;   // 128-byte aligned z rows
-    if (g.nz < 16) g.zp = g.nz;
+    g.single = s.precision == LBW_PREC_SINGLE ? 1 : 0;
+    const int row_elems = g.single ? 32 : 16;   // 128-byte aligned z rows
+    g.zp = (g.nz + row_elems - 1) / row_elems * row_elems;
+    if (g.nz < row_elems) g.zp = g.nz;
     g.dir_stride = (int64_t)g.ny * g.zp;
     g.plane_stride = 27 * g.dir_stride;
     g.x0 = s.slab_x0;
@@ -279,10 +283,13 @@ int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out) {
         for (int i = 0; i < 27; ++i) g.feq_in[i] = s.feq_in[i];
     else
         polynomial_equilibrium(1.0, s.u_in, g.feq_in);
+    // the reference stores the inflow ghost in the field's dtype (halo.py:152-156)
+    if (g.single)
+        for (int i = 0; i < 27; ++i) g.feq_in[i] = (double)(float)g.feq_in[i];
     d->relax = make_relax(s.omega, s.rates[0], s.rates[1], s.rates[2], s.rates[3], 1.0);
 
     int rc = LBW_OK;
-    const size_t buf_bytes = (size_t)(g.nxl + 2) * g.plane_stride * sizeof(double);
+    const size_t buf_bytes = (size_t)(g.nxl + 2) * g.plane_stride * elem_bytes(g);
     if (cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking) != cudaSuccess ||
         // the actuator chain runs beside the sweep: highest priority so its
         // few CTAs are dispatched ahead of the sweep's remaining ones
@@ -346,8 +353,8 @@ static size_t interior_cells(const lbw_domain* d) {
 static int freeze_macro_if(lbw_domain* d, bool touches_buf_cur, bool touches_user_force) {
     if (!alm_active(d) || d->msrc.kind != MS_GATHER) return LBW_OK;
     const bool hit = (touches_buf_cur && d->msrc.buf == d->cur) ||
-                     (touches_user_force && d->msrc.fv.row_slot == d->user.row_slot &&
-                      d->user.row_slot != nullptr);
+                     (touches_user_force && d->msrc.fv.row_key == d->user.row_key &&
+                      d->user.row_key != nullptr);
     if (!hit) return LBW_OK;
     if (!d->macro_dense) {
         int rc = alloc_dev(d, (void**)&d->macro_dense, interior_cells(d) * 4 * sizeof(double));
@@ -437,13 +444,13 @@ int lbw_domain_set_force(lbw_domain* d, const double* force_aos) {
     if (rc) return rc;
     if (!force_aos) {
         d->user_active = false;
-        d->shown_fv = ForceView{nullptr, nullptr};
+        d->shown_fv = ForceView{nullptr, nullptr, 0};
         return LBW_OK;
     }
     const int64_t rows = (int64_t)d->g.nxl * d->g.ny;
-    if (!d->user.row_slot) {
-        rc = alloc_dev(d, (void**)&d->user.row_slot, rows * sizeof(int32_t));
-        if (!rc) rc = alloc_dev(d, (void**)&d->user.pool, rows * 3 * d->g.zp * sizeof(double));
+    if (!d->user.row_key) {
+        rc = alloc_dev(d, (void**)&d->user.row_key, rows * sizeof(uint64_t));
+        if (!rc) rc = alloc_dev(d, (void**)&d->user.pool, rows * 3 * d->g.zp * elem_bytes(d->g));
         if (rc) return rc;
         d->user.cap = rows;
     }
@@ -451,10 +458,10 @@ int lbw_domain_set_force(lbw_domain* d, const double* force_aos) {
     rc = ensure_stage(d, bytes);
     if (rc) return rc;
     LBW_CK(cudaMemcpyAsync(d->stage, force_aos, bytes, cudaMemcpyHostToDevice, d->stream));
-    LBW_CK(launch_force_from_aos(d->stage, d->g, d->user.row_slot, d->user.pool, d->stream));
+    LBW_CK(launch_force_from_aos(d->stage, d->g, d->user.row_key, d->user.pool, d->stream));
     LBW_CK(cudaStreamSynchronize(d->stream));
     d->user_active = true;
-    d->shown_fv = d->user.view();
+    d->shown_fv = d->user.view(0);
     return LBW_OK;
 }
 
@@ -554,7 +561,7 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
     LBW_REQ(nsteps >= 0, "nsteps must be >= 0");
     LBW_CK(cudaSetDevice(d->device));
     for (int32_t s = 0; s < nsteps; ++s) {
-        ForceView fv = d->user_active ? d->user.view() : ForceView{nullptr, nullptr};
+        ForceView fv = d->user_active ? d->user.view(0) : ForceView{nullptr, nullptr, 0};
         // neighbours must have finished the previous sweep: it filled our
         // ghost planes and stopped reading theirs (which we overwrite now)
         {

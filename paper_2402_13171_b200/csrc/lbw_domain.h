@@ -28,14 +28,17 @@ void set_error(const std::string& msg);
     } while (0)
 
 // A sparse force field: rows (x,y) of the slab that carry force own a slot
-// of [3][zp] doubles in the pool.
+// of [3][zp] storage elements in the pool (keys: see ForceView).
 struct ForceSet {
-    int32_t* row_slot = nullptr;   // (nxl*ny), -1 = no force
-    double* pool = nullptr;        // (cap, 3, zp)
+    uint64_t* row_key = nullptr;   // (nxl*ny)
+    void* pool = nullptr;          // (cap, 3, zp) of the storage type
     int32_t* slot_row = nullptr;   // (cap) row of each used slot
-    int32_t* count = nullptr;      // device counter of used slots
+    int32_t* count = nullptr;      // used slots: the claiming step's counter
+    int32_t* counts = nullptr;     // (2) counters, alternating between uses of the set
+    int32_t* next_count = nullptr; // counter of the set's next use (zeroed by its fill)
+    uint32_t tag = 0;              // tag of the claiming step
     int64_t cap = 0;
-    ForceView view() const { return ForceView{row_slot, pool}; }
+    ForceView view(uint32_t t) const { return ForceView{row_key, pool, t}; }
 };
 
 enum MacroKind { MS_UNIFORM = 0, MS_DENSE = 1, MS_GATHER = 2 };
@@ -57,7 +60,7 @@ struct lbw_domain {
     lbw::Relax relax{};
     int device = 0;
     cudaStream_t stream = nullptr;
-    double* buf[2] = {nullptr, nullptr};
+    void* buf[2] = {nullptr, nullptr};   // populations, storage type per g.single
     int cur = 0;             // buffer holding the current state
     bool state_pre = true;   // buf[cur] holds pre-collision populations
     int64_t step = 0;
@@ -90,7 +93,7 @@ struct lbw_domain {
     bool linked = false;
     int nb_rank[2] = {-1, -1};
     int32_t nb_nxl[2] = {0, 0};
-    double* nb_buf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [side][buffer]
+    void* nb_buf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [side][buffer]
     double* nb_cube[2] = {nullptr, nullptr};
     uint32_t* nb_flags[2] = {nullptr, nullptr};
     // my flags, written by the neighbours: [0] sweeps done by lo, [1] by hi,

@@ -25,23 +25,36 @@ struct Geom {
     int64_t x0, nxg;           // first global x, global x size
     int32_t per_y, per_z;
     int32_t lo_src, hi_src;    // XSource for x-1 at x=0 and x+1 at x=nxl-1
-    double feq_in[27];
+    int32_t single;            // populations / force stored fp32 (LBW_PREC_SINGLE)
+    double feq_in[27];         // already rounded to the storage type
 };
 
 __host__ __device__ inline int64_t buf_index(const Geom& g, int p, int i, int y, int z) {
     return (int64_t)p * g.plane_stride + (int64_t)i * g.dir_stride + (int64_t)y * g.zp + z;
 }
 
+// Storage element of populations and forces: double, or float when
+// g.single (arithmetic stays fp64; values are rounded on store).
+__host__ __device__ inline size_t elem_bytes(const Geom& g) { return g.single ? 4 : 8; }
+
 // Force density of the cells that carry one: rows (x,y) with a slot hold
-// [3][zp] doubles in the pool; every other cell has F = 0.
+// [3][zp] storage elements in the pool; every other cell has F = 0.
+// Row keys are (tag << 32 | slot): a row carries force for this view only
+// when its tag matches, so a force set is re-used step after step without
+// clearing (the actuator chain tags its claims with step + 1; a caller-set
+// body force uses tag 0).
 struct ForceView {
-    const int32_t* row_slot;  // (nxl*ny) slot index or -1; nullptr = no force
-    const double* pool;       // [slot][3][zp]
+    const uint64_t* row_key;  // (nxl*ny); nullptr = no force anywhere
+    const void* pool;         // [slot][3][zp] of the storage type
+    uint32_t tag;
 };
+__host__ __device__ inline uint64_t row_key_of(uint32_t tag, int32_t slot) {
+    return ((uint64_t)tag << 32) | (uint32_t)slot;
+}
 
 struct HaloOut {
-    double* lo;  // receives dirs 0..8 of plane x=0   ([9][ny][zp]), or nullptr
-    double* hi;  // receives dirs 18..26 of plane x=nxl-1, or nullptr
+    void* lo;  // receives dirs 0..8 of plane x=0   ([9][ny][zp]), or nullptr
+    void* hi;  // receives dirs 18..26 of plane x=nxl-1, or nullptr
     // in-kernel completion signal: the last CTA of the two edge planes
     // (scheduled first) release-stores `value` into both neighbours' flags
     uint32_t* peer_flag[2];
@@ -52,8 +65,8 @@ struct HaloOut {
 
 // kernel launchers (defined in the .cu translation units)
 struct SweepArgs {
-    const double* src;
-    double* dst;
+    const void* src;   // storage type per g.single
+    void* dst;
     Geom g;
     ForceView fv;
     Relax r;
@@ -83,16 +96,18 @@ cudaError_t launch_block_moments(const double* f, const double* force, double* m
                                  int64_t ny, int64_t nz, double dt, cudaStream_t s);
 cudaError_t launch_block_stream(const double* fsrc, double* fdst, int64_t nx, int64_t ny,
                                 int64_t nz, cudaStream_t s);
-cudaError_t launch_aos_to_soa(const double* aos, double* buf, const Geom& g, cudaStream_t s);
-cudaError_t launch_fill_uniform(const double (&f27)[27], double* buf, const Geom& g,
+// population buffers / force pools are of the storage type (g.single);
+// the AoS host-side arrays are always fp64
+cudaError_t launch_aos_to_soa(const double* aos, void* buf, const Geom& g, cudaStream_t s);
+cudaError_t launch_fill_uniform(const double (&f27)[27], void* buf, const Geom& g,
                                 cudaStream_t s);
-cudaError_t launch_gather_aos(bool pull, const double* buf, const Geom& g, double* aos,
+cudaError_t launch_gather_aos(bool pull, const void* buf, const Geom& g, double* aos,
                               cudaStream_t s);
-cudaError_t launch_moments_soa(bool pull, const double* buf, const Geom& g, ForceView fv,
+cudaError_t launch_moments_soa(bool pull, const void* buf, const Geom& g, ForceView fv,
                                double dt, double* macro_aos, cudaStream_t s);
 cudaError_t launch_force_to_aos(ForceView fv, const Geom& g, double* aos, cudaStream_t s);
-cudaError_t launch_force_from_aos(const double* aos, const Geom& g, int32_t* row_slot,
-                                  double* pool, cudaStream_t s);
+cudaError_t launch_force_from_aos(const double* aos, const Geom& g, uint64_t* row_key,
+                                  void* pool, cudaStream_t s);
 
 void count_launch(int n = 1);
 

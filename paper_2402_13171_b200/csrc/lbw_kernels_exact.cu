@@ -11,13 +11,8 @@ cudaError_t launch_sweep_exact(int op, bool pull, const SweepArgs& a, cudaStream
     if (grd.z == 0) return cudaSuccess;
     SweepArgs b = a;
     b.halo.edge_ctas = grd.x * grd.y * (grd.z < 2 ? grd.z : 2u);
-    if (op == 1) {
-        if (pull) k_sweep<1, true><<<grd, blk, 0, s>>>(b);
-        else k_sweep<1, false><<<grd, blk, 0, s>>>(b);
-    } else {
-        if (pull) k_sweep<0, true><<<grd, blk, 0, s>>>(b);
-        else k_sweep<0, false><<<grd, blk, 0, s>>>(b);
-    }
+    if (a.g.single) launch_k_sweep<4, float>(op, pull, grd, blk, b, s);
+    else launch_k_sweep<4, double>(op, pull, grd, blk, b, s);
     count_launch();
     return cudaGetLastError();
 }
@@ -91,30 +86,32 @@ __global__ void k_block_stream(const double* __restrict__ fsrc, double* __restri
     }
 }
 
-__global__ void k_aos_to_soa(const double* __restrict__ aos, double* __restrict__ buf, Geom g) {
+template <class T>
+__global__ void k_aos_to_soa(const double* __restrict__ aos, T* __restrict__ buf, Geom g) {
     int x, y, z;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (!cell_of(g, t, x, y, z)) return;
-    double* d = buf + buf_index(g, x + 1, 0, y, z);
+    T* d = buf + buf_index(g, x + 1, 0, y, z);
 #pragma unroll
-    for (int i = 0; i < 27; ++i) d[(int64_t)i * g.dir_stride] = aos[t * 27 + i];
+    for (int i = 0; i < 27; ++i) st_pop(d + (int64_t)i * g.dir_stride, aos[t * 27 + i]);
 }
 
 struct F27 {
     double v[27];
 };
 
-__global__ void k_fill_uniform(F27 f, double* __restrict__ buf, Geom g) {
+template <class T>
+__global__ void k_fill_uniform(F27 f, T* __restrict__ buf, Geom g) {
     int x, y, z;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (!cell_of(g, t, x, y, z)) return;
-    double* d = buf + buf_index(g, x + 1, 0, y, z);
+    T* d = buf + buf_index(g, x + 1, 0, y, z);
 #pragma unroll
-    for (int i = 0; i < 27; ++i) d[(int64_t)i * g.dir_stride] = f.v[i];
+    for (int i = 0; i < 27; ++i) st_pop(d + (int64_t)i * g.dir_stride, f.v[i]);
 }
 
-template <bool PULL>
-__global__ void k_gather_aos(const double* __restrict__ buf, Geom g, double* __restrict__ aos) {
+template <bool PULL, class T>
+__global__ void k_gather_aos(const T* __restrict__ buf, Geom g, double* __restrict__ aos) {
     int x, y, z;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (!cell_of(g, t, x, y, z)) return;
@@ -124,8 +121,8 @@ __global__ void k_gather_aos(const double* __restrict__ buf, Geom g, double* __r
     for (int i = 0; i < 27; ++i) aos[t * 27 + i] = f[i];
 }
 
-template <bool PULL>
-__global__ void k_moments_soa(const double* __restrict__ buf, Geom g, ForceView fv, double dt,
+template <bool PULL, class T>
+__global__ void k_moments_soa(const T* __restrict__ buf, Geom g, ForceView fv, double dt,
                               double* __restrict__ macro) {
     int x, y, z;
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -133,8 +130,8 @@ __global__ void k_moments_soa(const double* __restrict__ buf, Geom g, ForceView 
     double f[27];
     load_cell<PULL>(buf, g, x, y, z, f);
     double Fx, Fy, Fz;
-    load_force(fv, g, x, y, z, Fx, Fy, Fz);
-    const Macro m = moments_exact(f, Fx, Fy, Fz, dt);
+    load_force<T>(fv, g, x, y, z, Fx, Fy, Fz);
+    const Macro m = stored_macro(g, moments_exact(f, Fx, Fy, Fz, dt));
     macro[t * 4] = m.rho;
     macro[t * 4 + 1] = m.ux;
     macro[t * 4 + 2] = m.uy;
@@ -146,7 +143,7 @@ __global__ void k_force_to_aos(ForceView fv, Geom g, double* __restrict__ aos) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (!cell_of(g, t, x, y, z)) return;
     double Fx, Fy, Fz;
-    load_force(fv, g, x, y, z, Fx, Fy, Fz);
+    load_force_any(fv, g, x, y, z, Fx, Fy, Fz);
     aos[t * 3] = Fx;
     aos[t * 3 + 1] = Fy;
     aos[t * 3 + 2] = Fz;
@@ -154,21 +151,22 @@ __global__ void k_force_to_aos(ForceView fv, Geom g, double* __restrict__ aos) {
 
 // one CTA per (x,y) row: copy the row into pool slot == row index and give
 // the row a slot only when some component is non-zero.
-__global__ void k_force_from_aos(const double* __restrict__ aos, Geom g, int32_t* __restrict__ row_slot,
-                                 double* __restrict__ pool) {
+template <class T>
+__global__ void k_force_from_aos(const double* __restrict__ aos, Geom g, uint64_t* __restrict__ row_key,
+                                 T* __restrict__ pool) {
     const int64_t row = blockIdx.x;
     bool nz_any = false;
     for (int z = threadIdx.x; z < g.nz; z += blockDim.x) {
         const int64_t t = row * g.nz + z;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const double v = aos[t * 3 + c];
+            const T v = (T)aos[t * 3 + c];
             pool[(row * 3 + c) * g.zp + z] = v;
-            nz_any |= (v != 0.0);
+            nz_any |= (v != (T)0);
         }
     }
     const int any = __syncthreads_or(nz_any);
-    if (threadIdx.x == 0) row_slot[row] = any ? (int32_t)row : -1;
+    if (threadIdx.x == 0) row_key[row] = row_key_of(0, any ? (int32_t)row : -1);
 }
 
 inline unsigned cells_blocks(const Geom& g, int threads) {
@@ -196,33 +194,47 @@ cudaError_t launch_block_stream(const double* fsrc, double* fdst, int64_t nx, in
     return cudaGetLastError();
 }
 
-cudaError_t launch_aos_to_soa(const double* aos, double* buf, const Geom& g, cudaStream_t s) {
-    k_aos_to_soa<<<cells_blocks(g, 128), 128, 0, s>>>(aos, buf, g);
+cudaError_t launch_aos_to_soa(const double* aos, void* buf, const Geom& g, cudaStream_t s) {
+    if (g.single) k_aos_to_soa<<<cells_blocks(g, 128), 128, 0, s>>>(aos, (float*)buf, g);
+    else k_aos_to_soa<<<cells_blocks(g, 128), 128, 0, s>>>(aos, (double*)buf, g);
     count_launch();
     return cudaGetLastError();
 }
 
-cudaError_t launch_fill_uniform(const double (&f27)[27], double* buf, const Geom& g,
+cudaError_t launch_fill_uniform(const double (&f27)[27], void* buf, const Geom& g,
                                 cudaStream_t s) {
     F27 f;
     for (int i = 0; i < 27; ++i) f.v[i] = f27[i];
-    k_fill_uniform<<<cells_blocks(g, 128), 128, 0, s>>>(f, buf, g);
+    if (g.single) k_fill_uniform<<<cells_blocks(g, 128), 128, 0, s>>>(f, (float*)buf, g);
+    else k_fill_uniform<<<cells_blocks(g, 128), 128, 0, s>>>(f, (double*)buf, g);
     count_launch();
     return cudaGetLastError();
 }
 
-cudaError_t launch_gather_aos(bool pull, const double* buf, const Geom& g, double* aos,
-                              cudaStream_t s) {
+template <class T>
+void gather_aos_t(bool pull, const T* buf, const Geom& g, double* aos, cudaStream_t s) {
     if (pull) k_gather_aos<true><<<cells_blocks(g, 128), 128, 0, s>>>(buf, g, aos);
     else k_gather_aos<false><<<cells_blocks(g, 128), 128, 0, s>>>(buf, g, aos);
+}
+template <class T>
+void moments_soa_t(bool pull, const T* buf, const Geom& g, ForceView fv, double dt, double* m,
+                   cudaStream_t s) {
+    if (pull) k_moments_soa<true><<<cells_blocks(g, 128), 128, 0, s>>>(buf, g, fv, dt, m);
+    else k_moments_soa<false><<<cells_blocks(g, 128), 128, 0, s>>>(buf, g, fv, dt, m);
+}
+
+cudaError_t launch_gather_aos(bool pull, const void* buf, const Geom& g, double* aos,
+                              cudaStream_t s) {
+    if (g.single) gather_aos_t(pull, (const float*)buf, g, aos, s);
+    else gather_aos_t(pull, (const double*)buf, g, aos, s);
     count_launch();
     return cudaGetLastError();
 }
 
-cudaError_t launch_moments_soa(bool pull, const double* buf, const Geom& g, ForceView fv,
+cudaError_t launch_moments_soa(bool pull, const void* buf, const Geom& g, ForceView fv,
                                double dt, double* macro_aos, cudaStream_t s) {
-    if (pull) k_moments_soa<true><<<cells_blocks(g, 128), 128, 0, s>>>(buf, g, fv, dt, macro_aos);
-    else k_moments_soa<false><<<cells_blocks(g, 128), 128, 0, s>>>(buf, g, fv, dt, macro_aos);
+    if (g.single) moments_soa_t(pull, (const float*)buf, g, fv, dt, macro_aos, s);
+    else moments_soa_t(pull, (const double*)buf, g, fv, dt, macro_aos, s);
     count_launch();
     return cudaGetLastError();
 }
@@ -233,11 +245,12 @@ cudaError_t launch_force_to_aos(ForceView fv, const Geom& g, double* aos, cudaSt
     return cudaGetLastError();
 }
 
-cudaError_t launch_force_from_aos(const double* aos, const Geom& g, int32_t* row_slot,
-                                  double* pool, cudaStream_t s) {
+cudaError_t launch_force_from_aos(const double* aos, const Geom& g, uint64_t* row_key,
+                                  void* pool, cudaStream_t s) {
     const unsigned rows = (unsigned)((int64_t)g.nxl * g.ny);
     if (rows == 0) return cudaSuccess;
-    k_force_from_aos<<<rows, 128, 0, s>>>(aos, g, row_slot, pool);
+    if (g.single) k_force_from_aos<<<rows, 128, 0, s>>>(aos, g, row_key, (float*)pool);
+    else k_force_from_aos<<<rows, 128, 0, s>>>(aos, g, row_key, (double*)pool);
     count_launch();
     return cudaGetLastError();
 }

@@ -18,17 +18,14 @@ cudaError_t launch_sweep_fast(int op, bool pull, const SweepArgs& a, cudaStream_
         const char* e = getenv("LBW_SWEEP_MINB");
         return e ? atoi(e) : 5;
     }();
-    if (op == 1) {
-        if (pull) {
-            if (minb == 6) k_sweep<1, true, 6><<<grd, blk, 0, s>>>(b);
-            else if (minb == 4) k_sweep<1, true, 4><<<grd, blk, 0, s>>>(b);
-            else k_sweep<1, true, 5><<<grd, blk, 0, s>>>(b);
-        } else {
-            k_sweep<1, false><<<grd, blk, 0, s>>>(b);
-        }
+    if (a.g.single) {
+        if (minb == 6) launch_k_sweep<6, float>(op, pull, grd, blk, b, s);
+        else if (minb == 4) launch_k_sweep<4, float>(op, pull, grd, blk, b, s);
+        else launch_k_sweep<5, float>(op, pull, grd, blk, b, s);
     } else {
-        if (pull) k_sweep<0, true><<<grd, blk, 0, s>>>(b);
-        else k_sweep<0, false><<<grd, blk, 0, s>>>(b);
+        if (minb == 6) launch_k_sweep<6, double>(op, pull, grd, blk, b, s);
+        else if (minb == 4) launch_k_sweep<4, double>(op, pull, grd, blk, b, s);
+        else launch_k_sweep<5, double>(op, pull, grd, blk, b, s);
     }
     count_launch();
     return cudaGetLastError();

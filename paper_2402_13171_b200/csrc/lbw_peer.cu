@@ -45,7 +45,7 @@ constexpr uint32_t kMagic = 0x4c425750;  // "LBWP"
 
 struct PeerBlob {
     uint32_t magic;
-    int32_t rank, nranks, nxl, ny, zp, n_points, has_cube;
+    int32_t rank, nranks, nxl, ny, zp, n_points, has_cube, single;
     int64_t plane_stride;
     cudaIpcMemHandle_t buf[2];
     cudaIpcMemHandle_t cube;
@@ -126,6 +126,7 @@ int lbw_domain_export_handle(lbw_domain* d, void* blob, int64_t* blob_bytes) {
     b.ny = d->g.ny;
     b.zp = d->g.zp;
     b.plane_stride = d->g.plane_stride;
+    b.single = d->g.single;
     for (int k = 0; k < 2; ++k) LBW_CK(cudaIpcGetMemHandle(&b.buf[k], d->buf[k]));
     LBW_CK(cudaIpcGetMemHandle(&b.flags, d->flags));
     double* cube = alm_cube(d);
@@ -155,8 +156,9 @@ int lbw_domain_import_peers(lbw_domain* d, const void* lo_blob, const void* hi_b
         std::memcpy(&pb[side], blobs[side], sizeof(PeerBlob));
         const PeerBlob& b = pb[side];
         LBW_REQ(b.magic == kMagic, "bad peer handle blob");
-        LBW_REQ(b.ny == d->g.ny && b.zp == d->g.zp && b.plane_stride == d->g.plane_stride,
-                "neighbour slab has a different y/z layout");
+        LBW_REQ(b.ny == d->g.ny && b.zp == d->g.zp && b.plane_stride == d->g.plane_stride &&
+                    b.single == d->g.single,
+                "neighbour slab has a different y/z layout or storage precision");
         LBW_REQ(b.rank != d->desc.rank, "a slab cannot be its own neighbour");
         LBW_REQ((b.has_cube != 0) == (alm_cube(d) != nullptr),
                 "neighbours disagree about actuator points");
@@ -175,17 +177,21 @@ int lbw_domain_import_peers(lbw_domain* d, const void* lo_blob, const void* hi_b
         }
         d->nb_rank[side] = b.rank;
         d->nb_nxl[side] = b.nxl;
-        d->nb_buf[side][0] = (double*)ptrs[0];
-        d->nb_buf[side][1] = (double*)ptrs[1];
+        d->nb_buf[side][0] = ptrs[0];
+        d->nb_buf[side][1] = ptrs[1];
         d->nb_flags[side] = (uint32_t*)ptrs[2];
         d->nb_cube[side] = (double*)ptrs[3];
     }
     // edge planes go straight into the neighbours' ghost planes
+    const int64_t eb = (int64_t)elem_bytes(d->g);
     for (int k = 0; k < 2; ++k) {
         d->halo[k].lo = d->nb_rank[0] >= 0
-                            ? d->nb_buf[0][k] + (int64_t)(d->nb_nxl[0] + 1) * d->g.plane_stride
+                            ? (char*)d->nb_buf[0][k] +
+                                  (int64_t)(d->nb_nxl[0] + 1) * d->g.plane_stride * eb
                             : nullptr;
-        d->halo[k].hi = d->nb_rank[1] >= 0 ? d->nb_buf[1][k] + 18 * d->g.dir_stride : nullptr;
+        d->halo[k].hi = d->nb_rank[1] >= 0
+                            ? (char*)d->nb_buf[1][k] + 18 * d->g.dir_stride * eb
+                            : nullptr;
     }
     LBW_REQ((d->g.lo_src == XS_GHOST) == (d->nb_rank[0] >= 0) &&
                 (d->g.hi_src == XS_GHOST) == (d->nb_rank[1] >= 0),

@@ -84,7 +84,9 @@ __device__ __forceinline__ void make_pull(const Geom& g, int x, int y, int z, Pu
 #define LBW_STREAM_HINTS 0
 #endif
 // Streaming cache hints for the single-use population traffic: loads skip
-// L1 allocation, stores are marked evict-first.
+// L1 allocation, stores are marked evict-first.  Storage is double or
+// float (precision: single); values are widened on load and rounded to
+// nearest on store, as numpy/numba do for float32 fields (_kernels.py:5-7).
 __device__ __forceinline__ double ld_pop(const double* p) {
 #if LBW_STREAM_HINTS
     double v;
@@ -94,6 +96,7 @@ __device__ __forceinline__ double ld_pop(const double* p) {
     return __ldg(p);
 #endif
 }
+__device__ __forceinline__ double ld_pop(const float* p) { return (double)__ldg(p); }
 __device__ __forceinline__ void st_pop(double* p, double v) {
 #if LBW_STREAM_HINTS
     __stcs(p, v);
@@ -101,14 +104,21 @@ __device__ __forceinline__ void st_pop(double* p, double v) {
     *p = v;
 #endif
 }
+__device__ __forceinline__ void st_pop(float* p, double v) { *p = (float)v; }
 
-template <bool PULL>
-__device__ __forceinline__ void load_cell(const double* __restrict__ src, const Geom& g, int x, int y,
+// the value a store of v into storage type T reads back as
+template <class T>
+__device__ __forceinline__ double stored(double v) {
+    return (double)(T)v;
+}
+
+template <bool PULL, class T>
+__device__ __forceinline__ void load_cell(const T* __restrict__ src, const Geom& g, int x, int y,
                                           int z, double (&f)[27]) {
     if constexpr (!PULL) {
-        const double* p = src + buf_index(g, x + 1, 0, y, z);
+        const T* p = src + buf_index(g, x + 1, 0, y, z);
 #pragma unroll
-        for (int i = 0; i < 27; ++i) f[i] = __ldg(p + (int64_t)i * g.dir_stride);
+        for (int i = 0; i < 27; ++i) f[i] = ld_pop(p + (int64_t)i * g.dir_stride);
     } else {
         PullSrc s;
         make_pull(g, x, y, z, s);
@@ -138,9 +148,10 @@ __device__ __forceinline__ bool pull_is_simple(const Geom& g, int x, int y, int 
     return xs && ys && zs;
 }
 
-__device__ __forceinline__ void load_cell_simple(const double* __restrict__ src, const Geom& g,
+template <class T>
+__device__ __forceinline__ void load_cell_simple(const T* __restrict__ src, const Geom& g,
                                                  int x, int y, int z, double (&f)[27]) {
-    const double* px[3];
+    const T* px[3];
 #pragma unroll
     for (int c = -1; c <= 1; ++c) {
         int64_t off;
@@ -161,26 +172,54 @@ __device__ __forceinline__ void load_cell_simple(const double* __restrict__ src,
         f[i] = ld_pop(px[cx_of(i) + 1] + (i * ds + yo[cy_of(i) + 1] + zo[cz_of(i) + 1]));
 }
 
+template <class T>
 __device__ __forceinline__ void load_force(const ForceView& fv, const Geom& g, int x, int y, int z,
                                            double& Fx, double& Fy, double& Fz) {
     Fx = Fy = Fz = 0.0;
-    if (fv.row_slot != nullptr) {
-        const int32_t slot = fv.row_slot[(int64_t)x * g.ny + y];
-        if (slot >= 0) {
-            const double* p = fv.pool + (int64_t)slot * 3 * g.zp + z;
-            Fx = p[0];
-            Fy = p[g.zp];
-            Fz = p[2 * g.zp];
+    if (fv.row_key != nullptr) {
+        const uint64_t key = fv.row_key[(int64_t)x * g.ny + y];
+        const int32_t slot = (int32_t)(uint32_t)key;
+        if ((uint32_t)(key >> 32) == fv.tag && slot >= 0) {
+            const T* p = static_cast<const T*>(fv.pool) + (int64_t)slot * 3 * g.zp + z;
+            Fx = (double)p[0];
+            Fy = (double)p[g.zp];
+            Fz = (double)p[2 * g.zp];
         }
     }
 }
 
+// runtime storage dispatch for the non-hot paths (actuator sampling, output)
+template <bool PULL>
+__device__ __forceinline__ void load_cell_any(const void* src, const Geom& g, int x, int y, int z,
+                                              double (&f)[27]) {
+    if (g.single) load_cell<PULL>(static_cast<const float*>(src), g, x, y, z, f);
+    else load_cell<PULL>(static_cast<const double*>(src), g, x, y, z, f);
+}
+__device__ __forceinline__ void load_force_any(const ForceView& fv, const Geom& g, int x, int y,
+                                               int z, double& Fx, double& Fy, double& Fz) {
+    if (g.single) load_force<float>(fv, g, x, y, z, Fx, Fy, Fz);
+    else load_force<double>(fv, g, x, y, z, Fx, Fy, Fz);
+}
+// macro as the reference's macro array of the storage dtype holds it
+__device__ __forceinline__ Macro stored_macro(const Geom& g, Macro m) {
+    if (g.single) {
+        m.rho = stored<float>(m.rho);
+        m.ux = stored<float>(m.ux);
+        m.uy = stored<float>(m.uy);
+        m.uz = stored<float>(m.uz);
+    }
+    return m;
+}
+
 // Non-finite macro -> atomicMin of (step, global cell, density-ok bit)
 // (sim.py:254-262: first offending cell in C order, "density" when rho is bad).
+// The reference checks its macro array, i.e. the values rounded to T.
+template <class T>
 __device__ __forceinline__ void flag_nonfinite(unsigned long long* key, int64_t step,
                                                int64_t cell, const Macro& m) {
-    const bool rho_ok = isfinite(m.rho);
-    if (!(rho_ok && isfinite(m.ux) && isfinite(m.uy) && isfinite(m.uz))) {
+    const bool rho_ok = isfinite(stored<T>(m.rho));
+    if (!(rho_ok && isfinite(stored<T>(m.ux)) && isfinite(stored<T>(m.uy)) &&
+          isfinite(stored<T>(m.uz)))) {
         const unsigned long long k = ((unsigned long long)step << 40) |
                                      ((unsigned long long)cell << 1) | (rho_ok ? 1ull : 0ull);
         atomicMin(key, k);
@@ -208,37 +247,38 @@ __device__ __forceinline__ void edge_done(const HaloOut& h) {
     }
 }
 
-template <int OP, bool PULL>
+template <int OP, bool PULL, class T>
 __device__ __forceinline__ void sweep_cell(const SweepArgs& a, int x, int y, int z) {
     const Geom& g = a.g;
+    const T* src = static_cast<const T*>(a.src);
     double f[27];
-    if (PULL && pull_is_simple(g, x, y, z)) load_cell_simple(a.src, g, x, y, z, f);
-    else load_cell<PULL>(a.src, g, x, y, z, f);
+    if (PULL && pull_is_simple(g, x, y, z)) load_cell_simple(src, g, x, y, z, f);
+    else load_cell<PULL>(src, g, x, y, z, f);
     double Fx, Fy, Fz;
-    load_force(a.fv, g, x, y, z, Fx, Fy, Fz);
+    load_force<T>(a.fv, g, x, y, z, Fx, Fy, Fz);
     const Macro m = collide_cell<OP>(f, Fx, Fy, Fz, a.r);
-    flag_nonfinite(a.nan_key, a.step, ((g.x0 + x) * g.ny + y) * (int64_t)g.nz + z, m);
-    double* d = a.dst + buf_index(g, x + 1, 0, y, z);
+    flag_nonfinite<T>(a.nan_key, a.step, ((g.x0 + x) * g.ny + y) * (int64_t)g.nz + z, m);
+    T* d = static_cast<T*>(a.dst) + buf_index(g, x + 1, 0, y, z);
 #pragma unroll
     for (int i = 0; i < 27; ++i) st_pop(d + i * (int)g.dir_stride, f[i]);
     // edge planes: the outgoing directions go straight into the neighbour
     // slab's ghost plane (NVLink stores; halo pointers are peer mappings)
     if (x == 0 && a.halo.lo != nullptr) {
-        double* h = a.halo.lo + (int64_t)y * g.zp + z;
+        T* h = static_cast<T*>(a.halo.lo) + (int64_t)y * g.zp + z;
 #pragma unroll
-        for (int i = 0; i < 9; ++i) h[(int64_t)i * g.dir_stride] = f[i];
+        for (int i = 0; i < 9; ++i) h[(int64_t)i * g.dir_stride] = (T)f[i];
     }
     if (x == g.nxl - 1 && a.halo.hi != nullptr) {
-        double* h = a.halo.hi + (int64_t)y * g.zp + z;
+        T* h = static_cast<T*>(a.halo.hi) + (int64_t)y * g.zp + z;
 #pragma unroll
-        for (int i = 18; i < 27; ++i) h[(int64_t)(i - 18) * g.dir_stride] = f[i];
+        for (int i = 18; i < 27; ++i) h[(int64_t)(i - 18) * g.dir_stride] = (T)f[i];
     }
 }
 
 // K1: fused pull-stream + collide (+Guo) over local planes [x_begin, x_end).
 // One thread per cell, z fastest.  PULL=false collides the stored state in
 // place position (first step after an upload of pre-collision data).
-template <int OP, bool PULL, int MINB = 4>
+template <int OP, bool PULL, int MINB, class T>
 __global__ void __launch_bounds__(kSweepThreads, MINB) k_sweep(SweepArgs a) {
     const Geom& g = a.g;
     const int z = blockIdx.x * blockDim.x + threadIdx.x;
@@ -248,7 +288,7 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) k_sweep(SweepArgs a) {
     const int bz = (int)blockIdx.z;
     const int x = a.x_begin + (bz == 0 ? 0 : (bz == 1 ? g.nxl - 1 : bz - 1));
     const bool edge = bz < 2 && a.halo.edge_counter != nullptr;
-    if (z < g.nz && y < g.ny) sweep_cell<OP, PULL>(a, x, y, z);
+    if (z < g.nz && y < g.ny) sweep_cell<OP, PULL, T>(a, x, y, z);
     if (edge) edge_done(a.halo);  // whole CTA, uniform branch
 }
 
@@ -296,6 +336,18 @@ inline dim3 sweep_block(const Geom& g) {
     int bz = 32;
     while (bz < g.nz && bz < kSweepThreads) bz *= 2;
     return dim3(bz, kSweepThreads / bz, 1);
+}
+
+// launch K1 for one (operator, pull, storage) combination
+template <int MINB, class T>
+void launch_k_sweep(int op, bool pull, dim3 grd, dim3 blk, const SweepArgs& b, cudaStream_t s) {
+    if (op == 1) {
+        if (pull) k_sweep<1, true, MINB, T><<<grd, blk, 0, s>>>(b);
+        else k_sweep<1, false, MINB, T><<<grd, blk, 0, s>>>(b);
+    } else {
+        if (pull) k_sweep<0, true, MINB, T><<<grd, blk, 0, s>>>(b);
+        else k_sweep<0, false, MINB, T><<<grd, blk, 0, s>>>(b);
+    }
 }
 
 }  // namespace LBW_FLAVOR

@@ -1,8 +1,10 @@
 """Host view of one device-resident slab (the PdfField surface of
 lbwind.fields, fields.py:22-67).
 
-The populations live on the GPU as two fp64 [x+1][27][y][z] buffers; this
-object exposes the reference's accessors on demand:
+The populations live on the GPU as two [x+1][27][y][z] buffers of the run's
+storage dtype (fp64, or fp32 with ``precision: single``; arithmetic is fp64
+either way, _kernels.py:5-7); this object exposes the reference's accessors
+on demand, as arrays of that dtype:
 
     interior        (nx,ny,nz,27)  f_n, the post-stream state between steps
     interior_force  (nx,ny,nz,3)   the force of the latest collide (or the
@@ -47,7 +49,12 @@ class DeviceField:
         self.size = tuple(int(s) for s in size)
         self.origin = tuple(int(o) for o in origin)
         self.block_id = int(block_id)
-        self.dtype = np.dtype(np.float64)
+        self.dtype = np.dtype(sim.cfg.dtype)
+
+    def _stored(self, out):
+        # device values of a single-precision field are fp32-representable:
+        # the cast is exact
+        return out if self.dtype == np.float64 else out.astype(self.dtype)
 
     # -- device handle
     @property
@@ -62,7 +69,7 @@ class DeviceField:
     def download_pdf(self):
         out = np.empty(self.size + (27,))
         _lib.check(_lib.load().lbw_domain_download_pdf(self._d, _lib.ptr(out)), "download")
-        return out
+        return self._stored(out)
 
     def upload_pdf(self, f):
         f = np.ascontiguousarray(np.broadcast_to(np.asarray(f, dtype=np.float64),
@@ -77,11 +84,20 @@ class DeviceField:
     def interior(self, value):
         self.upload_pdf(value)
 
+    @property
+    def f(self):
+        """Snapshot of PdfField.f (fields.py:32): the populations with a
+        zero one-cell ghost ring (ghosts live only inside the device sweep)."""
+        nx, ny, nz = self.size
+        out = np.zeros((nx + 2, ny + 2, nz + 2, 27), self.dtype)
+        out[1:-1, 1:-1, 1:-1] = self.download_pdf()
+        return out
+
     # -- force
     def download_force(self):
         out = np.empty(self.size + (3,))
         _lib.check(_lib.load().lbw_domain_download_force(self._d, _lib.ptr(out)), "force")
-        return out
+        return self._stored(out)
 
     def set_force(self, force):
         if force is None:
@@ -103,7 +119,7 @@ class DeviceField:
     def download_macro(self):
         out = np.empty(self.size + (4,))
         _lib.check(_lib.load().lbw_domain_download_macro(self._d, _lib.ptr(out)), "macro")
-        return out
+        return self._stored(out)
 
     def set_macro(self, macro):
         macro = np.ascontiguousarray(np.broadcast_to(np.asarray(macro, dtype=np.float64),

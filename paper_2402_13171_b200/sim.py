@@ -114,16 +114,17 @@ class ActuatorPoint:
 
 
 class Simulation:
-    """kinematics: "host" replays the reference's numpy kinematics exactly
-    and uploads them each step; "device" advances the turbine trees on the
-    GPU (no per-step host work or H2D).  Default: host for arithmetic
-    "exact" (bit-identical kinematics), device for "fast"."""
+    """kinematics: "device" (default) advances the turbine trees on the GPU
+    (no per-step host work or H2D; positions within 1e-13 of the reference,
+    inside the actuator tolerance); "host" replays the reference's numpy
+    kinematics bit for bit and uploads them each step (test_acceptance.py
+    test_07 budget: host replay costs ~0.2 ms/step of Python)."""
 
     def __init__(self, cfg, rank=0, nranks=1, device=None, kinematics=None):
         self.cfg = cfg
         self.units = cfg.units
         if kinematics is None:
-            kinematics = "device" if cfg.arithmetic == "fast" else "host"
+            kinematics = "device"
         if kinematics not in ("host", "device"):
             raise ConfigError(f"kinematics must be host or device, got {kinematics!r}")
         self.kinematics = kinematics
@@ -134,9 +135,6 @@ class Simulation:
                                          cfg.higher_order_rates).validate()
         wind_lat = self.units.velocity_to_lattice(np.asarray(cfg.wind, dtype=np.float64))
         self.boundary = BoundarySpec(cfg.boundary_kind, u_in_lat=wind_lat)
-        if cfg.precision != "double":
-            raise ConfigError("run.precision: the device build computes and stores fp64 "
-                              "(precision: single is not supported yet)")
         self.device = cfg.device if device is None else int(device)
         self._domain = self._create_domain(lib, desc, rank, nranks)
         self.fields = [DeviceField(self, desc.size, desc.origin, desc.id)]
@@ -169,6 +167,7 @@ class Simulation:
         for k in range(3):
             d.u_in[k] = float(self.boundary.u_in_lat[k])
         d.rank, d.nranks = rank, nranks
+        d.precision = _lib.LBW_PREC_SINGLE if cfg.precision == "single" else _lib.LBW_PREC_DOUBLE
         d.feq_in_given = 1
         feq = self.boundary.inflow_populations()
         for i in range(27):
@@ -444,6 +443,38 @@ class Simulation:
         self.step_index += 1
         self._macro_fresh = False
 
+    def advance(self, n):
+        """n steps; with device kinematics (or no actuator points) they are
+        queued by ONE native call (lbw_domain_step(n)) instead of n Python
+        step() calls -- the same launches, no per-step host work.  A
+        non-finite state aborts at the first offending step as step() does."""
+        n = int(n)
+        if n <= 0:
+            return
+        if self.points and self.kinematics == "host":
+            for _ in range(n):
+                self.step()
+            return
+        t = self.timer
+        t.start_phase("collide")
+        _lib.check(_lib.load().lbw_domain_step(self._domain, n), "step")
+        t.stop_phase()
+        self._results = None
+        self._poll(wait=False)
+        if self.cfg.topologies:
+            if not self.points:
+                t.start_phase("turbine")
+                for _ in range(n):
+                    for topo in self.cfg.topologies:
+                        topo.advance(self.units.dt)
+                t.stop_phase()
+            else:
+                self._kin_stale = True
+                self._topo_pending = True
+        t.count_step(n)
+        self.step_index += n
+        self._macro_fresh = False
+
     def synchronize(self):
         _lib.check(_lib.load().lbw_domain_sync(self._domain), "sync")
         self._poll(wait=True)
@@ -465,8 +496,13 @@ class Simulation:
     def run(self):
         cfg = self.cfg
         self.timer.start()
-        for _ in range(cfg.steps):
-            self.step()
+        remaining = cfg.steps
+        while remaining > 0:
+            n = remaining
+            if cfg.cadence > 0:
+                n = min(n, cfg.cadence - self.step_index % cfg.cadence)
+            self.advance(n)
+            remaining -= n
             if cfg.cadence > 0 and self.step_index % cfg.cadence == 0:
                 self.synchronize()
                 self.timer.stop()

@@ -17,6 +17,10 @@ Fixtures (numpy .npz, fp64):
   rotor_*.npz    rotating 3-blade actuator line on 12^3 periodic and 16x12x12
                  inflow/outflow domains (x 8): per-step kinematics, sampled
                  rho/u, blade forces, final populations and force field
+  disk.npz       2-ring actuator disk on 16^3 (x 6)
+  single.npz     precision: single TGV, inflow/outflow BGK and rotor runs
+  disk_wake.npz  (--wake) test_05's reduced wake case at 8 and 12 cells per
+                 diameter: deficit, axis / plane-mean u_x, ring forces
 """
 
 import os
@@ -278,8 +282,159 @@ def gen_disk(tmp):
     np.savez_compressed(os.path.join(HERE, "disk.npz"), **out)
 
 
+def gen_single(tmp):
+    """precision: single (fp32 storage, fp64 arithmetic; config.py:30,
+    _kernels.py:5-7): a TGV, an inflow/outflow BGK run and the rotor on the
+    inflow domain, as float32 fixtures."""
+    out = {}
+    # TGV (as gen_tgv)
+    cfg = parse_config({"domain": {"cells": [12, 10, 8]},
+                        "fluid": {"kinematic_viscosity": 0.1353, "wind": [0.0, 0.0, 0.0],
+                                  "reference_velocity": 1.0},
+                        "resolution": {"mach": 0.2},
+                        "run": {"steps": 0, "precision": "single",
+                                "collision": {"operator": "cumulant",
+                                              "higher_order_rates": [1.0, 1.2, 1.0, 0.9]}}})
+    sim = Simulation(cfg)
+    nx, ny, nz = cfg.cells
+    X, Y = np.meshgrid(np.arange(nx) + 0.5, np.arange(ny) + 0.5, indexing="ij")
+    u0 = cfg.units.u_lat
+    vel = np.zeros((nx, ny, nz, 3))
+    vel[..., 0] = (u0 * np.sin(2 * np.pi * X / nx) * np.cos(2 * np.pi * Y / ny))[:, :, None]
+    vel[..., 1] = (-u0 * np.cos(2 * np.pi * X / nx) * np.sin(2 * np.pi * Y / ny))[:, :, None]
+    vel[..., 2] = 0.3 * u0 * np.sin(2 * np.pi * (np.arange(nz) + 0.5) / nz)[None, None, :]
+    out["tgv_vel"] = vel
+    sim.fields[0].initialize_equilibrium(1.0, vel, product=True)
+    out["tgv_f0"] = sim.fields[0].interior.copy()
+    out["tgv_omega"] = np.array(cfg.units.omega)
+    for _ in range(6):
+        sim.step()
+    out["tgv_f6"] = sim.fields[0].interior.copy()
+    sim._recompute_moments()
+    out["tgv_macro6"] = sim.fields[0].interior_macro.copy()
+    sim.close()
+    # inflow/outflow BGK (as gen_inflow)
+    cfg = parse_config({"domain": {"cells": [14, 8, 6], "periodicity": [False, True, True]},
+                        "fluid": {"kinematic_viscosity": 0.3, "wind": [8.0, 0.5, -0.25]},
+                        "resolution": {"cells_per_diameter": 8, "reference_diameter": 1.0,
+                                       "mach": 0.1},
+                        "run": {"steps": 0, "precision": "single",
+                                "boundary": "velocity_inflow_outflow",
+                                "collision": {"operator": "bgk"}}})
+    sim = Simulation(cfg)
+    rng = np.random.default_rng(29)
+    fld = sim.fields[0]
+    fld.interior[...] *= 1.0 + 0.01 * rng.uniform(-1, 1, fld.interior.shape)
+    out["inflow_f0"] = fld.interior.copy()
+    for _ in range(5):
+        sim.step()
+    out["inflow_f5"] = fld.interior.copy()
+    sim.close()
+    # rotor, inflow/outflow (as gen_rotor "inflow")
+    with open(os.path.join(tmp, "rotor.yaml"), "w") as fh:
+        fh.write(ROTOR_YAML)
+    with open(os.path.join(tmp, "sym.csv"), "w") as fh:
+        fh.write(sym_polar_csv())
+    cfg = parse_config({"domain": {"cells": [16, 12, 12], "periodicity": [False, True, True]},
+                        "fluid": {"kinematic_viscosity": 0.866, "wind": [8.0, 0.0, 0.0]},
+                        "resolution": {"cells_per_diameter": 8, "reference_diameter": 1.0,
+                                       "mach": 0.1},
+                        "run": {"steps": 0, "precision": "single",
+                                "boundary": "velocity_inflow_outflow",
+                                "collision": {"operator": "cumulant"}},
+                        "turbines": [{"file": "rotor.yaml", "position": [0.9, 0.75, 0.0]}],
+                        "polars": [{"id": "sym", "file": "sym.csv"}]}, base_dir=tmp)
+    sim = Simulation(cfg)
+    P, nsteps = len(sim.points), 8
+    samples = np.zeros((nsteps, P, 4))
+    blade = np.zeros((nsteps, P, 3))
+    for n in range(nsteps):
+        sim.step()
+        for p in sim.points:
+            samples[n, p.global_id, 0] = p.sampled_rho
+            samples[n, p.global_id, 1:] = p.sampled_u
+            blade[n, p.global_id] = p.blade_force
+    out["rotor_samples"] = samples
+    out["rotor_blade"] = blade
+    out["rotor_f_final"] = sim.fields[0].interior.copy()
+    out["rotor_force_final"] = sim.fields[0].interior_force.copy()
+    sim.close()
+    for k in ("tgv_f0", "tgv_f6", "tgv_macro6", "inflow_f0", "inflow_f5", "rotor_f_final",
+              "rotor_force_final"):
+        assert out[k].dtype == np.float32, k
+    np.savez_compressed(os.path.join(HERE, "single.npz"), **out)
+
+
+WAKE_DISK_YAML = """
+name: disk
+components:
+  - name: hub
+    discretization: {type: disk, radius: 0.5, rings: 8, sectors: 16,
+                     thrust_coefficient: 0.5}
+"""
+
+
+def wake_observables(sim, sample_velocity):
+    """Disk-averaged deficit (test_acceptance.py:381-400) plus the recomputed
+    axial velocity on the domain axis and its per-plane mean."""
+    edges = np.linspace(0.0, 0.5, 7)
+    mids = 0.5 * (edges[:-1] + edges[1:])
+    theta = (np.arange(12) + 0.5) * 2.0 * np.pi / 12
+
+    def disk_avg_ux(x_plane):
+        tot_a = tot_u = 0.0
+        for j in range(6):
+            a = (edges[j + 1] ** 2 - edges[j] ** 2) / 12
+            for t in theta:
+                pos = (x_plane, 2.5 + mids[j] * np.cos(t), 2.5 + mids[j] * np.sin(t))
+                tot_u += a * sample_velocity(pos)[0]
+                tot_a += a
+        return tot_u / tot_a
+
+    return 1.0 - disk_avg_ux(3.0) / disk_avg_ux(1.0)
+
+
+def gen_disk_wake(tmp):
+    """test_05's reduced-resolution wake case (test_acceptance.py:355-441)
+    at 8 and 12 cells/diameter: ~12 min of reference CPU time, so only with
+    --wake."""
+    from lbwind.output import _sample_velocity
+    with open(os.path.join(tmp, "wdisk.yaml"), "w") as fh:
+        fh.write(WAKE_DISK_YAML)
+    out = {"disk_yaml": np.array(WAKE_DISK_YAML)}
+    for cpd, steps in ((8, 1200), (12, 1800)):
+        cfg = parse_config({
+            "domain": {"diameters": [10, 5, 5]},
+            "fluid": {"kinematic_viscosity": 0.09237, "wind": [8.0, 0.0, 0.0]},
+            "resolution": {"cells_per_diameter": cpd, "reference_diameter": 1.0,
+                           "mach": 0.05},
+            "run": {"steps": 0, "collision": {"operator": "bgk"}},
+            "turbines": [{"file": "wdisk.yaml", "position": [3.0, 2.5, 2.5]}]}, base_dir=tmp)
+        sim = Simulation(cfg)
+        for _ in range(steps):
+            sim.step()
+        sim._recompute_moments()
+        macro = sim.fields[0].interior_macro
+        ny, nz = macro.shape[1:3]
+        out[f"cpd{cpd}_steps"] = steps
+        out[f"cpd{cpd}_deficit"] = wake_observables(sim, lambda p: _sample_velocity(sim, p))
+        out[f"cpd{cpd}_ux_axis"] = macro[:, ny // 2, nz // 2, 1].copy()
+        out[f"cpd{cpd}_ux_plane_mean"] = macro[..., 1].mean(axis=(1, 2))
+        out[f"cpd{cpd}_blade"] = np.array([p.blade_force for p in sim.points])
+        sim.close()
+    np.savez_compressed(os.path.join(HERE, "disk_wake.npz"), **out)
+
+
 def main():
     import tempfile
+    if "--single" in sys.argv:
+        with tempfile.TemporaryDirectory() as tmp:
+            gen_single(tmp)
+        return
+    if "--wake" in sys.argv:
+        with tempfile.TemporaryDirectory() as tmp:
+            gen_disk_wake(tmp)
+        return
     _kernels.warm_up()
     gen_collide()
     gen_block()
@@ -291,6 +446,7 @@ def main():
         gen_rotor("inflow", (16, 12, 12), (False, True, True), "velocity_inflow_outflow",
                   (0.9, 0.75, 0.0), tmp)
         gen_disk(tmp)
+        gen_single(tmp)
     print("golden vectors written to", HERE, "with lbwind", lbwind.__version__)
 
 

@@ -51,12 +51,13 @@ def write_rotor_files(d):
 
 
 def rotor_raw(cells, periodic, boundary="periodic", position=(0.9, 0.3, 0.0), steps=0,
-              arithmetic="exact", nu=0.866, cpd=8, mach=0.1, operator="cumulant"):
+              arithmetic="exact", nu=0.866, cpd=8, mach=0.1, operator="cumulant",
+              precision="double"):
     return {"domain": {"cells": list(cells), "periodicity": list(periodic)},
             "fluid": {"kinematic_viscosity": nu, "wind": [8.0, 0.0, 0.0]},
             "resolution": {"cells_per_diameter": cpd, "reference_diameter": 1.0, "mach": mach},
             "run": {"steps": steps, "boundary": boundary, "arithmetic": arithmetic,
-                    "collision": {"operator": operator}},
+                    "precision": precision, "collision": {"operator": operator}},
             "turbines": [{"file": "rotor.yaml", "position": list(position)}],
             "polars": [{"id": "sym", "file": "sym.csv"}]}
 
@@ -91,7 +92,7 @@ def oracle_for(sim):
                             for comp, spec, offs, areas, sl in sim._disk_groups]}
     ref = orc.OracleSim(cfg.cells, periodic=cfg.periodicity, op=cfg.operator, omega=u.omega,
                         rates=cfg.higher_order_rates, boundary=cfg.boundary_kind,
-                        u_in=sim.boundary.u_in_lat, points=points)
+                        u_in=sim.boundary.u_in_lat, points=points, dtype=cfg.dtype)
     ref.initialize_equilibrium(1.0, sim.boundary.u_in_lat, product=(cfg.operator == "cumulant"))
     return ref
 

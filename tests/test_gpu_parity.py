@@ -294,7 +294,7 @@ def test_rotor_spreading_matches_oracle_bitwise_given_forces(gpu):
     """With identical point forces the deposit is bit-identical: compare the
     device force field against the oracle fed the device's blade forces."""
     cfg, tmp = rotor_config(cells=(12, 12, 12), position=(0.9, 0.3, 0.0))
-    sim = Simulation(cfg)
+    sim = Simulation(cfg, kinematics="host")
     sim.step()
     blade = sim._alm_results()[2]
     kin = sim._kin.copy()
@@ -341,3 +341,4 @@ def test_kernels_are_native(gpu):
     sim.synchronize()
     sim.close()
     assert _lib.kernel_launches() > before
+

@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert set(declared) == set(_lib.SIGNATURES), "ctypes table and header disagree"
-    assert lib.lbw_abi_version() == 1
+    assert lib.lbw_abi_version() == _lib.ABI_VERSION
 
 
 def test_library_is_sm100a():

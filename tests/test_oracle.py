@@ -132,3 +132,52 @@ def test_disk_oracle_matches_reference(golden):
     np.testing.assert_allclose(ref.force[1:-1, 1:-1, 1:-1], g["force_final"], rtol=1e-10,
                                atol=1e-18)
     tmp.cleanup()
+
+
+def test_single_precision_oracle_matches_reference(golden):
+    """precision: single (config.py:30; fp32 storage, fp64 arithmetic):
+    TGV and inflow/outflow BGK bit-exact; rotor samples / forces to the
+    actuator tolerance."""
+    from paper_2402_13171_b200 import parse_config
+    from paper_2402_13171_b200.sim import HostKinematics
+    from tests.scenarios import oracle_for, rotor_config
+    g = golden("single.npz")
+    # TGV 12x10x8
+    ref = orc.OracleSim((12, 10, 8), op="cumulant", omega=float(g["tgv_omega"]),
+                        rates=(1.0, 1.2, 1.0, 0.9), dtype=np.float32)
+    ref.initialize_equilibrium(1.0, g["tgv_vel"], product=True)
+    assert np.array_equal(ref.interior, g["tgv_f0"])
+    for _ in range(6):
+        ref.step()
+    assert np.array_equal(ref.interior, g["tgv_f6"])
+    assert np.array_equal(ref.recompute_moments(), g["tgv_macro6"])
+    # inflow/outflow BGK
+    cfg = parse_config({"domain": {"cells": [14, 8, 6], "periodicity": [False, True, True]},
+                        "fluid": {"kinematic_viscosity": 0.3, "wind": [8.0, 0.5, -0.25]},
+                        "resolution": {"cells_per_diameter": 8, "reference_diameter": 1.0,
+                                       "mach": 0.1},
+                        "run": {"precision": "single", "boundary": "velocity_inflow_outflow",
+                                "collision": {"operator": "bgk"}}})
+    u_in = cfg.units.velocity_to_lattice(np.array([8.0, 0.5, -0.25]))
+    ref = orc.OracleSim((14, 8, 6), periodic=(False, True, True), op="bgk",
+                        omega=cfg.units.omega, boundary="velocity_inflow_outflow", u_in=u_in,
+                        dtype=np.float32)
+    ref.interior[...] = g["inflow_f0"]
+    for _ in range(5):
+        ref.step()
+    assert np.array_equal(ref.interior, g["inflow_f5"])
+    # rotor on the inflow domain
+    cfg, tmp = rotor_config((16, 12, 12), (False, True, True), "velocity_inflow_outflow",
+                            (0.9, 0.75, 0.0), precision="single")
+    host = HostKinematics(cfg)
+    ref = oracle_for(host)
+    for n in range(g["rotor_samples"].shape[0]):
+        kin = host.refresh()
+        ref.step(kin)
+        host.advance()
+        np.testing.assert_allclose(ref.samples, g["rotor_samples"][n], rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(ref.blade, g["rotor_blade"][n], rtol=1e-10, atol=1e-13)
+    # the float32 rounding absorbs the einsum-order noise of the actuator path
+    assert np.array_equal(ref.interior, g["rotor_f_final"])
+    assert np.array_equal(ref.force[1:-1, 1:-1, 1:-1], g["rotor_force_final"])
+    tmp.cleanup()
