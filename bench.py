@@ -3,7 +3,8 @@
 "MLUP/s (D3Q27 cumulant fp64 + ALM) at 1/2/4/8 B200; % of HBM roofline").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--arithmetic exact|fast] [--config c2|c1|c3]
+                    [--arithmetic exact|fast] [--config c2|c1|c3|c4]
+                    [--precision double|single]
 
 Workload (BASELINE.json configs[1], "C2"): 256x128x128 D3Q27 cumulant fp64,
 velocity inflow / zero-gradient outflow in x, periodic y/z, one rotating
@@ -73,6 +74,7 @@ components:
 
 BYTES_PER_LUP = 2 * 27 * 8     # algorithmic bytes of the fused sweep (fp64)
 METRIC = "MLUP/s (D3Q27 cumulant fp64 + ALM)"
+METRIC_SINGLE = "MLUP/s (D3Q27 cumulant fp64 arithmetic, fp32 storage + ALM)"
 
 
 def polar_csv():
@@ -113,7 +115,7 @@ def workload(name, n_gpus):
 POINTS_PER_BLADE = 6
 
 
-def make_config(name, n_gpus, arithmetic, tmpdir):
+def make_config(name, n_gpus, arithmetic, tmpdir, precision="double"):
     from paper_2402_13171_b200 import parse_config
     with open(os.path.join(tmpdir, "rotor.yaml"), "w") as fh:
         fh.write(ROTOR.replace("points: 6", f"points: {POINTS_PER_BLADE}"))
@@ -121,6 +123,9 @@ def make_config(name, n_gpus, arithmetic, tmpdir):
         fh.write(polar_csv())
     raw, desc = workload(name, n_gpus)
     raw.setdefault("run", {})["arithmetic"] = arithmetic
+    raw["run"]["precision"] = precision
+    if precision == "single":
+        desc = desc.replace("fp64", "fp64 arithmetic / fp32 storage")
     return parse_config(raw, base_dir=tmpdir), desc
 
 
@@ -193,7 +198,8 @@ def run_ours(args, rank, world, local_rank):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     tmp = tempfile.TemporaryDirectory()
-    cfg, desc = make_config(args.config, world, args.arithmetic, tmp.name)
+    cfg, desc = make_config(args.config, world, args.arithmetic, tmp.name, args.precision)
+    bytes_per_lup = BYTES_PER_LUP if args.precision == "double" else 2 * 27 * 4
     if world > 1:
         from paper_2402_13171_b200 import parallel
         sim = parallel.SlabSimulation(cfg, rank=rank, nranks=world, device=local_rank)
@@ -261,33 +267,35 @@ def run_ours(args, rank, world, local_rank):
     e2e = cells_total * args.steps / t_e2e / 1e6
 
     peaks = _measured_peaks()
-    achieved = BYTES_PER_LUP * cells_local / (sweep_avg_ms / 1e3) / 1e9
+    achieved = bytes_per_lup * cells_local / (sweep_avg_ms / 1e3) / 1e9
     out = None
     if rank == 0:
         out = {
-            "metric": METRIC, "value": round(value, 2), "unit": "MLUP/s", "n_gpus": world,
+            "metric": METRIC if args.precision == "double" else METRIC_SINGLE,
+            "value": round(value, 2), "unit": "MLUP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
             "higher_is_better": True,
             "scaling": "strong" if args.config == "c4" else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "cells": list(cfg.cells),
                        "cells_per_gpu": cells_local, "actuator_points": P,
-                       "arithmetic": cfg.arithmetic, "parallelism": f"x-slab x{world}",
-                       "l2": "state (2 x 27 x 8 B x cells) far larger than the 126 MB L2; "
-                             "no flush needed"},
+                       "arithmetic": cfg.arithmetic, "storage": cfg.precision,
+                       "parallelism": f"x-slab x{world}",
+                       "l2": f"state (2 x 27 x {bytes_per_lup // 54} B x cells) far larger "
+                             "than the 126 MB L2; no flush needed"},
             "e2e": {"value": round(e2e, 2), "unit": "MLUP/s",
                     "h2d_bytes_per_step": P * 15 * 8,
                     "d2h_bytes_per_step": P * 3 * 8 + 8},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1),
                          "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": round(achieved / peaks["hbm_gbs"], 4),
-                         "traffic": _ncu_traffic(args.config, cells_local),
+                         "traffic": _ncu_traffic(args.config, cells_local, args.precision),
                          "kernel": "lbw::k_sweep<cumulant,pull> (fused stream-collide)",
-                         "bytes_per_lup": BYTES_PER_LUP,
+                         "bytes_per_lup": bytes_per_lup,
                          "sweep_ms": round(sweep_avg_ms, 4),
                          "sweep_share_of_step": round(sweep_avg_ms / (ms / args.steps), 4),
                          "peak_source": peaks["source"],
-                         "lup_ceiling_mlups": round(peaks["hbm_gbs"] * 1e3 / BYTES_PER_LUP, 1)},
+                         "lup_ceiling_mlups": round(peaks["hbm_gbs"] * 1e3 / bytes_per_lup, 1)},
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
         }
@@ -310,10 +318,11 @@ def _measured_peaks():
         return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md 6.65 TB/s)"}
 
 
-def _ncu_traffic(config, cells_local):
+def _ncu_traffic(config, cells_local, precision="double"):
     """dram bytes per sweep launch from the committed ncu capture, scaled to
     this launch's cell count (profiles/ncu_sweep.json), or None."""
-    path = os.path.join(ROOT, "profiles", "ncu_sweep.json")
+    path = os.path.join(ROOT, "profiles",
+                        "ncu_sweep.json" if precision == "double" else "ncu_sweep_single.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
@@ -359,11 +368,11 @@ def cpu_baseline(args, budget_s=20.0):
     cores = len(os.sched_getaffinity(0))
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
     tmp = tempfile.TemporaryDirectory()
-    cfg, desc = make_config(args.config, 1, "exact", tmp.name)
+    cfg, desc = make_config(args.config, 1, "exact", tmp.name, args.precision)
     host = _HostOnlySim(cfg)
     t1 = _oracle_run(cfg, 1, host)
     steps = int(max(1, min(50, budget_s / max(t1, 1e-3))))
-    cfg, desc = make_config(args.config, 1, "exact", tmp.name)
+    cfg, desc = make_config(args.config, 1, "exact", tmp.name, args.precision)
     host = _HostOnlySim(cfg)
     t = _oracle_run(cfg, steps, host)
     cells = int(np.prod(cfg.cells))
@@ -379,12 +388,12 @@ def run_reference(args, rank):
         return None
     cb = cpu_baseline(args, budget_s=args.cpu_budget)
     tmp = tempfile.TemporaryDirectory()
-    cfg, desc = make_config(args.config, 1, "exact", tmp.name)
+    cfg, desc = make_config(args.config, 1, "exact", tmp.name, args.precision)
     tmp.cleanup()
     # time exactly K steps (after W warm-ups) so the arm is comparable
     from oracle import oracle as orc  # noqa: F401
     tmp = tempfile.TemporaryDirectory()
-    cfg, desc = make_config(args.config, 1, "exact", tmp.name)
+    cfg, desc = make_config(args.config, 1, "exact", tmp.name, args.precision)
     host = _HostOnlySim(cfg)
     t = _oracle_run(cfg, args.steps, host)
     tmp.cleanup()
@@ -392,7 +401,8 @@ def run_reference(args, rank):
     value = cells * args.steps / t / 1e6
     cb["value"] = round(value, 3)
     cb["sample"] = f"{args.steps} full steps of {desc}, C oracle, {cb['cores']} threads"
-    return {"metric": METRIC, "value": round(value, 3), "unit": "MLUP/s", "n_gpus": 0,
+    return {"metric": METRIC if args.precision == "double" else METRIC_SINGLE,
+            "value": round(value, 3), "unit": "MLUP/s", "n_gpus": 0,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * t / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -411,6 +421,7 @@ def main():
     ap.add_argument("--config", choices=("c1", "c2", "c3", "c4"), default="c2")
     ap.add_argument("--points-per-blade", type=int, default=6)
     ap.add_argument("--arithmetic", choices=("exact", "fast"), default="fast")
+    ap.add_argument("--precision", choices=("double", "single"), default="double")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
