@@ -93,6 +93,12 @@ struct KinDev {
     double* spin_hist;   // (3, nc, 9): spin state of step j in slot j % 3
     double* cs_hist;     // (3, nc, kCS)
     int32_t hist_slot;
+    int32_t stage_points;   // per-point constants fit in shared memory
+    const int32_t* order;        // (nc) components by tree depth
+    const int32_t* level_start;  // (nlevels+1) into order
+    int32_t nlevels;
+    const int32_t* is_static;    // (nc) world transform constant in time
+    int32_t skip_static;         // their state from the previous launch is valid
     double dx;
 };
 
@@ -114,6 +120,10 @@ struct AlmState {
     int32_t n_rings = 0;
     double vscale = 0, rho_ref = 0, dt2 = 0, den = 0;
     ForceSet set[2];
+    // Few points: the sweep sums a tagged cell's force from the points'
+    // deposit data itself (no fill kernel, no pool); many points: K5 fills
+    // per-row pools.
+    bool on_the_fly = false;
     double* h_ring = nullptr;   // pinned (kRing, P, 18)
     cudaEvent_t ring_ev[kRing] = {};
     int ring_pos = 0;
@@ -137,6 +147,11 @@ struct AlmState {
     double* k_disk_center = nullptr;
     double k_dx = 1.0;
     int64_t kin_state_step = 0;  // step whose kinematics the device spins represent
+    bool kin_stage_points = false;
+    int32_t *k_order = nullptr, *k_level_start = nullptr, *k_static = nullptr;
+    int32_t k_nlevels = 0;
+    bool kin_static_ready = false;   // static components' state computed once
+    size_t kin_smem = 0;
     std::vector<void*> allocs;
 
     // device view for step m: outputs by parity, kinematics by m % 3
@@ -160,9 +175,9 @@ struct AlmState {
         a.kin = kin + (size_t)(m % 3) * n * kKin;
         a.samples = samples + (size_t)parity * n * 4;
         a.blade = blade + (size_t)parity * n * 3;
-        a.flat = flat;
-        a.dep_cell = dep_cell;
-        a.dep_w = dep_w;
+        a.flat = flat + (size_t)parity * n * 3;
+        a.dep_cell = dep_cell + (size_t)parity * n * 9;
+        a.dep_w = dep_w + (size_t)parity * n * 9;
         a.clamp_flags = clamp_flags;
         a.error_flags = error_flags;
         a.point_ring = point_ring;
@@ -195,6 +210,12 @@ struct AlmState {
         k.spin_hist = k_spin_hist;
         k.cs_hist = k_cs_hist;
         k.hist_slot = 0;
+        k.stage_points = kin_stage_points ? 1 : 0;
+        k.order = k_order;
+        k.level_start = k_level_start;
+        k.nlevels = k_nlevels;
+        k.is_static = k_static;
+        k.skip_static = 0;
         k.dx = k_dx;
         return k;
     }
@@ -238,17 +259,6 @@ __device__ void cross3(const double* a, const double* b, double* out) {
     out[1] = c1;
     out[2] = c2;
 }
-// max |T^T T - I| > 1e-12 (turbine.py:_DRIFT_TOL)
-__device__ bool drifted(const double* T) {
-    double m = 0.0;
-    for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j) {
-            double s = T[i] * T[j] + T[3 + i] * T[3 + j] + T[6 + i] * T[6 + j];
-            if (i == j) s -= 1.0;
-            m = fmax(m, fabs(s));
-        }
-    return m > 1e-12;
-}
 // Gram-Schmidt on the columns (turbine.py:83-90)
 __device__ void reorth(double* T) {
     double c0[3] = {T[0], T[3], T[6]}, c1[3] = {T[1], T[4], T[7]};
@@ -277,16 +287,179 @@ __device__ double np_mod(double a, double b) {
     return m;
 }
 
+// Warp-cooperative 3x3 algebra on shared memory for the tree walk: every
+// lane of the warp calls; lanes 0..8 (0..2) own one entry each, with the
+// per-entry arithmetic of mm3 / mv3 / cross3 / drifted (bit-identical).
+__device__ void wmm3(const double* A, const double* B, double* C, int lane) {
+    double t = 0.0;
+    if (lane < 9) {
+        const int i = lane / 3, j = lane % 3;
+        t = A[i * 3] * B[j] + A[i * 3 + 1] * B[3 + j] + A[i * 3 + 2] * B[6 + j];
+    }
+    __syncwarp();
+    if (lane < 9) C[lane] = t;
+    __syncwarp();
+}
+__device__ void wmv3(const double* A, const double* v, double* out, int lane) {
+    double t = 0.0;
+    if (lane < 3) t = A[lane * 3] * v[0] + A[lane * 3 + 1] * v[1] + A[lane * 3 + 2] * v[2];
+    __syncwarp();
+    if (lane < 3) out[lane] = t;
+    __syncwarp();
+}
+__device__ void wcross3(const double* a, const double* b, double* out, int lane) {
+    double t = 0.0;
+    if (lane == 0) t = a[1] * b[2] - a[2] * b[1];
+    if (lane == 1) t = a[2] * b[0] - a[0] * b[2];
+    if (lane == 2) t = a[0] * b[1] - a[1] * b[0];
+    __syncwarp();
+    if (lane < 3) out[lane] = t;
+    __syncwarp();
+}
+// max |T^T T - I| > 1e-12 (turbine.py:_DRIFT_TOL)
+__device__ bool wdrifted(const double* T, int lane) {
+    bool over = false;
+    if (lane < 9) {
+        const int i = lane / 3, j = lane % 3;
+        double s = T[i] * T[j] + T[3 + i] * T[3 + j] + T[6 + i] * T[6 + j];
+        if (i == j) s -= 1.0;
+        over = fabs(s) > 1e-12;   // max(...) > tol, NaN entries ignored as fmax does
+    }
+    return __any_sync(0xffffffffu, over);
+}
+__device__ void wreorth(double* T, int lane) {
+    __syncwarp();
+    if (lane == 0) reorth(T);
+    __syncwarp();
+}
+
+// parameters per component in the kinematics CTA's shared memory:
+// rel_p 3, rel_T 9, axis 3, rate 1, rstep 9, spin 9, parent 1, first 1, is_disk 1, disk p 3, T 9
+constexpr int kKP = 49;
+
+// One component of the tree walk (turbine.py:259-311, sim.py:167-191) by
+// one warp: lanes 0..8 own the entries of each 3x3 product (the per-entry
+// arithmetic of mm3 / mv3 / cross3, bit-identical to a serial walk).
+__device__ void walk_component(const KinDev& k, double* prm, double* cs, int c, int advance,
+                               const double* off, const double* orient, double* wt,
+                               const double* I3s, const double* zero3s, int lane) {
+    double* tmp9 = wt;
+    double* tmp9b = wt + 9;
+    double* tmp3 = wt + 18;
+    double* tmp3b = wt + 21;
+    double* q = prm + c * kKP;
+    double* s = cs + c * kCS;
+    const int par = (int)q[34];
+    const double* Pp = par >= 0 ? cs + par * kCS + CS_P : zero3s;
+    const double* PT = par >= 0 ? cs + par * kCS + CS_T : I3s;
+    const double* Pv = par >= 0 ? cs + par * kCS + CS_V : zero3s;
+    const double* Pw = par >= 0 ? cs + par * kCS + CS_W : zero3s;
+    double* spin = q + 25;
+    const double rate = q[15];
+    if (advance && rate != 0.0) {
+        wmm3(spin, q + 16, spin, lane);
+        if (wdrifted(spin, lane)) wreorth(spin, lane);
+    }
+    double* Tp_rp = tmp3;
+    double* Tp_Tr = tmp9;
+    wmv3(PT, q, Tp_rp, lane);
+    wmm3(PT, q + 3, Tp_Tr, lane);
+    if (lane < 3) s[CS_P + lane] = Pp[lane] + Tp_rp[lane];
+    wmm3(Tp_Tr, spin, s + CS_T, lane);
+    if (wdrifted(s + CS_T, lane)) wreorth(s + CS_T, lane);
+    wcross3(Pw, Tp_rp, tmp3b, lane);
+    if (lane < 3) {
+        s[CS_V + lane] = Pv[lane] + tmp3b[lane];
+        s[CS_W + lane] = Pw[lane];
+        s[CS_AX + lane] = par >= 0 ? cs[par * kCS + CS_AX + lane] : 0.0;
+    }
+    if (lane == 0) s[CS_HAX] = par >= 0 ? cs[par * kCS + CS_HAX] : 0.0;
+    __syncwarp();
+    if (rate != 0.0) {
+        wmv3(Tp_Tr, q + 12, s + CS_AX, lane);
+        if (lane == 0) s[CS_HAX] = 1.0;
+        if (lane < 3) s[CS_W + lane] = s[CS_W + lane] + s[CS_AX + lane] * rate;
+        __syncwarp();
+    }
+    if (lane < 9) s[CS_R + lane] = spin[lane];
+    __syncwarp();
+    const int first = (int)q[35];
+    if (q[36] != 0.0) {
+        // disk centre (update_disk, turbine.py:237-241) and its velocity
+        double* Tc_p = tmp3;
+        double* TcT = tmp9b;
+        wmv3(s + CS_T, q + 37, Tc_p, lane);
+        if (lane < 3) s[CS_SP + lane] = s[CS_P + lane] + Tc_p[lane];
+        wmm3(s + CS_T, q + 40, TcT, lane);
+        wmm3(TcT, spin, s + CS_ST, lane);
+        wcross3(s + CS_W, Tc_p, tmp3b, lane);
+        if (lane < 3) s[CS_VS + lane] = s[CS_V + lane] + tmp3b[lane];
+        __syncwarp();
+    } else if (first >= 0) {
+        const double* W = s + CS_T;
+        double* Tp_o0 = tmp3;
+        double* Tp_O0 = tmp9b;
+        wmv3(W, off + (int64_t)first * 3, Tp_o0, lane);
+        if (lane < 3) s[CS_SP + lane] = s[CS_P + lane] + Tp_o0[lane];
+        wmm3(W, orient + (int64_t)first * 9, Tp_O0, lane);
+        wmm3(Tp_O0, spin, s + CS_ST, lane);
+        wcross3(s + CS_W, Tp_o0, tmp3b, lane);
+        if (lane < 3) {
+            s[CS_VS + lane] = s[CS_V + lane] + tmp3b[lane];
+            s[CS_WS + lane] = s[CS_W + lane];
+        }
+        __syncwarp();
+        if (rate != 0.0) {
+            wmv3(Tp_O0, q + 12, tmp3b, lane);
+            if (lane < 3) s[CS_WS + lane] = s[CS_WS + lane] + tmp3b[lane] * rate;
+            __syncwarp();
+        }
+    }
+}
+
 // KK: tree walk + point kinematics, one CTA.  The component parameters and
 // state are staged in shared memory (the walk itself is one thread: a chain
 // of dependent 3x3 products down the tree); points are then evaluated in
 // parallel.  Layout per component in smem: params[kKP] then state[kCS].
 // rel_p 3, rel_T 9, axis 3, rate 1, rstep 9, spin 9, parent 1, first 1, is_disk 1, disk p 3, T 9
-constexpr int kKP = 49;
 __device__ void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g, int per_x,
                                int advance, double* ksm) {
+#ifdef LBW_KK_PROF
+    long long t0 = clock64();
+#endif
     double* prm = ksm;                         // (nc, kKP)
     double* cs = ksm + (size_t)k.nc * kKP;     // (nc, kCS)
+    // per-point constants staged too when they fit (k.stage_points): every
+    // global load of the kernel is then issued in this one parallel pass
+    double* sm_off = cs + (size_t)k.nc * kCS;            // (P,3)
+    double* sm_orient = sm_off + (size_t)a.n * 3;        // (P,9)
+    double* sm_lframe = sm_orient + (size_t)a.n * 9;     // (P,9)
+    int32_t* sm_comp = reinterpret_cast<int32_t*>(sm_lframe + (size_t)a.n * 9);  // (P)
+    // walk schedule (always staged, after the point block or after cs)
+    int32_t* sm_order = k.stage_points ? sm_comp + a.n
+                                       : reinterpret_cast<int32_t*>(cs + (size_t)k.nc * kCS);
+    int32_t* sm_static = sm_order + k.nc;
+    int32_t* sm_lstart = sm_static + k.nc;
+    for (int i = threadIdx.x; i < k.nc; i += blockDim.x) {
+        sm_order[i] = k.order[i];
+        sm_static[i] = k.is_static[i];
+    }
+    for (int i = threadIdx.x; i <= k.nlevels; i += blockDim.x) sm_lstart[i] = k.level_start[i];
+    if (k.skip_static)
+        for (int i = threadIdx.x; i < k.nc * kCS; i += blockDim.x)
+            if (k.is_static[i / kCS]) cs[i] = k.cs[i];
+    const double* off = k.stage_points ? sm_off : k.off;
+    const double* orient = k.stage_points ? sm_orient : k.orient;
+    const double* lframe = k.stage_points ? sm_lframe : k.lframe;
+    const int32_t* point_comp = k.stage_points ? sm_comp : k.point_comp;
+    if (k.stage_points) {
+        for (int i = threadIdx.x; i < a.n * 3; i += blockDim.x) sm_off[i] = k.off[i];
+        for (int i = threadIdx.x; i < a.n * 9; i += blockDim.x) {
+            sm_orient[i] = k.orient[i];
+            sm_lframe[i] = k.lframe[i];
+        }
+        for (int i = threadIdx.x; i < a.n; i += blockDim.x) sm_comp[i] = k.point_comp[i];
+    }
     for (int i = threadIdx.x; i < k.nc * kKP; i += blockDim.x) {
         const int c = i / kKP, j = i % kKP;
         double v;
@@ -303,87 +476,44 @@ __device__ void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g, 
         prm[i] = v;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        const double I3[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
-        const double zero3[3] = {0, 0, 0};
-        for (int c = 0; c < k.nc; ++c) {
-            double* q = prm + c * kKP;
-            double* s = cs + c * kCS;
-            const int par = (int)q[34];
-            const double* Pp = par >= 0 ? cs + par * kCS + CS_P : zero3;
-            const double* PT = par >= 0 ? cs + par * kCS + CS_T : I3;
-            const double* Pv = par >= 0 ? cs + par * kCS + CS_V : zero3;
-            const double* Pw = par >= 0 ? cs + par * kCS + CS_W : zero3;
-            double* spin = q + 25;
-            const double rate = q[15];
-            if (advance && rate != 0.0) {
-                mm3(spin, q + 16, spin);
-                if (drifted(spin)) reorth(spin);
+#ifdef LBW_KK_PROF
+    long long t1 = clock64();
+#endif
+    {
+        // level by level: the components of one depth in parallel, one warp
+        // each.  Components whose world transform never changes (no
+        // rotation on their path) keep the state of the first launch.
+        __shared__ double I3s[9], zero3s[3];
+        __shared__ double wtmp[8][24];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+        if (threadIdx.x < 9) I3s[threadIdx.x] = (threadIdx.x % 4 == 0) ? 1.0 : 0.0;
+        if (threadIdx.x < 3) zero3s[threadIdx.x] = 0.0;
+        __syncthreads();
+        for (int L = 0; L < k.nlevels; ++L) {
+            for (int j = sm_lstart[L] + warp; j < sm_lstart[L + 1]; j += nwarp) {
+                const int c = sm_order[j];
+                if (k.skip_static && sm_static[c]) continue;
+                walk_component(k, prm, cs, c, advance, off, orient, wtmp[warp], I3s, zero3s, lane);
             }
-            double Tp_rp[3], Tp_Tr[9];
-            mv3(PT, q, Tp_rp);
-            mm3(PT, q + 3, Tp_Tr);
-            for (int i = 0; i < 3; ++i) s[CS_P + i] = Pp[i] + Tp_rp[i];
-            mm3(Tp_Tr, spin, s + CS_T);
-            if (drifted(s + CS_T)) reorth(s + CS_T);
-            double cr[3];
-            cross3(Pw, Tp_rp, cr);
-            for (int i = 0; i < 3; ++i) s[CS_V + i] = Pv[i] + cr[i];
-            for (int i = 0; i < 3; ++i) s[CS_W + i] = Pw[i];
-            if (par >= 0) {
-                for (int i = 0; i < 3; ++i) s[CS_AX + i] = cs[par * kCS + CS_AX + i];
-                s[CS_HAX] = cs[par * kCS + CS_HAX];
-            } else {
-                s[CS_AX] = s[CS_AX + 1] = s[CS_AX + 2] = 0.0;
-                s[CS_HAX] = 0.0;
-            }
-            if (rate != 0.0) {
-                mv3(Tp_Tr, q + 12, s + CS_AX);
-                s[CS_HAX] = 1.0;
-                for (int i = 0; i < 3; ++i) s[CS_W + i] = s[CS_W + i] + s[CS_AX + i] * rate;
-            }
-            for (int i = 0; i < 9; ++i) s[CS_R + i] = spin[i];
-            const int first = (int)q[35];
-            if (q[36] != 0.0) {
-                // disk centre (update_disk, turbine.py:237-241) and its velocity
-                double Tc_p[3], TcT[9];
-                mv3(s + CS_T, q + 37, Tc_p);
-                for (int i = 0; i < 3; ++i) s[CS_SP + i] = s[CS_P + i] + Tc_p[i];
-                mm3(s + CS_T, q + 40, TcT);
-                mm3(TcT, spin, s + CS_ST);
-                cross3(s + CS_W, Tc_p, cr);
-                for (int i = 0; i < 3; ++i) s[CS_VS + i] = s[CS_V + i] + cr[i];
-            } else if (first >= 0) {
-                const double* W = s + CS_T;
-                double Tp_o0[3], Tp_O0[9], o0[3], O0[9];
-                for (int i = 0; i < 3; ++i) o0[i] = k.off[(int64_t)first * 3 + i];
-                for (int i = 0; i < 9; ++i) O0[i] = k.orient[(int64_t)first * 9 + i];
-                mv3(W, o0, Tp_o0);
-                for (int i = 0; i < 3; ++i) s[CS_SP + i] = s[CS_P + i] + Tp_o0[i];
-                mm3(W, O0, Tp_O0);
-                mm3(Tp_O0, spin, s + CS_ST);
-                cross3(s + CS_W, Tp_o0, cr);
-                for (int i = 0; i < 3; ++i) s[CS_VS + i] = s[CS_V + i] + cr[i];
-                for (int i = 0; i < 3; ++i) s[CS_WS + i] = s[CS_W + i];
-                if (rate != 0.0) {
-                    double ax[3];
-                    mv3(Tp_O0, q + 12, ax);
-                    for (int i = 0; i < 3; ++i) s[CS_WS + i] = s[CS_WS + i] + ax[i] * rate;
-                }
-            }
+            __syncthreads();
         }
     }
-    __syncthreads();
+#ifdef LBW_KK_PROF
+    long long t2 = clock64();
+#endif
     // persist spin + component state (downloadable), evaluate the points
     for (int i = threadIdx.x; i < k.nc * 9; i += blockDim.x)
         k.spin[i] = k.spin_hist[(int64_t)k.hist_slot * k.nc * 9 + i] =
             prm[(i / 9) * kKP + 25 + i % 9];
     for (int i = threadIdx.x; i < k.nc * kCS; i += blockDim.x)
         k.cs[i] = k.cs_hist[(int64_t)k.hist_slot * k.nc * kCS + i] = cs[i];
+#ifdef LBW_KK_PROF
+    long long t3 = clock64();
+#endif
     const int64_t dims[3] = {g.nxg, g.ny, g.nz};
     const int per[3] = {per_x, g.per_y, g.per_z};
     for (int p = threadIdx.x; p < a.n; p += blockDim.x) {
-        const int c = k.point_comp[p];
+        const int c = point_comp[p];
         const double* s = cs + c * kCS;
         const int kk = p - k.line_first[c];
         double pos[3], fr[9], vel[3];
@@ -392,7 +522,7 @@ __device__ void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g, 
             // world = centre.p + offs @ centre.T^T (sim.py:182-187); the disk
             // axis (centre frame +x) rides in the e_chord slot
             double rel[3];
-            mv3(s + CS_ST, k.off + (int64_t)p * 3, rel);
+            mv3(s + CS_ST, off + (int64_t)p * 3, rel);
             for (int i = 0; i < 3; ++i) pos[i] = s[CS_SP + i] + rel[i];
             for (int i = 0; i < 3; ++i) vel[i] = s[CS_VS + i];
             const double fr_d[9] = {s[CS_ST], s[CS_ST + 3], s[CS_ST + 6], 0, 1, 0, 0, 0, 1};
@@ -403,9 +533,9 @@ __device__ void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g, 
             for (int i = 0; i < 3; ++i) vel[i] = s[CS_VS + i];
         } else {
             double rel[3], tmp[9], cr[3];
-            mv3(s + CS_ST, k.off + (int64_t)p * 3, rel);
+            mv3(s + CS_ST, off + (int64_t)p * 3, rel);
             for (int i = 0; i < 3; ++i) pos[i] = s[CS_SP + i] + rel[i];
-            mm3(s + CS_ST, k.orient + (int64_t)p * 9, tmp);
+            mm3(s + CS_ST, orient + (int64_t)p * 9, tmp);
             mm3(tmp, s + CS_R, fr);
             cross3(s + CS_WS, rel, cr);
             for (int i = 0; i < 3; ++i) vel[i] = s[CS_VS + i] + cr[i];
@@ -422,9 +552,15 @@ __device__ void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g, 
         if (disk) {
             for (int i = 0; i < 9; ++i) out[6 + i] = fr[i];
         } else {
-            for (int f = 0; f < 3; ++f) mv3(fr, k.lframe + (int64_t)p * 9 + f * 3, out + 6 + 3 * f);
+            for (int f = 0; f < 3; ++f) mv3(fr, lframe + (int64_t)p * 9 + f * 3, out + 6 + 3 * f);
         }
     }
+#ifdef LBW_KK_PROF
+    __syncthreads();
+    if (threadIdx.x == 0)
+        printf("KKPROF stage %lld walk %lld persist %lld points %lld\n", t1 - t0, t2 - t1, t3 - t2,
+               clock64() - t3);
+#endif
 }
 
 __global__ void k_kinematics(KinDev k, AlmDev a, Geom g, int per_x, int advance) {
@@ -492,11 +628,14 @@ __device__ int macro_at_raw(const Geom& g, const MacroDev& m, int64_t gx, int64_
         put(m.dense + cell * 4);
         return MA_OWNED;
     }
+    // the force row key first, so its latency overlaps the population loads
+    const uint64_t key = m.fv.row_key ? m.fv.row_key[x * g.ny + gy] : 0ull;
     double f[27];
     if (m.pull) load_cell_any<true>(m.buf, g, (int)x, (int)gy, (int)gz, f);
     else load_cell_any<false>(m.buf, g, (int)x, (int)gy, (int)gz, f);
     double Fx, Fy, Fz;
-    load_force_any(m.fv, g, (int)x, (int)gy, (int)gz, Fx, Fy, Fz);
+    if (g.single) force_from_key<float>(m.fv, g, key, (int)x, (int)gy, (int)gz, Fx, Fy, Fz);
+    else force_from_key<double>(m.fv, g, key, (int)x, (int)gy, (int)gz, Fx, Fy, Fz);
     const Macro mm = moments_exact(f, Fx, Fy, Fz, 1.0);
     out[0] = mm.rho;
     out[1] = mm.ux;
@@ -521,46 +660,99 @@ __device__ __forceinline__ double roma(double r) {
     return 0.0;
 }
 
-// np.interp for a whole warp: every lane gets the same result.  The
-// bracketing index (largest j with xp[j] <= x, polars.py:65-80 tables are
-// increasing) is counted with ballots over 32-row chunks instead of a
-// binary search of dependent loads.
-__device__ int interp_index_warp(double x, const double* xp, int n, int lane) {
-    int cnt = 0;
-    for (int k0 = 0; k0 < n; k0 += 32) {
-        const int k = k0 + lane;
-        const bool le = k < n && xp[k] <= x;
-        cnt += __popc(__ballot_sync(0xffffffffu, le));
+// Per-point data that does not depend on the flow, loaded at the start of
+// K4 so its latency overlaps the sampling loads: the point's polar table
+// sits in registers (one row per lane) when it has at most 32 rows.
+struct PointStatic {
+    int pid, off, rows;
+    double chord, elen, twist;
+    double xl, cll, cdl;   // this lane's polar row
+};
+__device__ __forceinline__ PointStatic load_static(const AlmDev& a, int p, int lane) {
+    PointStatic ps;
+    ps.pid = a.polar_index[p];
+    ps.chord = a.chord[p];
+    ps.elen = a.elen[p];
+    ps.twist = a.twist[p];
+    ps.off = ps.rows = 0;
+    ps.xl = ps.cll = ps.cdl = 0.0;
+    if (ps.pid >= 0) {
+        ps.off = a.polar_offset[ps.pid];
+        ps.rows = a.polar_rows[ps.pid];
+        if (lane < ps.rows) {
+            ps.xl = a.p_alpha[ps.off + lane];
+            ps.cll = a.p_cl[ps.off + lane];
+            ps.cdl = a.p_cd[ps.off + lane];
+        }
     }
-    return cnt - 1;
+    return ps;
 }
-__device__ double interp_at(double x, const double* xp, const double* fp, int n, int j) {
-    if (isnan(x)) return x;
-    if (x < xp[0]) return fp[0];
-    if (x > xp[n - 1]) return fp[n - 1];
-    if (x == xp[n - 1]) return fp[n - 1];
-    if (xp[j] == x) return fp[j];
-    const double slope = (fp[j + 1] - fp[j]) / (xp[j + 1] - xp[j]);
-    double r = slope * (x - xp[j]) + fp[j];
-    if (isnan(r)) {
-        r = slope * (x - xp[j + 1]) + fp[j + 1];
-        if (isnan(r) && fp[j] == fp[j + 1]) r = fp[j];
+
+// polar row r of the point: from the lanes' registers (<= 32 rows) or memory
+__device__ __forceinline__ void polar_row(const AlmDev& a, const PointStatic& ps, int r,
+                                          double& x, double& cl, double& cd) {
+    if (ps.rows <= 32) {
+        x = __shfl_sync(0xffffffffu, ps.xl, r);
+        cl = __shfl_sync(0xffffffffu, ps.cll, r);
+        cd = __shfl_sync(0xffffffffu, ps.cdl, r);
+    } else {
+        x = a.p_alpha[ps.off + r];
+        cl = a.p_cl[ps.off + r];
+        cd = a.p_cd[ps.off + r];
     }
-    return r;
+}
+
+// np.interp (polars.py:65-80) of cl and cd at x for the whole warp: the
+// bracketing row (largest j with xp[j] <= x; tables are increasing) is
+// counted with a ballot instead of a binary search of dependent loads.
+__device__ void polar_interp(const AlmDev& a, const PointStatic& ps, double x, int lane,
+                             double& cl, double& cd) {
+    const int n = ps.rows;
+    double x0, c0l, c0d, xn, cnl, cnd;
+    polar_row(a, ps, 0, x0, c0l, c0d);
+    polar_row(a, ps, n - 1, xn, cnl, cnd);
+    int cnt = 0;
+    if (n <= 32) {
+        cnt = __popc(__ballot_sync(0xffffffffu, lane < n && ps.xl <= x));
+    } else {
+        for (int k0 = 0; k0 < n; k0 += 32) {
+            const int k = k0 + lane;
+            cnt += __popc(__ballot_sync(0xffffffffu, k < n && a.p_alpha[ps.off + k] <= x));
+        }
+    }
+    const int j = cnt > 0 ? (cnt - 1 < n - 2 ? cnt - 1 : n - 2) : 0;
+    double xa, cla, cda, xb, clb, cdb;
+    polar_row(a, ps, j, xa, cla, cda);
+    polar_row(a, ps, j + 1, xb, clb, cdb);
+    auto one = [&](double fa, double fb, double f0, double fn) -> double {
+        if (isnan(x)) return x;
+        if (x < x0) return f0;
+        if (x > xn) return fn;
+        if (x == xn) return fn;
+        if (xa == x) return fa;
+        const double slope = (fb - fa) / (xb - xa);
+        double r = slope * (x - xa) + fa;
+        if (isnan(r)) {
+            r = slope * (x - xb) + fb;
+            if (isnan(r) && fa == fb) r = fa;
+        }
+        return r;
+    };
+    cl = one(cla, clb, c0l, cnl);
+    cd = one(cda, cdb, c0d, cnd);
 }
 
 // blade-element force on the BLADE (actuator.py:117-146, sim.py:218-235),
 // evaluated by a whole warp (identical values on every lane; lane 0 raises
-// the flags): the polar lookups are one ballot round each.
-__device__ void blade_force_warp(const AlmDev& a, int p, const double* kin, const double* acc,
-                                 double* blade, int lane) {
+// the flags).  kr: the point's kinematics row.
+__device__ void blade_force_warp(const AlmDev& a, const PointStatic& ps, const double* kr,
+                                 const double* acc, double* blade, int lane) {
     blade[0] = blade[1] = blade[2] = 0.0;
-    const int pid = a.polar_index[p];
-    if (pid < 0) return;
-    const double* vel = kin + 3;
-    const double* ec = kin + 6;
-    const double* en = kin + 9;
-    const double* es = kin + 12;
+    if (ps.pid < 0) return;
+    const double* vel = kr + 3;
+    const double* ec = kr + 6;
+    const double* en = kr + 9;
+    const double* es = kr + 12;
     double urel[3];
     for (int c = 0; c < 3; ++c) urel[c] = acc[1 + c] * a.vscale - vel[c];
     const double along = dot3(urel, es);
@@ -569,22 +761,22 @@ __device__ void blade_force_warp(const AlmDev& a, int p, const double* kin, cons
     const double speed = sqrt(dot3(up, up));
     if (!(speed >= 1e-12)) return;  // DEGENERATE_SPEED (actuator.py:30)
     const double phi = atan2(dot3(up, en), dot3(up, ec));
-    double alpha = phi - a.twist[p];
+    double alpha = phi - ps.twist;
     double ed[3], el[3];
     for (int c = 0; c < 3; ++c) ed[c] = up[c] / speed;
     cross3(es, ed, el);
-    const int off = a.polar_offset[pid], rows = a.polar_rows[pid];
-    const double* xp = a.p_alpha + off;
-    if (alpha < xp[0] || alpha > xp[rows - 1]) {
-        if (lane == 0) atomicOr(&a.clamp_flags[pid], 1);
-        alpha = fmin(fmax(alpha, xp[0]), xp[rows - 1]);
+    double x0, c0l, c0d, xn, cnl, cnd;
+    polar_row(a, ps, 0, x0, c0l, c0d);
+    polar_row(a, ps, ps.rows - 1, xn, cnl, cnd);
+    if (alpha < x0 || alpha > xn) {
+        if (lane == 0) atomicOr(&a.clamp_flags[ps.pid], 1);
+        alpha = fmin(fmax(alpha, x0), xn);
     }
-    const int j = isnan(alpha) ? 0 : interp_index_warp(alpha, xp, rows, lane);
-    const double cl = interp_at(alpha, xp, a.p_cl + off, rows, j < 0 ? 0 : j);
-    const double cd = interp_at(alpha, xp, a.p_cd + off, rows, j < 0 ? 0 : j);
+    double cl, cd;
+    polar_interp(a, ps, alpha, lane, cl, cd);
     const double rho_phys = acc[0] * a.rho_ref;
     if (!(rho_phys > 0.0) && lane == 0) atomicOr(a.error_flags, 1);
-    const double scale = 0.5 * rho_phys * speed * speed * a.chord[p] * a.elen[p];
+    const double scale = 0.5 * rho_phys * speed * speed * ps.chord * ps.elen;
     for (int c = 0; c < 3; ++c) blade[c] = scale * (cl * el[c] + cd * ed[c]);
 }
 
@@ -615,6 +807,19 @@ __device__ void deposit_axis(double x, int64_t L, int periodic, int32_t* dc, dou
     }
 }
 
+// (x,y) row of deposit pair q = p*9 + k (k: 3 x-cells x 3 y-cells of point
+// p) as a slab row index, or -1 when it is not a cell of this slab.
+__device__ __forceinline__ int32_t pair_row(const AlmDev& a, const Geom& g, int q) {
+    const int32_t* dc = a.dep_cell + (int64_t)(q / 9) * 9;
+    const int k = q % 9;
+    const int32_t cxg = dc[k / 3], cy = dc[3 + k % 3];
+    const int64_t x = (int64_t)cxg - g.x0;
+    if (cxg < 0 || cy < 0 || x < 0 || x >= g.nxl) return -1;
+    return (int32_t)(x * g.ny + cy);
+}
+
+constexpr int kOnTheFlyMaxPoints = 64;
+
 // K4: one warp per point
 // phase 0: single slab, everything in one pass.  Multi-slab: phase 1 only
 // computes the cube values of this slab's cells and stores them into the
@@ -627,7 +832,21 @@ struct CubeArgs {
 
 __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, const ForceSet& s,
                            int phase, const CubeArgs& cube, int p, int lane) {
-    const double* kin = a.kin + (int64_t)p * kKin;
+    // flow-independent loads first: kinematics row (one value per lane),
+    // polar / chord data; deposit cells need only the position
+    const double kv = lane < 15 ? a.kin[(int64_t)p * kKin + lane] : 0.0;
+    const PointStatic ps = load_static(a, p, lane);
+    const bool disk = a.point_ring != nullptr && a.point_ring[p] >= 0;
+    double kr[15];
+    for (int k = 0; k < 15; ++k) kr[k] = __shfl_sync(0xffffffffu, kv, k);
+    const double* kin = kr;
+    if (phase != 1 && lane >= 8 && lane <= 10) {
+        const int k = lane - 8;
+        const int64_t L = k == 0 ? g.nxg : (k == 1 ? g.ny : g.nz);
+        const int per = k == 0 ? m.per_x : (k == 1 ? g.per_y : g.per_z);
+        deposit_axis(kin[k], L, per, a.dep_cell + (int64_t)p * 9 + 3 * k,
+                     a.dep_w + (int64_t)p * 9 + 3 * k);
+    }
     int64_t j0[3];
     double t[3];
     for (int k = 0; k < 3; ++k) {
@@ -664,8 +883,14 @@ __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, co
         const double w = wx * wy * wz;
         for (int q = 0; q < 4; ++q) acc[q] += w * vc[q];
     }
-    int32_t* dc = a.dep_cell + (int64_t)p * 9;
-    double* dw = a.dep_w + (int64_t)p * 9;
+    if (s.flag_rows && phase != 1) {
+        // tag this step's rows (benign race: equal values)
+        __syncwarp();
+        if (lane < 9) {
+            const int32_t row = pair_row(a, g, p * 9 + lane);
+            if (row >= 0) s.row_key[row] = row_key_of(s.tag, 0);
+        }
+    }
     // Multi-slab: only points whose Roma support reaches this slab (their
     // sampling cube is then complete: own + neighbour cells) are evaluated;
     // per-point outputs come from the slab owning floor(x).  (Warp-uniform.)
@@ -679,40 +904,12 @@ __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, co
         relevant = c - g.x0 >= 0 && c - g.x0 < g.nxl;
     }
     double blade[3] = {0.0, 0.0, 0.0};
-    const bool disk = a.point_ring != nullptr && a.point_ring[p] >= 0;
-    if (relevant && !disk) blade_force_warp(a, p, kin, acc, blade, lane);
+    if (relevant && !disk) blade_force_warp(a, ps, kin, acc, blade, lane);
     if (lane == 0) {
         for (int q = 0; q < 4; ++q) a.samples[p * 4 + q] = owner ? acc[q] : 0.0;
         for (int c = 0; c < 3; ++c) {
             a.blade[p * 3 + c] = owner ? blade[c] : 0.0;
             a.flat[p * 3 + c] = -blade[c] * a.dt2 / a.den;  // units.py:69
-        }
-    } else if (lane >= 1 && lane <= 3) {
-        const int k = lane - 1;
-        const int64_t L = k == 0 ? g.nxg : (k == 1 ? g.ny : g.nz);
-        const int per = k == 0 ? m.per_x : (k == 1 ? g.per_y : g.per_z);
-        deposit_axis(kin[k], L, per, dc + 3 * k, dw + 3 * k);
-    }
-    __syncwarp();
-    if (lane < 9) {  // one (x,y) row per lane
-        const int32_t cxg = dc[lane / 3], cy = dc[3 + lane % 3];
-        const int64_t x = (int64_t)cxg - g.x0;
-        if (cxg >= 0 && cy >= 0 && x >= 0 && x < g.nxl) {
-            const int64_t row = x * g.ny + cy;
-            // claim the row for this step (tag) unless a point already did;
-            // keys of earlier steps are simply overwritten (no clearing)
-            unsigned long long* key = reinterpret_cast<unsigned long long*>(s.row_key + row);
-            unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(key);
-            while ((uint32_t)(old >> 32) != s.tag) {
-                const unsigned long long prev = atomicCAS(key, old, row_key_of(s.tag, -2));
-                if (prev == old) {
-                    const int32_t slot = atomicAdd(s.count, 1);
-                    s.slot_row[slot] = (int32_t)row;
-                    atomicExch(key, row_key_of(s.tag, slot));
-                    break;
-                }
-                old = prev;
-            }
         }
     }
 }
@@ -766,15 +963,34 @@ __global__ void k_alm_disks(AlmDev a) {
     if (r < a.n_rings) disk_ring(a, r);
 }
 
-// K5 for one claimed row, one warp: lanes own z = z0 + lane; the points
-// touching the row are visited in ascending id (ballot over chunks of 32),
-// so each cell's sum has the same order as K5 / the reference.
-__device__ void fill_row_warp(const AlmDev& a, const Geom& g, const ForceSet& s, int slot,
-                              int lane) {
-    const int32_t row = s.slot_row[slot];
+// K5: one warp per deposit pair q.  The lowest pair touching a row owns it:
+// it writes the row's force into pool slot q (per cell, the sum over all
+// points touching the row in ascending id, as the reference's spreading
+// loop adds them, actuator.py:241-246) and tags the row for this step.  No
+// claims, counters or clearing: rows of earlier steps just keep old tags.
+constexpr int kFillSmemPairs = 4096;
+__global__ void k_alm_fill(AlmDev a, Geom g, ForceSet s) {
+    __shared__ int32_t rows_sm[kFillSmemPairs];
+    const int npairs = a.n * 9;
+    const bool staged = npairs <= kFillSmemPairs;
+    if (staged)
+        for (int q = threadIdx.x; q < npairs; q += blockDim.x) rows_sm[q] = pair_row(a, g, q);
+    __syncthreads();
+    const int q = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (q >= npairs) return;  // uniform per warp
+    const int32_t row = staged ? rows_sm[q] : pair_row(a, g, q);
+    if (row < 0) return;
+    bool dup = false;
+    for (int c0 = 0; c0 < q && !dup; c0 += 32) {
+        const int q2 = c0 + lane;
+        const bool same = q2 < q && (staged ? rows_sm[q2] : pair_row(a, g, q2)) == row;
+        dup = __any_sync(0xffffffffu, same);
+    }
+    if (dup) return;
     const int64_t xg = row / g.ny + g.x0;
     const int32_t y = row % g.ny;
-    const int64_t row0 = (int64_t)slot * 3 * g.zp;
+    const int64_t row0 = (int64_t)q * 3 * g.zp;
     for (int z0 = 0; z0 < g.nz; z0 += 32) {
         const int z = z0 + lane;
         double F[3] = {0.0, 0.0, 0.0};
@@ -787,9 +1003,9 @@ __device__ void fill_row_warp(const AlmDev& a, const Geom& g, const ForceSet& s,
                 const double* dw = a.dep_w + (int64_t)pl * 9;
                 double wx = 0.0, wy = 0.0;
                 bool hx = false, hy = false;
-                for (int q = 0; q < 3; ++q) {
-                    if (dc[q] == xg) { hx = true; wx = dw[q]; }
-                    if (dc[3 + q] == y) { hy = true; wy = dw[3 + q]; }
+                for (int t = 0; t < 3; ++t) {
+                    if (dc[t] == xg) { hx = true; wx = dw[t]; }
+                    if (dc[3 + t] == y) { hy = true; wy = dw[3 + t]; }
                 }
                 hit = hx && hy;
                 wxy = wx * wy;
@@ -803,9 +1019,11 @@ __device__ void fill_row_warp(const AlmDev& a, const Geom& g, const ForceSet& s,
                 if (z < g.nz) {
                     const int32_t* dc = a.dep_cell + (int64_t)p * 9 + 6;
                     const double* dw = a.dep_w + (int64_t)p * 9 + 6;
-                    for (int k = 0; k < 3; ++k) {
-                        if (dc[k] == z) {
-                            const double w = w2 * dw[k];
+                    for (int t = 0; t < 3; ++t) {
+                        if (dc[t] == z) {
+                            const double w = w2 * dw[t];
+                            // `force[c] += w * F_lat` on an array of the storage
+                            // dtype rounds after every addition (actuator.py:246)
                             if (g.single)
                                 for (int c = 0; c < 3; ++c)
                                     F[c] = stored<float>(F[c] + w * a.flat[p * 3 + c]);
@@ -826,14 +1044,7 @@ __device__ void fill_row_warp(const AlmDev& a, const Geom& g, const ForceSet& s,
             }
         }
     }
-}
-
-// K5: one warp per claimed row of this step's set (4 rows per CTA)
-__global__ void k_alm_fill(AlmDev a, Geom g, ForceSet s) {
-    const int slot = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-    if (blockIdx.x == 0 && threadIdx.x == 0) *s.next_count = 0;  // the set's next use
-    if (slot >= *s.count) return;  // uniform per warp
-    fill_row_warp(a, g, s, slot, threadIdx.x & 31);
+    if (lane == 0) s.row_key[row] = row_key_of(s.tag, q);
 }
 
 template <class T>
@@ -875,7 +1086,17 @@ bool alm_ready(const lbw_domain* d, int64_t m) { return d->alm->ready_step == m;
 bool alm_can_prelaunch(const lbw_domain* d) { return d->prelaunch && d->alm->kin_device; }
 
 ForceView alm_force_view(const lbw_domain* d, int64_t m) {
-    return d->alm->set[m & 1].view((uint32_t)(m + 1));
+    const AlmState* s = d->alm;
+    ForceView v = s->set[m & 1].view((uint32_t)(m + 1));
+    if (s->on_the_fly) {
+        const AlmDev a = s->dev(m);
+        v.pool = nullptr;
+        v.npts = s->n;
+        v.dep_cell = a.dep_cell;
+        v.dep_w = a.dep_w;
+        v.flat = a.flat;
+    }
+    return v;
 }
 
 int alm_invalidate(lbw_domain* d) {
@@ -898,14 +1119,16 @@ static int kin_launch(lbw_domain* d, int64_t j) {
     }
     const int advance = j > s->kin_state_step ? 1 : 0;
     LBW_CK(cudaStreamWaitEvent(s->kin_stream, s->ev_chain_done[j & 1], 0));
-    const size_t ksm = (size_t)s->nc * (kKP + kCS) * sizeof(double);
+    const size_t ksm = s->kin_smem;
     KinDev kd = s->kdev();
     kd.hist_slot = (int32_t)(j % 3);
+    kd.skip_static = s->kin_static_ready ? 1 : 0;
     k_kinematics<<<1, 256, ksm, s->kin_stream>>>(kd, s->dev(j), d->g,
                                                   d->desc.periodic[0] ? 1 : 0, advance);
     count_launch();
     LBW_CK(cudaGetLastError());
     LBW_CK(cudaEventRecord(s->ev_kin_done, s->kin_stream));
+    s->kin_static_ready = true;
     s->kin_state_step = j;
     s->kin_valid[j % 3] = j;
     return LBW_OK;
@@ -918,12 +1141,10 @@ int alm_launch(lbw_domain* d, int64_t m) {
     const int par = (int)(m & 1);
     const AlmDev a = s->dev(m);
     const int per_x = d->desc.periodic[0] ? 1 : 0;
-    // this step's use of force set m&1: claims tagged m+1, counter by use
+    // this step's use of force set m&1: rows tagged m+1
     ForceSet fs = s->set[par];
-    const int use = (int)((m >> 1) & 1);
-    fs.count = fs.counts + use;
-    fs.next_count = fs.counts + (1 - use);
     fs.tag = (uint32_t)(m + 1);
+    fs.flag_rows = s->on_the_fly ? 1 : 0;
     if (s->kin_device) {
         if (s->kin_valid[m % 3] != m) {
             int rc = kin_launch(d, m);
@@ -969,8 +1190,11 @@ int alm_launch(lbw_domain* d, int64_t m) {
         k_alm_disks<<<(unsigned)((s->n_rings + 63) / 64), 64, 0, st>>>(a);
         count_launch();
     }
-    k_alm_fill<<<(unsigned)((fs.cap + 3) / 4), 128, 0, st>>>(a, g, fs);
-    count_launch(2);
+    if (!s->on_the_fly) {
+        k_alm_fill<<<(unsigned)((s->n * 9 + 3) / 4), 128, 0, st>>>(a, g, fs);
+        count_launch();
+    }
+    count_launch();
     LBW_CK(cudaGetLastError());
     LBW_CK(cudaEventRecord(d->ev_alm_done, st));
     if (s->kin_device) {
@@ -1043,10 +1267,10 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     A(&s->kin, (size_t)3 * P * kKin);
     A(&s->samples, (size_t)2 * P * 4);
     A(&s->blade, (size_t)2 * P * 3);
-    A(&s->flat, (size_t)P * 3);
+    A(&s->flat, (size_t)2 * P * 3);
     A(&s->cube, (size_t)2 * P * 32);
-    A(&s->dep_cell, (size_t)P * 9);
-    A(&s->dep_w, (size_t)P * 9);
+    A(&s->dep_cell, (size_t)2 * P * 9);
+    A(&s->dep_w, (size_t)2 * P * 9);
     A(&s->clamp_flags, std::max(1, desc->n_polars));
     A(&s->error_flags, 1);
     const int R = desc->point_ring ? desc->n_rings : 0;
@@ -1059,14 +1283,15 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     }
     // sparse force sets: a point touches at most 3x3 (x,y) rows
     const int64_t rows = (int64_t)d->g.nxl * d->g.ny;
-    const int64_t cap = std::min<int64_t>(rows, (int64_t)9 * P);
+    s->on_the_fly = P <= kOnTheFlyMaxPoints;
+    const int64_t cap = s->on_the_fly ? 0 : (int64_t)9 * P;   // slot = deposit pair index
     for (auto& fs : s->set) {
         A(&fs.row_key, rows);
-        char* pool = nullptr;
-        A(&pool, (size_t)cap * 3 * d->g.zp * elem_bytes(d->g));
-        fs.pool = pool;
-        A(&fs.slot_row, cap);
-        A(&fs.counts, 2);
+        if (cap) {
+            char* pool = nullptr;
+            A(&pool, (size_t)cap * 3 * d->g.zp * elem_bytes(d->g));
+            fs.pool = pool;
+        }
         fs.cap = cap;
     }
     if (rc) {
@@ -1105,8 +1330,7 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     if (rc == LBW_OK) {
         for (auto& fs : s->set) {
             // keys with tag 0xffffffff match no step (chain tags are step+1)
-            if (cudaMemset(fs.row_key, 0xff, rows * 8) != cudaSuccess ||
-                cudaMemset(fs.counts, 0, 8) != cudaSuccess) {
+            if (cudaMemset(fs.row_key, 0xff, rows * 8) != cudaSuccess) {
                 cudaGetLastError();
                 rc = LBW_ECUDA;
             }
@@ -1176,7 +1400,26 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
     A(&s->k_cs_hist, (size_t)3 * C * kCS);
     A(&s->k_is_disk, C);
     A(&s->k_disk_center, (size_t)C * 12);
+    A(&s->k_order, C);
+    A(&s->k_static, C);
+    A(&s->k_level_start, (size_t)C + 1);
     if (rc) return rc;
+    // walk schedule: components by depth (parents precede children), and
+    // which ones never move (no rotation on the path from the root)
+    std::vector<int32_t> depth(C), stat(C), order, lstart;
+    for (int c = 0; c < C; ++c) {
+        const int pa = kd->parent[c];
+        depth[c] = pa < 0 ? 0 : depth[pa] + 1;
+        stat[c] = kd->rate[c] == 0.0 && (pa < 0 || stat[pa]);
+    }
+    const int maxd = *std::max_element(depth.begin(), depth.end());
+    for (int L = 0; L <= maxd; ++L) {
+        lstart.push_back((int32_t)order.size());
+        for (int c = 0; c < C; ++c)
+            if (depth[c] == L) order.push_back(c);
+    }
+    lstart.push_back((int32_t)order.size());
+    s->k_nlevels = maxd + 1;
     auto H = [&](void* dst, const void* src, size_t bytes) {
         if (rc == LBW_OK && cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
             cudaGetLastError();
@@ -1197,6 +1440,9 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
     H(s->k_off, kd->offsets, (size_t)P * 24);
     H(s->k_orient, kd->orientations, (size_t)P * 72);
     H(s->k_lframe, kd->local_frames, (size_t)P * 72);
+    H(s->k_order, order.data(), (size_t)C * 4);
+    H(s->k_static, stat.data(), (size_t)C * 4);
+    H(s->k_level_start, lstart.data(), lstart.size() * 4);
     {
         std::vector<int32_t> isd(C, 0);
         std::vector<double> dcen((size_t)C * 12, 0.0);
@@ -1209,7 +1455,10 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
         H(s->k_disk_center, dcen.data(), (size_t)C * 96);
     }
     if (rc) return rc;
-    const size_t ksm = (size_t)C * (kKP + kCS) * sizeof(double);
+    size_t ksm = (size_t)C * (kKP + kCS) * sizeof(double) + (size_t)(3 * C + 1) * 4;
+    const size_t kpts = (size_t)P * 21 * sizeof(double) + (size_t)P * sizeof(int32_t);
+    s->kin_stage_points = ksm + kpts <= 160 * 1024;
+    if (s->kin_stage_points) ksm += kpts;
     if (ksm > 48 * 1024 &&
         cudaFuncSetAttribute(k_kinematics, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)ksm) != cudaSuccess) {
@@ -1217,6 +1466,7 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
         set_error("too many turbine components for the kinematics CTA");
         return LBW_EINVAL;
     }
+    s->kin_smem = ksm;
     if (!s->kin_stream) {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -1235,6 +1485,7 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
     s->kin_device = true;
     s->kin_state_step = d->step - (kd->advance_first ? 1 : 0);
     s->kin_valid[0] = s->kin_valid[1] = s->kin_valid[2] = -1;
+    s->kin_static_ready = false;
     s->ready_step = -1;
     return LBW_OK;
 }

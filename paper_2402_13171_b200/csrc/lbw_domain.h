@@ -32,12 +32,9 @@ void set_error(const std::string& msg);
 struct ForceSet {
     uint64_t* row_key = nullptr;   // (nxl*ny)
     void* pool = nullptr;          // (cap, 3, zp) of the storage type
-    int32_t* slot_row = nullptr;   // (cap) row of each used slot
-    int32_t* count = nullptr;      // used slots: the claiming step's counter
-    int32_t* counts = nullptr;     // (2) counters, alternating between uses of the set
-    int32_t* next_count = nullptr; // counter of the set's next use (zeroed by its fill)
-    uint32_t tag = 0;              // tag of the claiming step
-    int64_t cap = 0;
+    uint32_t tag = 0;              // tag of the filling step
+    int32_t flag_rows = 0;         // actuator set without a pool: K4 tags the rows
+    int64_t cap = 0;               // slots: user set one per row, actuator set 9 per point
     ForceView view(uint32_t t) const { return ForceView{row_key, pool, t}; }
 };
 

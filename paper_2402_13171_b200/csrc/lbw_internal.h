@@ -45,8 +45,14 @@ __host__ __device__ inline size_t elem_bytes(const Geom& g) { return g.single ? 
 // body force uses tag 0).
 struct ForceView {
     const uint64_t* row_key;  // (nxl*ny); nullptr = no force anywhere
-    const void* pool;         // [slot][3][zp] of the storage type
+    const void* pool;         // [slot][3][zp] of the storage type, or nullptr:
     uint32_t tag;
+    // ... actuator view: a tagged row's force is summed from the points'
+    // deposit cells in ascending id at the cell (few points, see lbw_alm.cu)
+    int32_t npts;
+    const int32_t* dep_cell;  // (npts, 3 axes, 3) global cell or -1
+    const double* dep_w;      // (npts, 3, 3) Roma weights
+    const double* flat;       // (npts, 3) lattice force on the fluid
 };
 __host__ __device__ inline uint64_t row_key_of(uint32_t tag, int32_t slot) {
     return ((uint64_t)tag << 32) | (uint32_t)slot;

@@ -172,20 +172,62 @@ __device__ __forceinline__ void load_cell_simple(const T* __restrict__ src, cons
         f[i] = ld_pop(px[cx_of(i) + 1] + (i * ds + yo[cy_of(i) + 1] + zo[cz_of(i) + 1]));
 }
 
+// Roma spreading evaluated at one cell (actuator.py:190-247): the sum over
+// the points whose 3x3x3 support holds the cell, in ascending id, each
+// adding ((wx*wy)*wz)*F_lat; with float storage every addition is rounded
+// as `+=` on the reference's float32 force array rounds it.
+template <class T>
+__device__ __forceinline__ void actuator_force(const ForceView& fv, int64_t xg, int y, int z,
+                                            double& Fx, double& Fy, double& Fz) {
+    double F[3] = {0.0, 0.0, 0.0};
+    for (int p = 0; p < fv.npts; ++p) {
+        const int32_t* dc = fv.dep_cell + (int64_t)p * 9;
+        const double* dw = fv.dep_w + (int64_t)p * 9;
+        double wx = 0.0, wy = 0.0;
+        bool hx = false, hy = false;
+        for (int t = 0; t < 3; ++t) {
+            if (dc[t] == xg) { hx = true; wx = dw[t]; }
+            if (dc[3 + t] == y) { hy = true; wy = dw[3 + t]; }
+        }
+        if (!(hx && hy)) continue;
+        // explicit roundings: no FMA contraction in either flavour's TU
+        const double wxy = __dmul_rn(wx, wy);
+        for (int t = 0; t < 3; ++t) {
+            if (dc[6 + t] == z) {
+                const double w = __dmul_rn(wxy, dw[6 + t]);
+                for (int c = 0; c < 3; ++c)
+                    F[c] = (double)(T)__dadd_rn(F[c], __dmul_rn(w, fv.flat[p * 3 + c]));
+            }
+        }
+    }
+    Fx = F[0];
+    Fy = F[1];
+    Fz = F[2];
+}
+
+// force of cell (x,y,z) given its row's key (ForceView)
+template <class T>
+__device__ __forceinline__ void force_from_key(const ForceView& fv, const Geom& g, uint64_t key,
+                                               int x, int y, int z, double& Fx, double& Fy,
+                                               double& Fz) {
+    Fx = Fy = Fz = 0.0;
+    const int32_t slot = (int32_t)(uint32_t)key;
+    if (fv.row_key == nullptr || (uint32_t)(key >> 32) != fv.tag || slot < 0) return;
+    if (fv.pool != nullptr) {
+        const T* p = static_cast<const T*>(fv.pool) + (int64_t)slot * 3 * g.zp + z;
+        Fx = (double)p[0];
+        Fy = (double)p[g.zp];
+        Fz = (double)p[2 * g.zp];
+    } else {
+        actuator_force<T>(fv, g.x0 + x, y, z, Fx, Fy, Fz);
+    }
+}
+
 template <class T>
 __device__ __forceinline__ void load_force(const ForceView& fv, const Geom& g, int x, int y, int z,
                                            double& Fx, double& Fy, double& Fz) {
-    Fx = Fy = Fz = 0.0;
-    if (fv.row_key != nullptr) {
-        const uint64_t key = fv.row_key[(int64_t)x * g.ny + y];
-        const int32_t slot = (int32_t)(uint32_t)key;
-        if ((uint32_t)(key >> 32) == fv.tag && slot >= 0) {
-            const T* p = static_cast<const T*>(fv.pool) + (int64_t)slot * 3 * g.zp + z;
-            Fx = (double)p[0];
-            Fy = (double)p[g.zp];
-            Fz = (double)p[2 * g.zp];
-        }
-    }
+    const uint64_t key = fv.row_key != nullptr ? fv.row_key[(int64_t)x * g.ny + y] : 0ull;
+    force_from_key<T>(fv, g, key, x, y, z, Fx, Fy, Fz);
 }
 
 // runtime storage dispatch for the non-hot paths (actuator sampling, output)
