@@ -94,6 +94,21 @@ def workload(name, n_gpus):
                          "reference_velocity": 1.0},
                "resolution": {"mach": 0.02}, "run": {"collision": {"operator": "cumulant"}}}
         return raw, f"C1 TGV {64 * n_gpus}x64x64 periodic cumulant fp64, no turbine"
+    if name == "c5":     # strong scaling, three aligned rotors, turbulent-like start
+        cells, cpd, nu = [2048, 512, 512], 64, 0.0866
+        raw = {"domain": {"cells": cells, "periodicity": [False, True, True]},
+               "fluid": {"kinematic_viscosity": nu, "wind": [8.0, 0.0, 0.0]},
+               "resolution": {"cells_per_diameter": cpd, "reference_diameter": 1.0,
+                              "mach": 0.05},
+               "run": {"boundary": "velocity_inflow_outflow",
+                       "collision": {"operator": "cumulant"}},
+               "turbines": [{"file": "rotor.yaml", "position": [x, 4.0, 3.2]}
+                            for x in (4.05, 11.05, 18.05)],
+               "polars": [{"id": "sym", "file": "sym.csv"}]}
+        desc = (f"C5 2048x512x512 cumulant fp64, inflow/outflow x, aligned row of 3 rotors "
+                f"at 4D/11D/18D ({9 * POINTS_PER_BLADE} points), turbulent-like initial field "
+                f"(32 seeded divergence-free Fourier modes, 5 % intensity)")
+        return raw, desc
     if name == "c4":     # strong scaling: the global domain is fixed
         cells, cpd, nu, pos = [1024, 512, 512], 64, 0.0866, [4.05, 4.0, 3.2]
     else:                # weak scaling: one slab of this size per GPU
@@ -205,6 +220,10 @@ def run_ours(args, rank, world, local_rank):
         sim = parallel.SlabSimulation(cfg, rank=rank, nranks=world, device=local_rank)
     else:
         sim = Simulation(cfg, device=local_rank)
+    if args.config == "c5":
+        from paper_2402_13171_b200.fields import fourier_modes
+        u0 = sim.boundary.u_in_lat
+        sim.fields[0].initialize_modes(1.0, u0, fourier_modes(cfg.cells, u0), product=True)
     cells_total = int(np.prod(cfg.cells))
     cells_local = int(np.prod(sim.fields[0].size))
     lib = _lib.load()
@@ -275,7 +294,8 @@ def run_ours(args, rank, world, local_rank):
             "value": round(value, 2), "unit": "MLUP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
             "higher_is_better": True,
-            "scaling": "strong" if args.config == "c4" else "weak", "vs_baseline": None,
+            "scaling": "strong" if args.config in ("c4", "c5") else "weak",
+            "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "cells": list(cfg.cells),
                        "cells_per_gpu": cells_local, "actuator_points": P,
@@ -301,7 +321,8 @@ def run_ours(args, rank, world, local_rank):
         }
     sim.close()
     tmp.cleanup()
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config != "c4":
+    if (rank == 0 and world == 1 and not args.no_cpu_baseline
+            and args.config not in ("c4", "c5")):
         out["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_budget)
     if dist is not None:
         dist.destroy_process_group()
@@ -418,15 +439,16 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", choices=("c1", "c2", "c3", "c4"), default="c2")
-    ap.add_argument("--points-per-blade", type=int, default=6)
+    ap.add_argument("--config", choices=("c1", "c2", "c3", "c4", "c5"), default="c2")
+    ap.add_argument("--points-per-blade", type=int, default=None,
+                    help="default 6 (demo rotor); 50 for c5 (paper-like blades)")
     ap.add_argument("--arithmetic", choices=("exact", "fast"), default="fast")
     ap.add_argument("--precision", choices=("double", "single"), default="double")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     global POINTS_PER_BLADE
-    POINTS_PER_BLADE = args.points_per_blade
+    POINTS_PER_BLADE = args.points_per_blade or (50 if args.config == "c5" else 6)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     rank = int(os.environ.get("RANK", "0"))

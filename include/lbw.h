@@ -152,6 +152,15 @@ int lbw_domain_download_pdf(lbw_domain* d, double* f_aos);
 int lbw_domain_fill_uniform(lbw_domain* d, const double* f27);
 /* Same, but on device buffers already laid out AoS (no host copies). */
 int lbw_domain_upload_pdf_device(lbw_domain* d, const double* f_aos_dev);
+/* Every owned cell at equilibrium of (rho, u(x)) computed on the device,
+ * u(x) = u0 + sum_m a_m sin(k_m . x + phi_m) with x the global cell centre
+ * (lattice units): a seeded "turbulent-like" initial field for domains too
+ * large for a host array (fields.py:54-67 semantics: the
+ * macro field becomes exactly (rho, u), the force is cleared).  modes:
+ * n_modes rows of 7 doubles (kx, ky, kz, ax, ay, az, phi), host memory.
+ * product: 1 = product equilibrium (cumulant), 0 = polynomial (BGK). */
+int lbw_domain_init_modes(lbw_domain* d, double rho, const double* u0, int32_t n_modes,
+                          const double* modes, int32_t product);
 
 /* Body force density, host AoS (slab_nx, ny, nz, 3), lattice units.
  * set: the force the next collide applies when no actuator points exist

@@ -140,6 +140,7 @@ SIGNATURES = {
     "lbw_domain_download_pdf": (_I, [_VP, _VP]),
     "lbw_domain_upload_pdf_device": (_I, [_VP, _VP]),
     "lbw_domain_fill_uniform": (_I, [_VP, _VP]),
+    "lbw_domain_init_modes": (_I, [_VP, _D, _VP, _I32, _VP, _I32]),
     "lbw_domain_set_force": (_I, [_VP, _VP]),
     "lbw_domain_download_force": (_I, [_VP, _VP]),
     "lbw_domain_set_macro": (_I, [_VP, _VP, _VP]),

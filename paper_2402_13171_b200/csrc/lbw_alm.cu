@@ -1166,7 +1166,8 @@ int alm_launch(lbw_domain* d, int64_t m) {
     for (int k = 0; k < 3; ++k) md.u_in[k] = d->desc.u_in[k];
     md.inflow = d->desc.boundary == LBW_BC_INFLOW_OUTFLOW ? 1 : 0;
     md.per_x = per_x;
-    const int threads = 128;
+    // one warp per CTA: fits in the registers a full sweep leaves free
+    const int threads = 32;
     const unsigned blocks = (unsigned)((s->n * 32 + threads - 1) / threads);
     CubeArgs cube{};
     if (d->linked) {

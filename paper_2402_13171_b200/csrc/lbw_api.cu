@@ -2,6 +2,7 @@
 // device-resident domain (one x-slab on one GPU).  See include/lbw.h.
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -248,6 +249,12 @@ int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out) {
 
     lbw_domain* d = new lbw_domain();
     d->desc = s;
+    {
+        // LBW_PRELAUNCH=0: queue each actuator chain only when its step runs
+        // (diagnostics: the serial chain + sweep time)
+        const char* e = getenv("LBW_PRELAUNCH");
+        d->prelaunch = !(e && e[0] == '0');
+    }
     d->device = s.device;
     if (cudaSetDevice(d->device) != cudaSuccess) {
         cudaGetLastError();
@@ -399,6 +406,42 @@ int lbw_domain_fill_uniform(lbw_domain* d, const double* f27) {
     LBW_CK(launch_fill_uniform(v, d->buf[d->cur], d->g, d->stream));
     LBW_CK(cudaStreamSynchronize(d->stream));
     d->state_pre = true;
+    return LBW_OK;
+}
+
+int lbw_domain_init_modes(lbw_domain* d, double rho, const double* u0, int32_t n_modes,
+                          const double* modes, int32_t product) {
+    LBW_REQ(d && u0, "null argument");
+    LBW_REQ(n_modes >= 0 && (n_modes == 0 || modes), "bad mode table");
+    LBW_REQ(rho > 0.0, "density must be positive");
+    LBW_CK(cudaSetDevice(d->device));
+    {
+        int rc_ = alm_invalidate(d);
+        if (rc_) return rc_;
+    }
+    int rc = freeze_macro_if(d, true, false);
+    if (rc) return rc;
+    if (!d->macro_dense) {
+        rc = alloc_dev(d, (void**)&d->macro_dense, interior_cells(d) * 4 * sizeof(double));
+        if (rc) return rc;
+    }
+    double* dmodes = nullptr;
+    const size_t mb = (size_t)(n_modes > 0 ? n_modes : 1) * 7 * sizeof(double);
+    LBW_CK(cudaMalloc(&dmodes, mb));
+    if (n_modes > 0)
+        LBW_CK(cudaMemcpyAsync(dmodes, modes, (size_t)n_modes * 7 * sizeof(double),
+                               cudaMemcpyHostToDevice, d->stream));
+    const double u[3] = {u0[0], u0[1], u0[2]};
+    const cudaError_t e = launch_init_modes(rho, u, n_modes, dmodes, product ? 1 : 0,
+                                            d->buf[d->cur], d->macro_dense, d->g, d->stream);
+    const cudaError_t e2 = cudaStreamSynchronize(d->stream);
+    cudaFree(dmodes);
+    LBW_CK(e);
+    LBW_CK(e2);
+    d->state_pre = true;
+    d->msrc.kind = MS_DENSE;
+    d->user_active = false;
+    d->shown_fv = ForceView{nullptr, nullptr, 0};
     return LBW_OK;
 }
 

@@ -107,6 +107,10 @@ cudaError_t launch_block_stream(const double* fsrc, double* fdst, int64_t nx, in
 cudaError_t launch_aos_to_soa(const double* aos, void* buf, const Geom& g, cudaStream_t s);
 cudaError_t launch_fill_uniform(const double (&f27)[27], void* buf, const Geom& g,
                                 cudaStream_t s);
+// equilibrium of (rho, u0 + sum of sine modes) in every owned cell, macro too
+cudaError_t launch_init_modes(double rho, const double (&u0)[3], int32_t n_modes,
+                              const double* modes_dev, int product, void* buf, double* macro,
+                              const Geom& g, cudaStream_t s);
 cudaError_t launch_gather_aos(bool pull, const void* buf, const Geom& g, double* aos,
                               cudaStream_t s);
 cudaError_t launch_moments_soa(bool pull, const void* buf, const Geom& g, ForceView fv,

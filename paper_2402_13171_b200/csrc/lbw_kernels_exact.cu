@@ -110,6 +110,47 @@ __global__ void k_fill_uniform(F27 f, T* __restrict__ buf, Geom g) {
     for (int i = 0; i < 27; ++i) st_pop(d + (int64_t)i * g.dir_stride, f.v[i]);
 }
 
+// collision.py:54-100 for one cell: polynomial w rho (1 + 3cu + 4.5cu^2 -
+// 1.5u.u) or product rho g(ux) g(uy) g(uz)
+template <class T>
+__global__ void k_init_modes(double rho, double ux0, double uy0, double uz0, int32_t n_modes,
+                             const double* __restrict__ modes, int product, T* __restrict__ buf,
+                             double* __restrict__ macro, Geom g) {
+    int x, y, z;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (!cell_of(g, t, x, y, z)) return;
+    const double X = (double)(g.x0 + x) + 0.5, Y = (double)y + 0.5, Z = (double)z + 0.5;
+    double u[3] = {ux0, uy0, uz0};
+    for (int m = 0; m < n_modes; ++m) {
+        const double* md = modes + (int64_t)m * 7;
+        const double sn = sin(md[0] * X + md[1] * Y + md[2] * Z + md[6]);
+        for (int c = 0; c < 3; ++c) u[c] += md[3 + c] * sn;
+    }
+    double f[27];
+    if (product) {
+        double gx[3][3];
+        for (int c = 0; c < 3; ++c) {
+            const double uu = u[c] * u[c];
+            gx[c][0] = 0.5 * (uu - u[c] + 1.0 / 3.0);
+            gx[c][1] = 1.0 - uu - 1.0 / 3.0;
+            gx[c][2] = 0.5 * (uu + u[c] + 1.0 / 3.0);
+        }
+        for (int i = 0; i < 27; ++i)
+            f[i] = rho * gx[0][cx_of(i) + 1] * gx[1][cy_of(i) + 1] * gx[2][cz_of(i) + 1];
+    } else {
+        const double usq = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+        for (int i = 0; i < 27; ++i) {
+            const double cu = cx_of(i) * u[0] + cy_of(i) * u[1] + cz_of(i) * u[2];
+            f[i] = w_of(i) * rho * (1.0 + 3.0 * cu + 4.5 * cu * cu - 1.5 * usq);
+        }
+    }
+    T* d = buf + buf_index(g, x + 1, 0, y, z);
+#pragma unroll
+    for (int i = 0; i < 27; ++i) st_pop(d + (int64_t)i * g.dir_stride, f[i]);
+    macro[t * 4] = rho;
+    for (int c = 0; c < 3; ++c) macro[t * 4 + 1 + c] = u[c];
+}
+
 template <bool PULL, class T>
 __global__ void k_gather_aos(const T* __restrict__ buf, Geom g, double* __restrict__ aos) {
     int x, y, z;
@@ -221,6 +262,20 @@ void moments_soa_t(bool pull, const T* buf, const Geom& g, ForceView fv, double 
                    cudaStream_t s) {
     if (pull) k_moments_soa<true><<<cells_blocks(g, 128), 128, 0, s>>>(buf, g, fv, dt, m);
     else k_moments_soa<false><<<cells_blocks(g, 128), 128, 0, s>>>(buf, g, fv, dt, m);
+}
+
+cudaError_t launch_init_modes(double rho, const double (&u0)[3], int32_t n_modes,
+                              const double* modes_dev, int product, void* buf, double* macro,
+                              const Geom& g, cudaStream_t s) {
+    const unsigned nb = cells_blocks(g, 128);
+    if (g.single)
+        k_init_modes<<<nb, 128, 0, s>>>(rho, u0[0], u0[1], u0[2], n_modes, modes_dev, product,
+                                        (float*)buf, macro, g);
+    else
+        k_init_modes<<<nb, 128, 0, s>>>(rho, u0[0], u0[1], u0[2], n_modes, modes_dev, product,
+                                        (double*)buf, macro, g);
+    count_launch();
+    return cudaGetLastError();
 }
 
 cudaError_t launch_gather_aos(bool pull, const void* buf, const Geom& g, double* aos,

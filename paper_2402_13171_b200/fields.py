@@ -43,6 +43,26 @@ def _write_through(arr, push):
     return out
 
 
+def fourier_modes(cells, u0, intensity=0.05, n_modes=32, seed=2402):
+    """(n_modes, 7) table (kx, ky, kz, ax, ay, az, phase) of a seeded
+    "turbulent-like" velocity perturbation for DeviceField.initialize_modes
+    (u = U e_x + du, du a random Fourier field at ~5 %
+    intensity).  Wavenumbers are whole periods of the domain (1..4 per
+    axis), amplitudes are perpendicular to k (divergence free) and scaled
+    so the rms of |du| is intensity * |u0|."""
+    rng = np.random.default_rng(seed)
+    L = np.asarray(cells, dtype=np.float64)
+    out = np.zeros((n_modes, 7))
+    for m in range(n_modes):
+        k = 2.0 * np.pi * rng.integers(1, 5, 3) * rng.choice([-1, 1], 3) / L
+        a = rng.normal(size=3)
+        a -= (a @ k) / (k @ k) * k
+        out[m, 0:3], out[m, 3:6], out[m, 6] = k, a, rng.uniform(0.0, 2.0 * np.pi)
+    rms = np.sqrt(0.5 * np.sum(out[:, 3:6] ** 2))
+    out[:, 3:6] *= intensity * np.linalg.norm(u0) / rms
+    return out
+
+
 class DeviceField:
     def __init__(self, sim, size, origin, block_id=0):
         self._sim = sim
@@ -133,6 +153,15 @@ class DeviceField:
     @interior_macro.setter
     def interior_macro(self, value):
         self.set_macro(value)
+
+    def initialize_modes(self, rho, u0, modes, product=False):
+        """initialize_equilibrium with u(x) = u0 + sum_m a_m sin(k_m.x + phi_m)
+        evaluated on the device (no lattice-sized host array; fourier_modes)."""
+        modes = np.ascontiguousarray(np.asarray(modes, dtype=np.float64).reshape(-1, 7))
+        u0 = np.ascontiguousarray(np.asarray(u0, dtype=np.float64).reshape(3))
+        _lib.check(_lib.load().lbw_domain_init_modes(self._d, float(rho), _lib.ptr(u0),
+                                                     modes.shape[0], _lib.ptr(modes),
+                                                     int(bool(product))), "init")
 
     def initialize_equilibrium(self, rho, u, product=False):
         """Interior populations at equilibrium of (rho, u); the sampled macro

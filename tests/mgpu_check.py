@@ -101,6 +101,10 @@ def main():
         ok &= run_case(f"rotor-{arith}-{kin}",
                        lambda: rotor_config(cells=(nx, 12, 12), position=(1.5, 0.3, 0.0),
                                             arithmetic=arith)[0], 10, False, kinematics=kin)
+    # 90 points: the many-point path (K5 fills per-row pools)
+    ok &= run_case("rotor-many-points",
+                   lambda: rotor_config(cells=(nx, 12, 12), position=(1.5, 0.3, 0.0),
+                                        arithmetic="fast", points_per_blade=30)[0], 8, False)
     dist.barrier()
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)

@@ -43,9 +43,9 @@ def sym_polar_csv():
     return "\n".join(rows) + "\n"
 
 
-def write_rotor_files(d):
+def write_rotor_files(d, points_per_blade=6):
     with open(os.path.join(d, "rotor.yaml"), "w") as fh:
-        fh.write(ROTOR_YAML)
+        fh.write(ROTOR_YAML.replace("points: 6", f"points: {points_per_blade}"))
     with open(os.path.join(d, "sym.csv"), "w") as fh:
         fh.write(sym_polar_csv())
 
@@ -63,11 +63,12 @@ def rotor_raw(cells, periodic, boundary="periodic", position=(0.9, 0.3, 0.0), st
 
 
 def rotor_config(cells=(12, 12, 12), periodic=(True, True, True), boundary="periodic",
-                 position=(0.9, 0.3, 0.0), steps=0, arithmetic="exact", **kw):
+                 position=(0.9, 0.3, 0.0), steps=0, arithmetic="exact", points_per_blade=6,
+                 **kw):
     """(RunConfig, TemporaryDirectory) for the golden-style rotor."""
     from paper_2402_13171_b200 import parse_config
     tmp = tempfile.TemporaryDirectory()
-    write_rotor_files(tmp.name)
+    write_rotor_files(tmp.name, points_per_blade)
     cfg = parse_config(rotor_raw(cells, periodic, boundary, position, steps, arithmetic, **kw),
                        base_dir=tmp.name)
     return cfg, tmp

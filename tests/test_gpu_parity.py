@@ -241,6 +241,58 @@ def test_rotor_vs_reference(gpu, golden, tag, kinematics):
     tmp.cleanup()
 
 
+@pytest.mark.parametrize("ppb", [6, 30])
+def test_rotor_vs_oracle_point_counts(gpu, ppb):
+    """18 points (forces summed inside the sweep) and 90 points (per-row
+    pools filled by K5) against the oracle over 6 steps."""
+    from paper_2402_13171_b200.sim import HostKinematics
+    cfg, tmp = rotor_config(cells=(16, 12, 12), periodic=(False, True, True),
+                            boundary="velocity_inflow_outflow", position=(0.9, 0.75, 0.0),
+                            points_per_blade=ppb)
+    sim = Simulation(cfg, kinematics="host")
+    cfg2, tmp2 = rotor_config(cells=(16, 12, 12), periodic=(False, True, True),
+                              boundary="velocity_inflow_outflow", position=(0.9, 0.75, 0.0),
+                              points_per_blade=ppb)
+    host = HostKinematics(cfg2)
+    ref = oracle_for(host)
+    for _ in range(6):
+        sim.step()
+        ref.step(host.refresh())
+        host.advance()
+        rho, u, blade = sim._alm_results()
+        np.testing.assert_allclose(rho, ref.samples[:, 0], rtol=1e-12)
+        np.testing.assert_allclose(blade, ref.blade, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(sim.fields[0].interior, ref.interior, rtol=0, atol=1e-14)
+    np.testing.assert_allclose(sim.fields[0].interior_force, ref.force[1:-1, 1:-1, 1:-1],
+                               rtol=1e-9, atol=1e-17)
+    sim.close()
+    tmp.cleanup()
+    tmp2.cleanup()
+
+
+def test_initialize_modes_matches_host_equilibrium(gpu):
+    """The device-side initial field (lbw_domain_init_modes) equals the host
+    initialize_equilibrium of the same u(x) to libm rounding."""
+    from paper_2402_13171_b200.collision import equilibrium_pdf, product_equilibrium
+    from paper_2402_13171_b200.fields import fourier_modes
+    for op in ("cumulant", "bgk"):
+        sim = _lbm_sim((12, 10, 8), op=op)
+        u0 = np.array([0.03, 0.0, 0.0])
+        modes = fourier_modes((12, 10, 8), u0, intensity=0.1, n_modes=8, seed=3)
+        sim.fields[0].initialize_modes(1.0, u0, modes, product=(op == "cumulant"))
+        X, Y, Z = np.meshgrid(np.arange(12) + 0.5, np.arange(10) + 0.5, np.arange(8) + 0.5,
+                              indexing="ij")
+        u = np.broadcast_to(u0, (12, 10, 8, 3)).copy()
+        for m in modes:
+            sn = np.sin(m[0] * X + m[1] * Y + m[2] * Z + m[6])
+            u += m[3:6] * sn[..., None]
+        want = (product_equilibrium if op == "cumulant" else equilibrium_pdf)(1.0, u)
+        np.testing.assert_allclose(sim.fields[0].interior, want, rtol=0, atol=1e-15)
+        np.testing.assert_allclose(sim.fields[0].interior_macro[..., 1:], u, rtol=0, atol=1e-16)
+        assert np.sqrt(np.mean(np.sum((u - u0) ** 2, axis=-1))) > 0.05 * 0.03
+        sim.close()
+
+
 def test_device_kinematics_long_run(gpu):
     """600 steps of device kinematics stay on the host (reference-identical)
     kinematics to 1e-12 m, and sync_topologies restores the host objects."""
