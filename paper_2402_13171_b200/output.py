@@ -139,7 +139,7 @@ def rotor_loads(sim, turbine=0):
         if hub is None:
             continue
         F = sim._alm_results()[2][sl]
-        arm = sim._pos_m[sl] - hub
+        arm = sim._kin_view()[sl, 15:18] - hub   # world positions (m), unwrapped
         thrust += float(np.sum(F @ axis))
         tq = float(np.sum(np.cross(arm, F) @ axis))
         torque += tq

@@ -116,5 +116,92 @@ class SlabSimulation(Simulation):
         _dist().all_gather_object(parts, mine, group=self._group)
         return np.concatenate(parts, axis=0) if self.rank == root else None
 
+    # ------------------------------------------------------------ output
+    def _probe_tick(self):
+        """Output tick of the whole lattice (output.py:33-167): the slabs'
+        macro (and force, for VTK) fields and the owners' actuator results
+        are gathered on rank 0, which writes the same files a single-GPU run
+        writes."""
+        from . import output
+        cfg = self.cfg
+        if not (cfg.probes or cfg.vtk):
+            return
+        if not self._macro_fresh:
+            self._recompute_moments()
+        macro = self.fields[0].download_macro()
+        force = self.fields[0].download_force() if cfg.vtk else None
+        results = self.alm_results_global() if self.points else None
+        parts = [None] * self.nranks
+        _dist().all_gather_object(parts, (macro, force), group=self._group)
+        if self.rank == 0:
+            gm = np.concatenate([p[0] for p in parts], axis=0)
+            gf = np.concatenate([p[1] for p in parts], axis=0) if cfg.vtk else None
+            output.probe_tick(_GlobalView(self, gm, gf, results))
+        _dist().barrier(group=self._group)
 
-__all__ = ["SlabGrid", "SlabSimulation", "first_nonfinite", "slab_neighbours"]
+    def _write_report(self, report):
+        if self.rank == 0:
+            super()._write_report(report)
+
+
+class _GlobalField:
+    def __init__(self, macro, force):
+        self._macro, self._force = macro, force
+
+    def download_macro(self):
+        return self._macro
+
+    def download_force(self):
+        return self._force
+
+
+class _GlobalPoint:
+    """An ActuatorPoint whose per-step outputs come from the gathered
+    (owner) results."""
+
+    def __init__(self, point, results):
+        self._p, self._r = point, results
+
+    def __getattr__(self, name):
+        return getattr(self._p, name)
+
+    blade_force = property(lambda s: s._r[2][s._p.global_id].copy())
+    fluid_force = property(lambda s: -s._r[2][s._p.global_id])
+    sampled_rho = property(lambda s: float(s._r[0][s._p.global_id]))
+    sampled_u = property(lambda s: s._r[1][s._p.global_id].copy())
+
+
+class _GlobalView:
+    """What output.probe_tick needs of a Simulation, for the whole lattice
+    on rank 0 (a single-block grid over the global extent)."""
+
+    def __init__(self, sim, macro, force, results):
+        cfg = sim.cfg
+        self.cfg, self.units, self.boundary = cfg, sim.units, sim.boundary
+        self.step_index = sim.step_index
+        self.grid = SlabGrid(cfg.cells, cfg.periodicity, 1, 0)
+        self.fields = [_GlobalField(macro, force)]
+        self._line_groups = sim._line_groups
+        self._avg = sim._avg
+        self._macro_fresh = True
+        self._kin_view = sim._kin_view
+        self.points = [_GlobalPoint(p, results) for p in sim.points] if results else []
+        self._alm_results = lambda: results
+
+
+def run_slab_simulation(cfg, group=None, kinematics=None):
+    """Simulation.run over all ranks of torch.distributed (one process per
+    GPU, device = LOCAL_RANK); rank 0 writes the probes, VTK and report."""
+    import os
+    dist = _dist()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    device = int(os.environ.get("LOCAL_RANK", rank))
+    sim = SlabSimulation(cfg, rank, world, device=device, group=group, kinematics=kinematics)
+    try:
+        return sim.run()
+    finally:
+        sim.close()
+
+
+__all__ = ["SlabGrid", "SlabSimulation", "first_nonfinite", "run_slab_simulation",
+           "slab_neighbours"]

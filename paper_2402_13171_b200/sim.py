@@ -513,10 +513,13 @@ class Simulation:
         if cfg.cadence == 0 and (cfg.probes or cfg.vtk):
             self._probe_tick()
         report = self.report()
-        os.makedirs(cfg.output_dir, exist_ok=True)
-        with open(os.path.join(cfg.output_dir, "report.json"), "w") as fh:
-            json.dump(report, fh, indent=2, sort_keys=True)
+        self._write_report(report)
         return report
+
+    def _write_report(self, report):
+        os.makedirs(self.cfg.output_dir, exist_ok=True)
+        with open(os.path.join(self.cfg.output_dir, "report.json"), "w") as fh:
+            json.dump(report, fh, indent=2, sort_keys=True)
 
     def report(self):
         cfg = self.cfg

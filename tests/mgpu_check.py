@@ -79,6 +79,52 @@ def run_case(name, make_cfg, steps, perturb, kinematics=None):
     return flag.item() == 0
 
 
+def output_case(world, nx):
+    """Probes (axial line, radial profile with running average, blade loads)
+    and VTK dumps of a run over N slabs are the same files as one GPU's."""
+    import filecmp
+    import tempfile
+    rank = dist.get_rank()
+    base = tempfile.mkdtemp() if rank == 0 else None
+    holder = [base]
+    dist.broadcast_object_list(holder, 0)
+    base = holder[0]
+
+    def cfg_for(out):
+        from tests.scenarios import rotor_raw, write_rotor_files
+        files = os.path.join(base, "files")
+        if rank == 0 or not os.path.exists(files):
+            os.makedirs(files, exist_ok=True)
+            write_rotor_files(files)
+        raw = rotor_raw((nx, 12, 12), (True, True, True), position=(1.5, 0.3, 0.0), steps=6,
+                        arithmetic="fast")
+        raw["output"] = {"directory": out, "cadence": 3, "vtk": True,
+                         "probes": [{"kind": "axial_line", "name": "ax", "samples": 7},
+                                    {"kind": "radial_profile", "name": "rp", "x_m": 1.4,
+                                     "samples": 5, "average_from_step": 3},
+                                    {"kind": "blade_loads", "name": "bl", "turbine": 0,
+                                     "component": "blade1"}]}
+        return parse_config(raw, base_dir=files)
+
+    from paper_2402_13171_b200.parallel import run_slab_simulation
+    multi = os.path.join(base, "multi")
+    run_slab_simulation(cfg_for(multi), kinematics="device")
+    ok = True
+    if rank == 0:
+        from paper_2402_13171_b200 import run_simulation
+        single = os.path.join(base, "single")
+        run_simulation(cfg_for(single))
+        names = sorted(f for f in os.listdir(single) if f != "report.json")
+        same = [filecmp.cmp(os.path.join(single, f), os.path.join(multi, f), shallow=False)
+                for f in names]
+        ok = len(names) > 6 and all(same) and os.path.exists(os.path.join(multi, "report.json"))
+        print(f"[output-files] world={world} {'OK' if ok else 'MISMATCH'} "
+              f"{sum(same)}/{len(names)} identical", flush=True)
+    flag = torch.tensor([0 if ok else 1])
+    dist.broadcast(flag, 0)
+    return flag.item() == 0
+
+
 def main():
     dist.init_process_group("gloo")
     rank = dist.get_rank()
@@ -105,6 +151,7 @@ def main():
     ok &= run_case("rotor-many-points",
                    lambda: rotor_config(cells=(nx, 12, 12), position=(1.5, 0.3, 0.0),
                                         arithmetic="fast", points_per_blade=30)[0], 8, False)
+    ok &= output_case(world, nx)
     dist.barrier()
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)

@@ -293,6 +293,41 @@ def test_initialize_modes_matches_host_equilibrium(gpu):
         sim.close()
 
 
+@pytest.mark.parametrize("kinematics", ["host", "device"])
+def test_rotor_loads_time_series_vs_reference(gpu, golden, kinematics):
+    """Thrust / torque / power series (output.rotor_loads) against the same
+    sums over the reference's own blade forces (golden rotor run) at the
+    reference's point positions (HostKinematics, bit-identical)."""
+    from paper_2402_13171_b200 import rotor_loads
+    from paper_2402_13171_b200.sim import HostKinematics
+    g = golden("rotor_inflow.npz")
+    args = dict(cells=tuple(int(c) for c in g["cells"]),
+                periodic=tuple(bool(p) for p in g["periodicity"]),
+                boundary=str(g["boundary"]), position=tuple(g["position"]))
+    cfg, tmp = rotor_config(**args)
+    cfg2, tmp2 = rotor_config(**args)
+    host = HostKinematics(cfg2)
+    sim = Simulation(cfg, kinematics=kinematics)
+    hub = next(c for c in cfg2.topologies[0].components if c.rate != 0.0)
+    for n in range(g["blade"].shape[0]):
+        sim.step()
+        sim.synchronize()
+        host.refresh()
+        pos_m = host._pos_m.copy()
+        hub_p, rate = hub.world.p.copy(), hub.rate
+        axis = np.array([1.0, 0.0, 0.0])
+        host.advance()
+        F = g["blade"][n]
+        thrust = np.sum(F @ axis)
+        torque = np.sum(np.cross(pos_m - hub_p, F) @ axis)
+        got = rotor_loads(sim)
+        np.testing.assert_allclose(got, (thrust, torque, torque * rate), rtol=1e-9, atol=1e-12)
+    assert abs(got[0]) > 0 and abs(got[2]) > 0
+    sim.close()
+    tmp.cleanup()
+    tmp2.cleanup()
+
+
 def test_device_kinematics_long_run(gpu):
     """600 steps of device kinematics stay on the host (reference-identical)
     kinematics to 1e-12 m, and sync_topologies restores the host objects."""
