@@ -69,7 +69,10 @@ struct AlmDev {
     const int32_t* ring_first;
     const int32_t* ring_count;
     const double* ring_ct;
-    int32_t* error_flags;  // bit 0: non-positive density, bit 1: point outside domain
+    int32_t* error_flags;  // bit 0: non-positive density, bit 1: point outside domain,
+                           // bit 2: an actuator disk spans more than three slabs
+    double* ring_samples;     // (P,4) disk samples for the ring averages
+    int32_t* ring_sample_ok;  // (P)
 };
 
 struct KinDev {
@@ -111,7 +114,9 @@ struct AlmState {
     double *samples = nullptr;   // (2,P,4)
     double *blade = nullptr;     // (2,P,3)
     double *flat = nullptr;      // (P,3)
-    double* cube = nullptr;      // (2,P,8,4) sampled cube values (multi-slab runs)
+    double* cube = nullptr;      // (2,P,8,4) sampled cube values + (2,P,8) tags (multi-slab)
+    double* ring_samples = nullptr;
+    int32_t* ring_sample_ok = nullptr;
     int32_t* dep_cell = nullptr;
     double* dep_w = nullptr;
     int32_t *clamp_flags = nullptr, *error_flags = nullptr;
@@ -179,6 +184,8 @@ struct AlmState {
         a.dep_cell = dep_cell + (size_t)parity * n * 9;
         a.dep_w = dep_w + (size_t)parity * n * 9;
         a.clamp_flags = clamp_flags;
+        a.ring_samples = ring_samples;
+        a.ring_sample_ok = ring_sample_ok;
         a.error_flags = error_flags;
         a.point_ring = point_ring;
         a.area = area;
@@ -828,6 +835,11 @@ constexpr int kOnTheFlyMaxPoints = 64;
 struct CubeArgs {
     double* local;   // (P,8,4) of this step's parity
     double* peer[2];
+    // per cube cell: epoch of the launch that wrote it (same allocation,
+    // after the values), so a reader knows which cells are this step's
+    int32_t* tag_local;  // (P,8)
+    int32_t* tag_peer[2];
+    int32_t epoch;
 };
 
 __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, const ForceSet& s,
@@ -855,23 +867,31 @@ __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, co
         t[k] = kin[k] - 0.5 - fl;
     }
     double v[4] = {0.0, 0.0, 0.0, 0.0};
+    bool have = true;  // this lane's cube cell is this step's value
     if (phase == 2) {
-        if (lane < 8)
+        if (lane < 8) {
             for (int q = 0; q < 4; ++q) v[q] = cube.local[((int64_t)p * 8 + lane) * 4 + q];
+            have = cube.tag_local[(int64_t)p * 8 + lane] == cube.epoch;
+        }
     } else if (lane < 8) {
         const int code = macro_at(g, m, j0[0] + ((lane >> 2) & 1), j0[1] + ((lane >> 1) & 1),
                                   j0[2] + (lane & 1), v);
         if (phase == 1) {
             const int64_t o = ((int64_t)p * 8 + lane) * 4;
-            if (code != MA_REMOTE)
+            if (code != MA_REMOTE) {
                 for (int q = 0; q < 4; ++q) cube.local[o + q] = v[q];
+                cube.tag_local[(int64_t)p * 8 + lane] = cube.epoch;
+            }
             if (code == MA_OWNED)
                 for (int side = 0; side < 2; ++side)
-                    if (cube.peer[side])
+                    if (cube.peer[side]) {
                         for (int q = 0; q < 4; ++q) cube.peer[side][o + q] = v[q];
+                        cube.tag_peer[side][(int64_t)p * 8 + lane] = cube.epoch;
+                    }
         }
     }
     if (phase == 1) return;
+    const bool complete = __all_sync(0xffffffffu, have);
     // lane 0: trilinear sum in (dx,dy,dz) lexicographic order (actuator.py:88-92)
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int c = 0; c < 8; ++c) {
@@ -911,6 +931,11 @@ __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, co
             a.blade[p * 3 + c] = owner ? blade[c] : 0.0;
             a.flat[p * 3 + c] = -blade[c] * a.dt2 / a.den;  // units.py:69
         }
+        if (disk) {
+            // ring averages need every sample of the ring, owned or not
+            for (int q = 0; q < 4; ++q) a.ring_samples[p * 4 + q] = acc[q];
+            a.ring_sample_ok[p] = complete ? 1 : 0;
+        }
     }
 }
 
@@ -923,9 +948,43 @@ __global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s, int phase
 // K4d: actuator-disk rings (actuator.py:149-183), one thread per ring, fixed
 // summation order.  Fluid force per sample = direction * thrust/area_ring *
 // area_i * axis; the blade force is its negation (sim.py:236-244).
-__device__ void disk_ring(const AlmDev& a, int r) {
+// Slab-local view of a disk point (multi-slab): its Roma support reaches
+// this slab / floor(x) lies in it.
+__device__ bool point_relevant(const Geom& g, int per_x, double x) {
+    const int64_t n0 = (int64_t)floor(x);
+    for (int dxc = -1; dxc <= 1; ++dxc) {
+        int64_t c = n0 + dxc;
+        if (per_x) c = (c % g.nxg + g.nxg) % g.nxg;
+        if (c - g.x0 >= 0 && c - g.x0 < g.nxl) return true;
+    }
+    return false;
+}
+
+__device__ void disk_ring(const AlmDev& a, const Geom& g, int per_x, int linked, int r) {
     const int first = a.ring_first[r], cnt = a.ring_count[r];
     const double ct = a.ring_ct[r];
+    if (linked) {
+        // across slabs: the ring's samples must all be known here (owned by
+        // this slab or a neighbour) if any of its forces land here
+        bool all_ok = true, needed = false;
+        for (int i = 0; i < cnt; ++i) {
+            const int p = first + i;
+            all_ok &= a.ring_sample_ok[p] != 0;
+            needed |= point_relevant(g, per_x, a.kin[(int64_t)p * kKin]);
+        }
+        if (!needed) {
+            for (int i = 0; i < cnt; ++i)
+                for (int c = 0; c < 3; ++c) {
+                    a.blade[(first + i) * 3 + c] = 0.0;
+                    a.flat[(first + i) * 3 + c] = 0.0;
+                }
+            return;
+        }
+        if (!all_ok) {
+            atomicOr(a.error_flags, 4);
+            return;
+        }
+    }
     const double* k0 = a.kin + (int64_t)first * kKin;
     double axis[3] = {k0[6], k0[7], k0[8]};
     const double nrm = sqrt(dot3(axis, axis));
@@ -937,10 +996,10 @@ __device__ void disk_ring(const AlmDev& a, int r) {
         const int p = first + i;
         const double ar = a.area[p];
         double up[3];
-        for (int c = 0; c < 3; ++c) up[c] = a.samples[p * 4 + 1 + c] * a.vscale;
+        for (int c = 0; c < 3; ++c) up[c] = a.ring_samples[p * 4 + 1 + c] * a.vscale;
         ring_area += ar;
         su += dot3(up, axis) * ar;
-        srho += a.samples[p * 4] * a.rho_ref * ar;
+        srho += a.ring_samples[p * 4] * a.rho_ref * ar;
     }
     const double u_d = su / ring_area;
     const double rho = srho / ring_area;
@@ -950,17 +1009,19 @@ __device__ void disk_ring(const AlmDev& a, int r) {
     const double per_area = thrust / ring_area;
     for (int i = 0; i < cnt; ++i) {
         const int p = first + i;
+        const int64_t ox = (int64_t)floor(a.kin[(int64_t)p * kKin]) - g.x0;
+        const bool owner = !linked || (ox >= 0 && ox < g.nxl);
         for (int c = 0; c < 3; ++c) {
             const double f = direction * per_area * a.area[p] * axis[c];
-            a.blade[p * 3 + c] = -f;
+            a.blade[p * 3 + c] = owner ? -f : 0.0;
             a.flat[p * 3 + c] = f * a.dt2 / a.den;
         }
     }
 }
 
-__global__ void k_alm_disks(AlmDev a) {
+__global__ void k_alm_disks(AlmDev a, Geom g, int per_x, int linked) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < a.n_rings) disk_ring(a, r);
+    if (r < a.n_rings) disk_ring(a, g, per_x, linked, r);
 }
 
 // K5: one warp per deposit pair q.  The lowest pair touching a row owns it:
@@ -1172,9 +1233,17 @@ int alm_launch(lbw_domain* d, int64_t m) {
     CubeArgs cube{};
     if (d->linked) {
         const size_t off = (size_t)par * s->n * 32;
+        const size_t tags = (size_t)2 * s->n * 32;   // tags follow the values
+        const size_t toff = (size_t)par * s->n * 8;
         cube.local = s->cube + off;
-        for (int side = 0; side < 2; ++side)
+        cube.tag_local = reinterpret_cast<int32_t*>(s->cube + tags) + toff;
+        for (int side = 0; side < 2; ++side) {
             cube.peer[side] = d->nb_cube[side] ? d->nb_cube[side] + off : nullptr;
+            cube.tag_peer[side] = d->nb_cube[side]
+                                      ? reinterpret_cast<int32_t*>(d->nb_cube[side] + tags) + toff
+                                      : nullptr;
+        }
+        cube.epoch = (int32_t)(d->alm_launches + 1);
         k_alm_points<<<blocks, threads, 0, st>>>(a, g, md, fs, 1, cube);
         count_launch();
         LBW_CK(cudaGetLastError());
@@ -1188,7 +1257,8 @@ int alm_launch(lbw_domain* d, int64_t m) {
     }
     d->alm_launches += 1;
     if (s->n_rings > 0) {
-        k_alm_disks<<<(unsigned)((s->n_rings + 63) / 64), 64, 0, st>>>(a);
+        k_alm_disks<<<(unsigned)((s->n_rings + 63) / 64), 64, 0, st>>>(a, g, per_x,
+                                                                       d->linked ? 1 : 0);
         count_launch();
     }
     if (!s->on_the_fly) {
@@ -1269,7 +1339,9 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     A(&s->samples, (size_t)2 * P * 4);
     A(&s->blade, (size_t)2 * P * 3);
     A(&s->flat, (size_t)2 * P * 3);
-    A(&s->cube, (size_t)2 * P * 32);
+    A(&s->cube, (size_t)2 * P * 32 + (size_t)2 * P * 4);   // values, then (2,P,8) int32 tags
+    A(&s->ring_samples, (size_t)P * 4);
+    A(&s->ring_sample_ok, P);
     A(&s->dep_cell, (size_t)2 * P * 9);
     A(&s->dep_w, (size_t)2 * P * 9);
     A(&s->clamp_flags, std::max(1, desc->n_polars));
@@ -1338,6 +1410,7 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
         }
         if (cudaMemset(s->clamp_flags, 0, std::max(1, desc->n_polars) * 4) != cudaSuccess ||
             cudaMemset(s->error_flags, 0, 4) != cudaSuccess ||
+            cudaMemset(s->cube, 0, ((size_t)2 * P * 32 + (size_t)2 * P * 4) * 8) != cudaSuccess ||
             cudaMemset(s->samples, 0, (size_t)2 * P * 32) != cudaSuccess ||
             cudaMemset(s->blade, 0, (size_t)2 * P * 24) != cudaSuccess ||
             cudaMemset(s->kin, 0, (size_t)3 * P * kKin * 8) != cudaSuccess ||
@@ -1572,6 +1645,11 @@ int lbw_alm_get(lbw_domain* d, double* rho, double* u, double* blade_force) {
     }
     if (err & 2) {
         set_error("actuator point outside the non-periodic domain");
+        return LBW_EINVAL;
+    }
+    if (err & 4) {
+        set_error("an actuator disk spans more than three x-slabs (its ring averages need "
+                  "samples from beyond the neighbouring slabs)");
         return LBW_EINVAL;
     }
     if (err & 1) {

@@ -57,10 +57,6 @@ class SlabSimulation(Simulation):
     def __init__(self, cfg, rank, nranks, device=None, group=None, kinematics=None):
         super().__init__(cfg, rank=rank, nranks=nranks, device=device, kinematics=kinematics)
         self.rank, self.nranks, self._group = int(rank), int(nranks), group
-        if self._disk_groups and self.nranks > 1:
-            self.close()
-            raise ConfigError("actuator disks run on a single GPU in this build "
-                              "(ring averages are not exchanged between slabs)")
         self._pending_abort = None
         self._link()
 

@@ -34,6 +34,33 @@ def lbm_raw(cells, periodic, boundary, op, arithmetic):
                     "collision": {"operator": op, "higher_order_rates": [1.1, 0.9, 1.3, 1.0]}}}
 
 
+DISK = """
+name: d
+components:
+  - name: mast
+    position: [2.9, 2.0, 2.0]
+    orientation: {axis: [0.0, 0.0, 1.0], angle_deg: YAW}
+  - name: rotor
+    parent: mast
+    discretization: {type: disk, radius: 1.0, rings: 2, sectors: 6,
+                     thrust_coefficient: [0.5, 0.3]}
+"""
+
+
+def disk_cfg(nx, yaw):
+    import tempfile
+    d = tempfile.mkdtemp()
+    with open(os.path.join(d, "d.yaml"), "w") as fh:
+        fh.write(DISK.replace("YAW", repr(yaw)))
+    return parse_config({"domain": {"cells": [nx, 16, 16], "periodicity": [False, True, True]},
+                         "fluid": {"kinematic_viscosity": 5.0, "wind": [8.0, 0.0, 0.0]},
+                         "resolution": {"cells_per_diameter": 8, "reference_diameter": 2.0,
+                                        "mach": 0.1},
+                         "run": {"boundary": "velocity_inflow_outflow", "arithmetic": "fast",
+                                 "collision": {"operator": "cumulant"}},
+                         "turbines": [{"file": "d.yaml"}]}, base_dir=d)
+
+
 def run_case(name, make_cfg, steps, perturb, kinematics=None):
     rank, world = dist.get_rank(), dist.get_world_size()
     cfg = make_cfg()
@@ -151,6 +178,10 @@ def main():
     ok &= run_case("rotor-many-points",
                    lambda: rotor_config(cells=(nx, 12, 12), position=(1.5, 0.3, 0.0),
                                         arithmetic="fast", points_per_blade=30)[0], 8, False)
+    # actuator disks: an aligned disk on the slab face and a yawed one whose
+    # rings spread over neighbouring slabs (ring averages across GPUs)
+    for name, yaw in (("disk-aligned", 0.0), ("disk-yawed", 35.0)):
+        ok &= run_case(name, lambda yaw=yaw: disk_cfg(nx, yaw), 8, False)
     ok &= output_case(world, nx)
     dist.barrier()
     dist.destroy_process_group()
