@@ -189,3 +189,90 @@ class DeviceField:
             m[..., 0] = rho_arr
             m[..., 1:4] = u_arr
             self.set_macro(m)
+
+
+class PdfField:
+    """Host block storage of the reference (fields.py:22-67): f, f_next,
+    force, macro as (nx+2, ny+2, nz+2, ncomp) arrays with a ghost ring.  Its
+    collide / stream (collide_field, stream below) run the sm_100a block
+    kernels through liblbw; the device-resident time step (Simulation) does
+    not use this class."""
+
+    def __init__(self, size, dtype=np.float64, origin=(0, 0, 0), block_id=0):
+        nx, ny, nz = (int(s) for s in size)
+        if min(nx, ny, nz) < 1:
+            raise ValueError("block size must be positive")
+        self.size = (nx, ny, nz)
+        self.dtype = np.dtype(dtype)
+        self.origin = tuple(int(o) for o in origin)
+        self.block_id = int(block_id)
+        shape = (nx + 2, ny + 2, nz + 2)
+        self.f = np.zeros(shape + (27,), self.dtype)
+        self.f_next = np.zeros(shape + (27,), self.dtype)
+        self.force = np.zeros(shape + (3,), self.dtype)
+        self.macro = np.zeros(shape + (4,), self.dtype)
+        self.macro[..., 0] = 1.0
+
+    @property
+    def interior(self):
+        return self.f[1:-1, 1:-1, 1:-1, :]
+
+    @property
+    def interior_macro(self):
+        return self.macro[1:-1, 1:-1, 1:-1, :]
+
+    @property
+    def interior_force(self):
+        return self.force[1:-1, 1:-1, 1:-1, :]
+
+    def cell_count(self):
+        nx, ny, nz = self.size
+        return nx * ny * nz
+
+    def initialize_equilibrium(self, rho, u, product=False):
+        n = self.size
+        rho_arr = np.broadcast_to(np.asarray(rho, np.float64), n)
+        u_arr = np.broadcast_to(np.asarray(u, np.float64), n + (3,))
+        eq = product_equilibrium(rho_arr, u_arr) if product else equilibrium_pdf(rho_arr, u_arr)
+        self.interior[...] = eq
+        self.interior_macro[..., 0] = rho_arr
+        self.interior_macro[..., 1:4] = u_arr
+        self.force[...] = 0.0
+
+
+def _as64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def collide_field(field, cfg, dt=1.0):
+    """Collide every interior cell of a PdfField in place and refresh its
+    macro (fields.py:70-83) with the block kernels of liblbw.  float32 fields
+    are widened exactly and rounded back on store, as the reference's
+    kernels do (_kernels.py:5-7)."""
+    from . import kernels
+    cfg.validate()
+    f, force, macro = _as64(field.f), _as64(field.force), _as64(field.macro)
+    if cfg.operator == "bgk":
+        kernels.collide_bgk_block(f, force, macro, float(cfg.omega), float(dt))
+    else:
+        w3, w4, w5, w6 = (float(r) for r in cfg.higher_order_rates)
+        kernels.collide_cumulant_block(f, force, macro, float(cfg.omega), w3, w4, w5, w6,
+                                       float(dt))
+    if f is not field.f:
+        field.f[...] = f
+    if macro is not field.macro:
+        field.macro[...] = macro
+    return field
+
+
+def stream(field):
+    """Pull streaming into f_next and swap (fields.py:86-94); the ghost ring
+    of f must be filled."""
+    from . import kernels
+    src = _as64(field.f)
+    dst = _as64(field.f_next)
+    kernels.stream_pull_block(src, dst)
+    if dst is not field.f_next:
+        field.f_next[...] = dst
+    field.f, field.f_next = field.f_next, field.f
+    return field

@@ -429,3 +429,30 @@ def test_kernels_are_native(gpu):
     sim.close()
     assert _lib.kernel_launches() > before
 
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_pdffield_collide_and_stream(gpu, dtype):
+    """The reference's block-level API (fields.py PdfField / collide_field /
+    stream) on the GPU block kernels, float64 and float32 storage, against
+    the oracle."""
+    from paper_2402_13171_b200 import PdfField, collide_field, stream
+    rng = np.random.default_rng(7)
+    fld = PdfField((6, 5, 7), dtype=dtype)
+    f = (orc.W * (1.0 + 0.3 * rng.uniform(-1, 1, fld.f.shape))).astype(dtype)
+    F = rng.uniform(-1e-3, 1e-3, fld.force.shape).astype(dtype)
+    fld.f[...] = f
+    fld.force[...] = F
+    cfg = CollisionConfig("cumulant", 1.6, (1.0, 1.2, 0.9, 1.1))
+    collide_field(fld, cfg)
+    ref_f = f.astype(np.float64)
+    ref_m = np.zeros(fld.macro.shape)
+    orc.collide_block("cumulant", ref_f, F.astype(np.float64), ref_m, 1.6, (1.0, 1.2, 0.9, 1.1))
+    inner = (slice(1, -1),) * 3
+    assert fld.f.dtype == dtype
+    assert np.array_equal(fld.f[inner], ref_f[inner].astype(dtype))
+    assert np.array_equal(fld.macro[inner], ref_m[inner].astype(dtype))
+    stream(fld)
+    dst = np.zeros_like(ref_f)
+    orc.stream_pull_block(fld.f_next.astype(np.float64), dst)
+    assert np.array_equal(fld.f[inner], dst[inner].astype(dtype))
