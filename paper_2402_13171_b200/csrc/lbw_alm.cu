@@ -71,6 +71,7 @@ struct AlmDev {
     const double* ring_ct;
     int32_t* error_flags;  // bit 0: non-positive density, bit 1: point outside domain,
                            // bit 2: an actuator disk spans more than three slabs
+    int64_t step;             // the step this view serves (diagnostics)
     double* ring_samples;     // (P,4) disk samples for the ring averages
     int32_t* ring_sample_ok;  // (P)
 };
@@ -184,6 +185,7 @@ struct AlmState {
         a.dep_cell = dep_cell + (size_t)parity * n * 9;
         a.dep_w = dep_w + (size_t)parity * n * 9;
         a.clamp_flags = clamp_flags;
+        a.step = m;
         a.ring_samples = ring_samples;
         a.ring_sample_ok = ring_sample_ok;
         a.error_flags = error_flags;
@@ -572,7 +574,9 @@ __device__ void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g, 
 
 __global__ void k_kinematics(KinDev k, AlmDev a, Geom g, int per_x, int advance) {
     extern __shared__ double ksm[];
+    LBW_TRACE_BEGIN(1, a.step);
     kinematics_cta(k, a, g, per_x, advance, ksm);
+    LBW_TRACE_END(1, a.step);
 }
 
 // Macro (rho, u) of global cell (gx,gy,gz), following the ghost semantics
@@ -940,9 +944,33 @@ __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, co
 }
 
 __global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s, int phase, CubeArgs cube) {
+    extern __shared__ double alm_sm[];
     const int p = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    LBW_TRACE_BEGIN(2, a.step);
+    // The sampled cells lie in the rows the previous step's points forced:
+    // their force is summed from that step's deposit data (actuator view),
+    // which is staged in shared memory first -- one parallel load instead
+    // of a dependent global load per point inside every cube cell.
+    const ForceView& fv = m.fv;
+    if (fv.row_key != nullptr && fv.pool == nullptr && fv.npts > 0 && fv.npts <= kOnTheFlyMaxPoints &&
+        phase != 2) {
+        const int n = fv.npts;
+        double* w = alm_sm;                                   // (n, 9)
+        double* fl = w + n * 9;                               // (n, 3)
+        int32_t* dc = reinterpret_cast<int32_t*>(fl + n * 3); // (n, 9)
+        for (int i = threadIdx.x; i < n * 9; i += blockDim.x) {
+            w[i] = fv.dep_w[i];
+            dc[i] = fv.dep_cell[i];
+        }
+        for (int i = threadIdx.x; i < n * 3; i += blockDim.x) fl[i] = fv.flat[i];
+        __syncthreads();
+        m.fv.dep_w = w;
+        m.fv.flat = fl;
+        m.fv.dep_cell = dc;
+    }
     if (p >= a.n) return;  // uniform per warp
     point_warp(a, g, m, s, phase, cube, p, threadIdx.x & 31);
+    LBW_TRACE_END(2, a.step);
 }
 
 // K4d: actuator-disk rings (actuator.py:149-183), one thread per ring, fixed
@@ -1021,7 +1049,9 @@ __device__ void disk_ring(const AlmDev& a, const Geom& g, int per_x, int linked,
 
 __global__ void k_alm_disks(AlmDev a, Geom g, int per_x, int linked) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    LBW_TRACE_BEGIN(3, a.step);
     if (r < a.n_rings) disk_ring(a, g, per_x, linked, r);
+    LBW_TRACE_END(3, a.step);
 }
 
 // K5: one warp per deposit pair q.  The lowest pair touching a row owns it:
@@ -1032,6 +1062,7 @@ __global__ void k_alm_disks(AlmDev a, Geom g, int per_x, int linked) {
 constexpr int kFillSmemPairs = 4096;
 __global__ void k_alm_fill(AlmDev a, Geom g, ForceSet s) {
     __shared__ int32_t rows_sm[kFillSmemPairs];
+    LBW_TRACE_BEGIN(4, a.step);
     const int npairs = a.n * 9;
     const bool staged = npairs <= kFillSmemPairs;
     if (staged)
@@ -1106,6 +1137,7 @@ __global__ void k_alm_fill(AlmDev a, Geom g, ForceSet s) {
         }
     }
     if (lane == 0) s.row_key[row] = row_key_of(s.tag, q);
+    LBW_TRACE_END(4, a.step);
 }
 
 template <class T>
@@ -1229,6 +1261,10 @@ int alm_launch(lbw_domain* d, int64_t m) {
     md.per_x = per_x;
     // one warp per CTA: fits in the registers a full sweep leaves free
     const int threads = 32;
+    const size_t pts_smem =
+        (md.fv.row_key != nullptr && md.fv.pool == nullptr && md.fv.npts <= kOnTheFlyMaxPoints)
+            ? (size_t)md.fv.npts * (12 * sizeof(double) + 9 * sizeof(int32_t))
+            : 0;
     const unsigned blocks = (unsigned)((s->n * 32 + threads - 1) / threads);
     CubeArgs cube{};
     if (d->linked) {
@@ -1244,16 +1280,16 @@ int alm_launch(lbw_domain* d, int64_t m) {
                                       : nullptr;
         }
         cube.epoch = (int32_t)(d->alm_launches + 1);
-        k_alm_points<<<blocks, threads, 0, st>>>(a, g, md, fs, 1, cube);
+        k_alm_points<<<blocks, threads, pts_smem, st>>>(a, g, md, fs, 1, cube);
         count_launch();
         LBW_CK(cudaGetLastError());
         const uint32_t epoch = (uint32_t)(d->alm_launches + 1);
         int rc = peer_signal(d, st, 1, epoch);
         if (!rc) rc = peer_wait(d, st, 1, epoch);
         if (rc) return rc;
-        k_alm_points<<<blocks, threads, 0, st>>>(a, g, md, fs, 2, cube);
+        k_alm_points<<<blocks, threads, pts_smem, st>>>(a, g, md, fs, 2, cube);
     } else {
-        k_alm_points<<<blocks, threads, 0, st>>>(a, g, md, fs, 0, cube);
+        k_alm_points<<<blocks, threads, pts_smem, st>>>(a, g, md, fs, 0, cube);
     }
     d->alm_launches += 1;
     if (s->n_rings > 0) {
@@ -1670,3 +1706,5 @@ int lbw_alm_clamp_flags(lbw_domain* d, int32_t* per_polar) {
 }
 
 }  // extern "C"
+
+LBW_TRACE_EXPORT(alm)

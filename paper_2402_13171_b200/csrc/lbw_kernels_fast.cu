@@ -54,3 +54,5 @@ cudaError_t launch_block_collide_fast(int op, double* f, const double* force, do
 }
 
 }  // namespace lbw
+
+LBW_TRACE_EXPORT(fast)

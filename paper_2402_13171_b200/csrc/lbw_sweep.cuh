@@ -4,6 +4,7 @@
 // contracting compiler (-fmad=false is a per-TU flag).
 #pragma once
 #include "lbw_internal.h"
+#include "lbw_trace.cuh"
 
 #ifndef LBW_FAST
 #error "define LBW_FAST before including lbw_sweep.cuh"
@@ -330,8 +331,10 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) k_sweep(SweepArgs a) {
     const int bz = (int)blockIdx.z;
     const int x = a.x_begin + (bz == 0 ? 0 : (bz == 1 ? g.nxl - 1 : bz - 1));
     const bool edge = bz < 2 && a.halo.edge_counter != nullptr;
+    LBW_TRACE_BEGIN(0, a.step);
     if (z < g.nz && y < g.ny) sweep_cell<OP, PULL, T>(a, x, y, z);
     if (edge) edge_done(a.halo);  // whole CTA, uniform branch
+    LBW_TRACE_END(0, a.step);
 }
 
 // K0: batch collide of (n,27) rows (_kernels.py:400-427)
