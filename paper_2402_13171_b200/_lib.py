@@ -159,6 +159,8 @@ SIGNATURES = {
     "lbw_alm_kinematics_step": (_I64, [_VP]),
     "lbw_alm_set_kinematics": (_I, [_VP, _VP]),
     "lbw_alm_get": (_I, [_VP, _VP, _VP, _VP]),
+    "lbw_alm_record_loads": (_I, [_VP, _I64]),
+    "lbw_alm_read_loads": (_I, [_VP, _VP, _I64, _VP, _VP]),
     "lbw_alm_clamp_flags": (_I, [_VP, _c_i32_p]),
     "lbw_peer_blob_bytes": (_I64, []),
     "lbw_domain_export_handle": (_I, [_VP, _VP, _c_i64_p]),

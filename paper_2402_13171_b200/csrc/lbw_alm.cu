@@ -140,6 +140,9 @@ struct AlmState {
     cudaEvent_t ev_kin_done = nullptr;
     cudaEvent_t ev_chain_done[2] = {nullptr, nullptr};  // chain of a step parity done
     int64_t kin_valid[3] = {-1, -1, -1};  // step whose kinematics kin[slot] holds
+    // per-step blade-force series (lbw_alm_record_loads)
+    double* h_loads = nullptr;   // pinned (loads_cap, P, 3)
+    int64_t loads_cap = 0, loads_from = 0;
     // device kinematics
     bool kin_device = false;
     int32_t nc = 0;
@@ -1170,6 +1173,7 @@ void alm_destroy(lbw_domain* d) {
         if (e) cudaEventDestroy(e);
     if (s->kin_stream) cudaStreamDestroy(s->kin_stream);
     if (s->h_ring) cudaFreeHost(s->h_ring);
+    if (s->h_loads) cudaFreeHost(s->h_loads);
     delete s;
     d->alm = nullptr;
 }
@@ -1193,6 +1197,7 @@ ForceView alm_force_view(const lbw_domain* d, int64_t m) {
 }
 
 int alm_invalidate(lbw_domain* d) {
+    d->touched = true;
     if (!alm_active(d)) return LBW_OK;
     LBW_CK(cudaStreamSynchronize(d->alm_stream));
     if (d->alm->kin_stream) LBW_CK(cudaStreamSynchronize(d->alm->kin_stream));
@@ -1304,6 +1309,9 @@ int alm_launch(lbw_domain* d, int64_t m) {
     count_launch();
     LBW_CK(cudaGetLastError());
     LBW_CK(cudaEventRecord(d->ev_alm_done, st));
+    if (s->loads_cap > 0)
+        LBW_CK(cudaMemcpyAsync(s->h_loads + (size_t)(m % s->loads_cap) * s->n * 3, a.blade,
+                               (size_t)s->n * 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
     if (s->kin_device) {
         LBW_CK(cudaEventRecord(s->ev_chain_done[par], st));
         // prefetch the next step's kinematics while this chain and sweep run
@@ -1327,6 +1335,7 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     LBW_REQ(desc->n_points >= 0 && desc->n_points <= 16384, "n_points outside [0, 16384]");
     LBW_REQ(desc->n_polars >= 0, "n_polars must be >= 0");
     LBW_CK(cudaSetDevice(d->device));
+    d->touched = true;
     LBW_CK(cudaStreamSynchronize(d->stream));
     LBW_CK(cudaStreamSynchronize(d->alm_stream));
     alm_destroy(d);
@@ -1692,6 +1701,49 @@ int lbw_alm_get(lbw_domain* d, double* rho, double* u, double* blade_force) {
         set_error("density must be positive at an actuator point");
         return LBW_EINVAL;
     }
+    return LBW_OK;
+}
+
+int lbw_alm_record_loads(lbw_domain* d, int64_t capacity) {
+    LBW_REQ(d && capacity >= 0, "bad argument");
+    LBW_REQ(alm_active(d), "no actuator points configured");
+    AlmState* s = d->alm;
+    LBW_CK(cudaSetDevice(d->device));
+    LBW_CK(cudaStreamSynchronize(d->alm_stream));
+    if (s->h_loads) cudaFreeHost(s->h_loads);
+    s->h_loads = nullptr;
+    s->loads_cap = 0;
+    if (capacity > 0) {
+        LBW_REQ(capacity >= 2, "capacity must be >= 2");
+        LBW_CK(cudaMallocHost(&s->h_loads, (size_t)capacity * s->n * 3 * sizeof(double)));
+        s->loads_cap = capacity;
+    }
+    s->loads_from = d->step;
+    // a chain already queued for the next step has not recorded its loads
+    s->ready_step = -1;
+    return LBW_OK;
+}
+
+int lbw_alm_read_loads(lbw_domain* d, double* out, int64_t max_steps, int64_t* first_step,
+                       int64_t* n) {
+    LBW_REQ(d && out && first_step && n && max_steps >= 0, "null argument");
+    LBW_REQ(alm_active(d) && d->alm->loads_cap > 0, "load recording is not enabled");
+    AlmState* s = d->alm;
+    LBW_CK(cudaSetDevice(d->device));
+    const int64_t avail = d->step - s->loads_from;
+    LBW_REQ(avail < s->loads_cap || avail == 0,
+            "load ring overflow: read the loads at least every capacity-1 steps");
+    LBW_CK(cudaStreamSynchronize(d->alm_stream));
+    const int64_t k = std::min(avail, max_steps);
+    const size_t row = (size_t)s->n * 3;
+    for (int64_t i = 0; i < k; ++i) {
+        const int64_t st = s->loads_from + i;
+        std::memcpy(out + (size_t)i * row, s->h_loads + (size_t)(st % s->loads_cap) * row,
+                    row * sizeof(double));
+    }
+    *first_step = s->loads_from;
+    *n = k;
+    s->loads_from += k;
     return LBW_OK;
 }
 

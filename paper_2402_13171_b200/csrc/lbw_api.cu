@@ -1,5 +1,6 @@
 // lbw_api.cu — C ABI of liblbw.so: host-array kernel entry points and the
 // device-resident domain (one x-slab on one GPU).  See include/lbw.h.
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -206,7 +207,8 @@ static void free_domain(lbw_domain* d) {
     if (d->stage) cudaFree(d->stage);
     for (cudaEvent_t ev : d->ev_pool) cudaEventDestroy(ev);
     peer_close(d);
-    for (cudaEvent_t ev : {d->ev_main, d->ev_ready, d->ev_alm_done, d->ev_sweep[0], d->ev_sweep[1]})
+    for (cudaEvent_t ev : {d->ev_main, d->ev_ready, d->ev_ready_prev, d->ev_alm_done,
+                           d->ev_sweep[0], d->ev_sweep[1]})
         if (ev) cudaEventDestroy(ev);
     if (d->alm_stream) cudaStreamDestroy(d->alm_stream);
     if (d->stream) cudaStreamDestroy(d->stream);
@@ -307,6 +309,7 @@ int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out) {
         }() != cudaSuccess ||
         cudaEventCreateWithFlags(&d->ev_main, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&d->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&d->ev_ready_prev, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&d->ev_alm_done, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&d->ev_sweep[0], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&d->ev_sweep[1], cudaEventDisableTiming) != cudaSuccess) {
@@ -611,14 +614,22 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
             int rc = peer_wait(d, d->stream, 0, (uint32_t)d->steps_done);
             if (rc) return rc;
         }
+        std::swap(d->ev_ready, d->ev_ready_prev);
         LBW_CK(cudaEventRecord(d->ev_ready, d->stream));
         if (alm_active(d)) {
             // The actuator chain of this step normally was queued on the
-            // actuator stream while the previous sweep ran; otherwise queue
-            // it now behind everything already on the main stream.
+            // actuator stream while the previous sweep ran.  Otherwise (host
+            // kinematics, first step) queue it now: it needs the sweep two
+            // steps back (ev_ready_prev: its sampled state and force set)
+            // unless a call changed state since the last step, in which case
+            // it waits for everything already on the main stream.
             if (!alm_ready(d, d->step)) {
-                LBW_CK(cudaEventRecord(d->ev_main, d->stream));
-                LBW_CK(cudaStreamWaitEvent(d->alm_stream, d->ev_main, 0));
+                if (d->touched) {
+                    LBW_CK(cudaEventRecord(d->ev_main, d->stream));
+                    LBW_CK(cudaStreamWaitEvent(d->alm_stream, d->ev_main, 0));
+                } else {
+                    LBW_CK(cudaStreamWaitEvent(d->alm_stream, d->ev_ready_prev, 0));
+                }
                 int rc = alm_launch(d, d->step);
                 if (rc) return rc;
             }
@@ -669,6 +680,7 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
         d->last_fv = fv;
         d->shown_fv = fv;
         LBW_CK(cudaEventRecord(d->ev_sweep[d->step & 1], d->stream));
+        d->touched = false;
         d->cur = 1 - d->cur;
         d->state_pre = false;
         d->step += 1;

@@ -86,6 +86,8 @@ struct lbw_domain {
     int64_t steps_done = 0;   // sweeps executed in this domain's lifetime
     bool prelaunch = true;
     cudaEvent_t ev_ready = nullptr;   // main stream passed the neighbour waits of a step
+    cudaEvent_t ev_ready_prev = nullptr;  // ... of the step before
+    bool touched = true;              // state changed by a call since the last step
     // x-slab neighbours (lbw_peer.cu): side 0 = lo (x-1), side 1 = hi (x+1)
     bool linked = false;
     int nb_rank[2] = {-1, -1};

@@ -475,6 +475,28 @@ class Simulation:
         self.step_index += n
         self._macro_fresh = False
 
+    def record_loads(self, capacity=4096):
+        """Start recording every step's blade forces (the thrust / power time
+        series) device->host without synchronising the step loop."""
+        if self.points:
+            _lib.check(_lib.load().lbw_alm_record_loads(self._domain, int(capacity)), "loads")
+        self._loads_cap = int(capacity)
+
+    def read_loads(self):
+        """(first_step, blade forces (n, P, 3)) of the steps executed since
+        the last read (record_loads must be on)."""
+        P = len(self.points)
+        n_max = max(1, getattr(self, "_loads_cap", 0))
+        out = np.empty((n_max, P, 3))
+        first = _lib.ctypes.c_int64()
+        n = _lib.ctypes.c_int64()
+        if not P:
+            return self.step_index, out[:0]
+        _lib.check(_lib.load().lbw_alm_read_loads(self._domain, _lib.ptr(out), n_max,
+                                                  _lib.ctypes.byref(first),
+                                                  _lib.ctypes.byref(n)), "loads")
+        return int(first.value), out[:n.value]
+
     def synchronize(self):
         _lib.check(_lib.load().lbw_domain_sync(self._domain), "sync")
         self._poll(wait=True)
