@@ -183,6 +183,13 @@ def main():
     for name, yaw in (("disk-aligned", 0.0), ("disk-yawed", 35.0)):
         ok &= run_case(name, lambda yaw=yaw: disk_cfg(nx, yaw), 8, False)
     ok &= output_case(world, nx)
+    if os.environ.get("LBW_MGPU_LONG"):
+        # test_acceptance.py test_04 at its size: 64^3 periodic, one rotating
+        # 3-blade turbine, 200 steps (slabs of 64/world planes)
+        ok &= run_case("test04-64cubed-200steps",
+                       lambda: rotor_config(cells=(64, 64, 64), position=(1.0, 1.0, 0.2),
+                                            nu=0.1732, cpd=None, mach=0.05,
+                                            arithmetic="exact")[0], 200, False)
     dist.barrier()
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)

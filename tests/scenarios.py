@@ -53,9 +53,11 @@ def write_rotor_files(d, points_per_blade=6):
 def rotor_raw(cells, periodic, boundary="periodic", position=(0.9, 0.3, 0.0), steps=0,
               arithmetic="exact", nu=0.866, cpd=8, mach=0.1, operator="cumulant",
               precision="double"):
+    res = {"mach": mach} if cpd is None else {"cells_per_diameter": cpd,
+                                                "reference_diameter": 1.0, "mach": mach}
     return {"domain": {"cells": list(cells), "periodicity": list(periodic)},
             "fluid": {"kinematic_viscosity": nu, "wind": [8.0, 0.0, 0.0]},
-            "resolution": {"cells_per_diameter": cpd, "reference_diameter": 1.0, "mach": mach},
+            "resolution": res,
             "run": {"steps": steps, "boundary": boundary, "arithmetic": arithmetic,
                     "precision": precision, "collision": {"operator": operator}},
             "turbines": [{"file": "rotor.yaml", "position": list(position)}],
