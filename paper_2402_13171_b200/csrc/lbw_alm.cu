@@ -849,22 +849,42 @@ struct CubeArgs {
     int32_t epoch;
 };
 
+// Flow-independent per-point inputs, loaded by the kernel before anything
+// that waits (kinematics row one value per lane, polar / chord data).
+struct PointInputs {
+    double kv;
+    PointStatic ps;
+    bool disk;
+};
+__device__ __forceinline__ PointInputs load_point_inputs(const AlmDev& a, int p, int lane) {
+    PointInputs in;
+    in.kv = lane < 15 ? a.kin[(int64_t)p * kKin + lane] : 0.0;
+    in.ps = load_static(a, p, lane);
+    in.disk = a.point_ring != nullptr && a.point_ring[p] >= 0;
+    return in;
+}
+
 __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, const ForceSet& s,
-                           int phase, const CubeArgs& cube, int p, int lane) {
-    // flow-independent loads first: kinematics row (one value per lane),
-    // polar / chord data; deposit cells need only the position
-    const double kv = lane < 15 ? a.kin[(int64_t)p * kKin + lane] : 0.0;
-    const PointStatic ps = load_static(a, p, lane);
-    const bool disk = a.point_ring != nullptr && a.point_ring[p] >= 0;
+                           int phase, const CubeArgs& cube, int p, int lane,
+                           const PointInputs& in) {
+    const PointStatic& ps = in.ps;
+    const bool disk = in.disk;
     double kr[15];
-    for (int k = 0; k < 15; ++k) kr[k] = __shfl_sync(0xffffffffu, kv, k);
+    for (int k = 0; k < 15; ++k) kr[k] = __shfl_sync(0xffffffffu, in.kv, k);
     const double* kin = kr;
+    // deposit cells / Roma weights per axis (lanes 8..10), kept in registers
+    // for the row tags below and stored for the sweep / fill / next sample
+    int32_t dcl[3] = {-1, -1, -1};
     if (phase != 1 && lane >= 8 && lane <= 10) {
         const int k = lane - 8;
         const int64_t L = k == 0 ? g.nxg : (k == 1 ? g.ny : g.nz);
         const int per = k == 0 ? m.per_x : (k == 1 ? g.per_y : g.per_z);
-        deposit_axis(kin[k], L, per, a.dep_cell + (int64_t)p * 9 + 3 * k,
-                     a.dep_w + (int64_t)p * 9 + 3 * k);
+        double dwl[3];
+        deposit_axis(kin[k], L, per, dcl, dwl);
+        for (int q = 0; q < 3; ++q) {
+            a.dep_cell[(int64_t)p * 9 + 3 * k + q] = dcl[q];
+            a.dep_w[(int64_t)p * 9 + 3 * k + q] = dwl[q];
+        }
     }
     int64_t j0[3];
     double t[3];
@@ -911,11 +931,18 @@ __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, co
         for (int q = 0; q < 4; ++q) acc[q] += w * vc[q];
     }
     if (s.flag_rows && phase != 1) {
-        // tag this step's rows (benign race: equal values)
-        __syncwarp();
+        // tag this step's rows (benign race: equal values); the x / y cells
+        // come from lanes 8 / 9 by shuffle, not back from memory
+        int32_t cx[3], cy[3];
+        for (int q = 0; q < 3; ++q) {
+            cx[q] = __shfl_sync(0xffffffffu, dcl[q], 8);
+            cy[q] = __shfl_sync(0xffffffffu, dcl[q], 9);
+        }
         if (lane < 9) {
-            const int32_t row = pair_row(a, g, p * 9 + lane);
-            if (row >= 0) s.row_key[row] = row_key_of(s.tag, 0);
+            const int32_t cxg = cx[lane / 3], cyy = cy[lane % 3];
+            const int64_t x = (int64_t)cxg - g.x0;
+            if (cxg >= 0 && cyy >= 0 && x >= 0 && x < g.nxl)
+                s.row_key[x * g.ny + cyy] = row_key_of(s.tag, 0);
         }
     }
     // Multi-slab: only points whose Roma support reaches this slab (their
@@ -954,6 +981,11 @@ __global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s, int phase
     // their force is summed from that step's deposit data (actuator view),
     // which is staged in shared memory first -- one parallel load instead
     // of a dependent global load per point inside every cube cell.
+    // flow-independent loads of this warp's point are issued first, so their
+    // latency overlaps the staging below
+    const int lane = threadIdx.x & 31;
+    PointInputs in{};
+    if (p < a.n) in = load_point_inputs(a, p, lane);
     const ForceView& fv = m.fv;
     if (fv.row_key != nullptr && fv.pool == nullptr && fv.npts > 0 && fv.npts <= kOnTheFlyMaxPoints &&
         phase != 2) {
@@ -972,7 +1004,7 @@ __global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s, int phase
         m.fv.dep_cell = dc;
     }
     if (p >= a.n) return;  // uniform per warp
-    point_warp(a, g, m, s, phase, cube, p, threadIdx.x & 31);
+    point_warp(a, g, m, s, phase, cube, p, lane, in);
     LBW_TRACE_END(2, a.step);
 }
 
@@ -1338,6 +1370,10 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     LBW_REQ(desc->n_polars >= 0, "n_polars must be >= 0");
     LBW_CK(cudaSetDevice(d->device));
     d->touched = true;
+    if (desc->n_points > 0) {
+        int rc_ = green_partition(d, alm_sm_count());
+        if (rc_) return rc_;
+    }
     LBW_CK(cudaStreamSynchronize(d->stream));
     LBW_CK(cudaStreamSynchronize(d->alm_stream));
     alm_destroy(d);
@@ -1591,7 +1627,9 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
     if (!s->kin_stream) {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        if (cudaStreamCreateWithPriority(&s->kin_stream, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        s->kin_stream = green_alm_stream(d);   // on the chain's SMs when partitioned
+        if ((!s->kin_stream &&
+             cudaStreamCreateWithPriority(&s->kin_stream, cudaStreamNonBlocking, hi) != cudaSuccess) ||
             cudaEventCreateWithFlags(&s->ev_kin_done, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&s->ev_chain_done[0], cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&s->ev_chain_done[1], cudaEventDisableTiming) != cudaSuccess) {

@@ -210,6 +210,7 @@ static void free_domain(lbw_domain* d) {
     for (cudaEvent_t ev : {d->ev_main, d->ev_ready, d->ev_ready_prev, d->ev_alm_done,
                            d->ev_sweep[0], d->ev_sweep[1]})
         if (ev) cudaEventDestroy(ev);
+    green_release(d);
     if (d->alm_stream) cudaStreamDestroy(d->alm_stream);
     if (d->stream) cudaStreamDestroy(d->stream);
     delete d;

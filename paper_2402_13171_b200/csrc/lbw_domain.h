@@ -82,6 +82,11 @@ struct lbw_domain {
     // actuator work runs on its own stream so the next step's sampling /
     // forces / spreading overlap the current sweep (see lbw_domain_step)
     cudaStream_t alm_stream = nullptr;
+    // optional SM partition (lbw_green.cu): green contexts of the sweep /
+    // actuator-chain streams (CUgreenCtx), SMs given to the chain
+    void* green_sweep = nullptr;
+    void* green_alm = nullptr;
+    int alm_sms = 0;
     cudaEvent_t ev_main = nullptr, ev_alm_done = nullptr, ev_sweep[2] = {nullptr, nullptr};
     int64_t steps_done = 0;   // sweeps executed in this domain's lifetime
     bool prelaunch = true;
@@ -132,4 +137,10 @@ int peer_wait(lbw_domain* d, cudaStream_t s, int which, uint32_t value);    // w
 int peer_signal(lbw_domain* d, cudaStream_t s, int which, uint32_t value);
 void peer_close(lbw_domain* d);
 int ensure_stage(lbw_domain* d, size_t bytes);
+
+// lbw_green.cu: SM partition between the sweep and the actuator chain
+int alm_sm_count();
+int green_partition(lbw_domain* d, int alm_sms);
+cudaStream_t green_alm_stream(lbw_domain* d);   // nullptr without a partition
+void green_release(lbw_domain* d);
 }  // namespace lbw

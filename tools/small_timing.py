@@ -26,7 +26,7 @@ def make(turbine, arithmetic, n=64):
 
 
 N = 400
-for n in (64, 128):
+for n in ([int(a) for a in sys.argv[1:]] or (64, 128)):
     for arith in ("exact", "fast"):
         for turb in (False, True):
             sim = make(turb, arith, n)
