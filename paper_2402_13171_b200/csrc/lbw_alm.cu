@@ -941,6 +941,7 @@ __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, co
         if (lane < 9) {
             const int32_t cxg = cx[lane / 3], cyy = cy[lane % 3];
             const int64_t x = (int64_t)cxg - g.x0;
+            LBW_CHECK(cyy < g.ny);
             if (cxg >= 0 && cyy >= 0 && x >= 0 && x < g.nxl)
                 s.row_key[x * g.ny + cyy] = row_key_of(s.tag, 0);
         }
@@ -1117,6 +1118,7 @@ __global__ void k_alm_fill(AlmDev a, Geom g, ForceSet s) {
     if (dup) return;
     const int64_t xg = row / g.ny + g.x0;
     const int32_t y = row % g.ny;
+    LBW_CHECK(q >= 0 && q < npairs && row >= 0 && row < (int64_t)g.nxl * g.ny);
     const int64_t row0 = (int64_t)q * 3 * g.zp;
     for (int z0 = 0; z0 < g.nz; z0 += 32) {
         const int z = z0 + lane;

@@ -29,7 +29,25 @@ struct Geom {
     double feq_in[27];         // already rounded to the storage type
 };
 
+// LBW_BOUNDS builds (EXTRA=-DLBW_BOUNDS) trap on any out-of-range index of
+// the population buffers, force rows and actuator arrays: the bounds-checked
+// library the GPU tests can run against (LBW_LIB) in place of a sanitizer.
+#ifdef LBW_BOUNDS
+#define LBW_CHECK(cond)          \
+    do {                         \
+        if (!(cond)) __trap();   \
+    } while (0)
+#else
+#define LBW_CHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 __host__ __device__ inline int64_t buf_index(const Geom& g, int p, int i, int y, int z) {
+#if defined(LBW_BOUNDS) && defined(__CUDA_ARCH__)
+    LBW_CHECK(p >= 0 && p < g.nxl + 2 && i >= 0 && i < 27 && y >= 0 && y < g.ny && z >= 0 &&
+              z < g.zp);
+#endif
     return (int64_t)p * g.plane_stride + (int64_t)i * g.dir_stride + (int64_t)y * g.zp + z;
 }
 

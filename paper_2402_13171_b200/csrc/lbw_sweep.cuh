@@ -160,6 +160,7 @@ __device__ __forceinline__ void load_cell_simple(const T* __restrict__ src, cons
         x_source(g, x, c, off, kind);
         px[c + 1] = src + off;
     }
+    LBW_CHECK(x >= 0 && x < g.nxl && y >= 0 && y < g.ny && z >= 0 && z < g.nz);
     const int ym = (y + 1 < g.ny ? y + 1 : y + 1 - g.ny) * g.zp;  // cy = -1: y+1
     const int y0 = y * g.zp;
     const int yp = (y > 0 ? y - 1 : y - 1 + g.ny) * g.zp;        // cy = +1: y-1
@@ -214,6 +215,7 @@ __device__ __forceinline__ void force_from_key(const ForceView& fv, const Geom& 
     Fx = Fy = Fz = 0.0;
     const int32_t slot = (int32_t)(uint32_t)key;
     if (fv.row_key == nullptr || (uint32_t)(key >> 32) != fv.tag || slot < 0) return;
+    LBW_CHECK(x >= 0 && x < g.nxl && y >= 0 && y < g.ny && z >= 0 && z < g.nz);
     if (fv.pool != nullptr) {
         const T* p = static_cast<const T*>(fv.pool) + (int64_t)slot * 3 * g.zp + z;
         Fx = (double)p[0];
@@ -227,6 +229,7 @@ __device__ __forceinline__ void force_from_key(const ForceView& fv, const Geom& 
 template <class T>
 __device__ __forceinline__ void load_force(const ForceView& fv, const Geom& g, int x, int y, int z,
                                            double& Fx, double& Fy, double& Fz) {
+    LBW_CHECK(x >= 0 && x < g.nxl && y >= 0 && y < g.ny);
     const uint64_t key = fv.row_key != nullptr ? fv.row_key[(int64_t)x * g.ny + y] : 0ull;
     force_from_key<T>(fv, g, key, x, y, z, Fx, Fy, Fz);
 }
