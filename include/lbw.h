@@ -64,6 +64,12 @@ extern "C" {
 #define LBW_PREC_DOUBLE 0
 #define LBW_PREC_SINGLE 1
 
+/* walls on non-periodic y / z faces (an extension: the reference leaves
+ * those ghosts unwritten, i.e. LBW_WALL_NONE) */
+#define LBW_WALL_NONE 0      /* zero ghost populations (the reference's semantics) */
+#define LBW_WALL_NO_SLIP 1   /* halfway bounce-back                               */
+#define LBW_WALL_FREE_SLIP 2 /* specular reflection                               */
+
 /* outer boundary along x (halo.py:122-141, BoundarySpec.KINDS) */
 #define LBW_BC_PERIODIC 0
 #define LBW_BC_INFLOW_OUTFLOW 1
@@ -130,8 +136,9 @@ typedef struct lbw_domain_desc {
     int32_t feq_in_given;    /* 1: use feq_in below for the inflow ghost     */
     double feq_in[27];       /* equilibrium_pdf(1, u_in) as the host computed it */
     int32_t precision;       /* LBW_PREC_* (host arrays stay fp64 either way)  */
+    int32_t walls[4];        /* LBW_WALL_* of the y_lo, y_hi, z_lo, z_hi faces   */
     int32_t reserved32;
-    int64_t reserved[7];
+    int64_t reserved[5];
 } lbw_domain_desc;
 
 int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out);

@@ -57,6 +57,7 @@ def lib():
         L.orc_moments_block.argtypes = [vp, vp, vp, i64, i64, i64, d]
         L.orc_stream_pull_block.argtypes = [vp, vp, i64, i64, i64]
         L.orc_fill_ghosts.argtypes = [vp, i64, i64, i64, ctypes.c_int, vp]
+        L.orc_apply_walls.argtypes = [vp, i64, i64, i64, vp, vp]
         L.orc_apply_inflow_outflow.argtypes = [vp, i64, i64, i64, vp]
         for fn in (L.orc_collide_batch, L.orc_collide_block, L.orc_moments_block,
                    L.orc_stream_pull_block, L.orc_fill_ghosts, L.orc_apply_inflow_outflow):
@@ -303,9 +304,11 @@ class OracleSim:
 
     def __init__(self, cells, periodic=(True, True, True), op="cumulant", omega=1.0,
                  rates=(1.0, 1.0, 1.0, 1.0), boundary="periodic", u_in=(0.0, 0.0, 0.0),
-                 points=None, dtype=np.float64):
+                 points=None, dtype=np.float64, walls=(0, 0, 0, 0)):
         self.dims = tuple(int(c) for c in cells)
         self.rnd = round_f32 if np.dtype(dtype) == np.float32 else _identity
+        # y_lo, y_hi, z_lo, z_hi: 0 none, 1 no-slip, 2 free-slip (extension)
+        self.walls = np.ascontiguousarray(walls, dtype=np.int32)
         nx, ny, nz = self.dims
         shape = (nx + 2, ny + 2, nz + 2)
         self.periodic = tuple(bool(p) for p in periodic)
@@ -386,6 +389,11 @@ class OracleSim:
             self.force[0] = 0.0
             self.macro[-1] = self.macro[-2]
             self.force[-1] = self.force[-2]
+        if self.walls.any():
+            per = np.ascontiguousarray([int(p) for p in self.periodic], dtype=np.int32)
+            nx, ny, nz = self.dims
+            lib().orc_apply_walls(_p(self.f), nx, ny, nz, ctypes.c_void_p(self.walls.ctypes.data),
+                                  ctypes.c_void_p(per.ctypes.data))
         stream_pull_block(self.f, self.f_next)
         self.f, self.f_next = self.f_next, self.f
         self.step_index += 1

@@ -20,6 +20,7 @@ LIB_PATH = os.environ.get("LBW_LIB") or os.path.join(
 ABI_VERSION = 2
 LBW_PREC_DOUBLE = 0
 LBW_PREC_SINGLE = 1
+WALL_KINDS = {"none": 0, "no_slip": 1, "free_slip": 2}
 
 LBW_OK = 0
 LBW_EINVAL = -1
@@ -59,8 +60,9 @@ class DomainDesc(ctypes.Structure):
         ("feq_in_given", ctypes.c_int32),
         ("feq_in", ctypes.c_double * 27),
         ("precision", ctypes.c_int32),
+        ("walls", ctypes.c_int32 * 4),
         ("reserved32", ctypes.c_int32),
-        ("reserved", ctypes.c_int64 * 7),
+        ("reserved", ctypes.c_int64 * 5),
     ]
 
 

@@ -246,6 +246,11 @@ int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out) {
     LBW_REQ(s.nranks >= 1 && s.rank >= 0 && s.rank < s.nranks, "bad rank/nranks");
     LBW_REQ(s.precision == LBW_PREC_DOUBLE || s.precision == LBW_PREC_SINGLE,
             "unknown storage precision");
+    for (int k = 0; k < 4; ++k) {
+        LBW_REQ(s.walls[k] >= LBW_WALL_NONE && s.walls[k] <= LBW_WALL_FREE_SLIP, "unknown wall kind");
+        LBW_REQ(s.walls[k] == LBW_WALL_NONE || !s.periodic[1 + k / 2],
+                "walls need a non-periodic axis");
+    }
     const int ndev = lbw_device_count();
     LBW_REQ(ndev > 0, "no CUDA device visible");
     LBW_REQ(s.device >= 0 && s.device < ndev, "device ordinal out of range");
@@ -270,6 +275,7 @@ int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out) {
     g.ny = (int32_t)s.cells[1];
     g.nz = (int32_t)s.cells[2];
     g.single = s.precision == LBW_PREC_SINGLE ? 1 : 0;
+    for (int k = 0; k < 4; ++k) g.walls[k] = s.walls[k];
     const int row_elems = g.single ? 32 : 16;   // 128-byte aligned z rows
     g.zp = (g.nz + row_elems - 1) / row_elems * row_elems;
     if (g.nz < row_elems) g.zp = g.nz;

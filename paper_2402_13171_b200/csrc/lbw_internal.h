@@ -26,6 +26,7 @@ struct Geom {
     int32_t per_y, per_z;
     int32_t lo_src, hi_src;    // XSource for x-1 at x=0 and x+1 at x=nxl-1
     int32_t single;            // populations / force stored fp32 (LBW_PREC_SINGLE)
+    int32_t walls[4];          // LBW_WALL_* of the y_lo, y_hi, z_lo, z_hi faces
     double feq_in[27];         // already rounded to the storage type
 };
 

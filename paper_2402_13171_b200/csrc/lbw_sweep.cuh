@@ -46,6 +46,7 @@ struct PullSrc {
     int32_t yoff[3];  // ys*zp for cy = -1, 0, +1
     int32_t zs[3];
     bool yok[3], zok[3];
+    int8_t ywall[3], zwall[3];  // LBW_WALL_* of the face a failing source crosses
 };
 
 __device__ __forceinline__ void x_source(const Geom& g, int x, int cx, int64_t& off, int32_t& kind) {
@@ -72,12 +73,14 @@ __device__ __forceinline__ void make_pull(const Geom& g, int x, int y, int z, Pu
         else if (ys >= g.ny) { if (g.per_y) ys -= g.ny; else yok = false; }
         s.yoff[c + 1] = yok ? ys * g.zp : 0;
         s.yok[c + 1] = yok;
+        s.ywall[c + 1] = yok ? 0 : (int8_t)g.walls[ys < 0 ? 0 : 1];
         int zs = z - c;
         bool zok = true;
         if (zs < 0) { if (g.per_z) zs += g.nz; else zok = false; }
         else if (zs >= g.nz) { if (g.per_z) zs -= g.nz; else zok = false; }
         s.zs[c + 1] = zok ? zs : 0;
         s.zok[c + 1] = zok;
+        s.zwall[c + 1] = zok ? 0 : (int8_t)g.walls[zs < 0 ? 2 : 3];
     }
 }
 
@@ -113,6 +116,28 @@ __device__ __forceinline__ double stored(double v) {
     return (double)(T)v;
 }
 
+// Population i of cell (x,y,z) whose pull source lies beyond a y / z wall
+// (the walls are halfway between the boundary cells and the ghosts):
+// no-slip -> halfway bounce-back, f_i = f*_opp(i) of the cell itself;
+// free-slip on every crossed face -> specular reflection, f_i = f*_i' of
+// the cell (x - cx, y or y - cy, z or z - cz) with the crossed components
+// of c_i negated.  Any no-slip face crossed wins at an edge.
+template <class T>
+__device__ __forceinline__ double wall_pull(const T* __restrict__ src, const Geom& g,
+                                            const PullSrc& s, int x, int y, int z, int i, int a,
+                                            int b, int c) {
+    const bool yo = !s.yok[b], zo = !s.zok[c];
+    if ((yo && s.ywall[b] == 1) || (zo && s.zwall[c] == 1))
+        return ld_pop(src + buf_index(g, x + 1, 26 - i, y, z));
+    const int cx = a - 1, cy = b - 1, cz = c - 1;
+    const int ip = (cx + 1) * 9 + ((yo ? -cy : cy) + 1) * 3 + ((zo ? -cz : cz) + 1);
+    if (s.xkind[a] == 1) return g.feq_in[ip];
+    if (s.xkind[a] == 2) return 0.0;
+    const int ys = yo ? y : (int)(s.yoff[b] / g.zp);
+    const int zsrc = zo ? z : s.zs[c];
+    return ld_pop(src + s.xoff[a] + (int64_t)ip * g.dir_stride + (int64_t)ys * g.zp + zsrc);
+}
+
 template <bool PULL, class T>
 __device__ __forceinline__ void load_cell(const T* __restrict__ src, const Geom& g, int x, int y,
                                           int z, double (&f)[27]) {
@@ -126,9 +151,14 @@ __device__ __forceinline__ void load_cell(const T* __restrict__ src, const Geom&
 #pragma unroll
         for (int i = 0; i < 27; ++i) {
             const int a = cx_of(i) + 1, b = cy_of(i) + 1, c = cz_of(i) + 1;
-            if (s.xkind[a] == 1) {
+            const bool out = !s.yok[b] || !s.zok[c];
+            const bool wall = out && !(!s.yok[b] && s.ywall[b] == 0) &&
+                              !(!s.zok[c] && s.zwall[c] == 0);
+            if (wall) {
+                f[i] = wall_pull(src, g, s, x, y, z, i, a, b, c);
+            } else if (s.xkind[a] == 1) {
                 f[i] = g.feq_in[i];
-            } else if (s.xkind[a] == 2 || !s.yok[b] || !s.zok[c]) {
+            } else if (s.xkind[a] == 2 || out) {
                 f[i] = 0.0;
             } else {
                 f[i] = ld_pop(src + s.xoff[a] + (int64_t)i * g.dir_stride + s.yoff[b] + s.zs[c]);

@@ -168,6 +168,8 @@ class Simulation:
             d.u_in[k] = float(self.boundary.u_in_lat[k])
         d.rank, d.nranks = rank, nranks
         d.precision = _lib.LBW_PREC_SINGLE if cfg.precision == "single" else _lib.LBW_PREC_DOUBLE
+        for k, code in enumerate(cfg.wall_codes()):
+            d.walls[k] = code
         d.feq_in_given = 1
         feq = self.boundary.inflow_populations()
         for i in range(27):

@@ -95,7 +95,8 @@ def oracle_for(sim):
                             for comp, spec, offs, areas, sl in sim._disk_groups]}
     ref = orc.OracleSim(cfg.cells, periodic=cfg.periodicity, op=cfg.operator, omega=u.omega,
                         rates=cfg.higher_order_rates, boundary=cfg.boundary_kind,
-                        u_in=sim.boundary.u_in_lat, points=points, dtype=cfg.dtype)
+                        u_in=sim.boundary.u_in_lat, points=points, dtype=cfg.dtype,
+                        walls=cfg.wall_codes())
     ref.initialize_equilibrium(1.0, sim.boundary.u_in_lat, product=(cfg.operator == "cumulant"))
     return ref
 

@@ -181,3 +181,25 @@ def test_single_precision_oracle_matches_reference(golden):
     assert np.array_equal(ref.interior, g["rotor_f_final"])
     assert np.array_equal(ref.force[1:-1, 1:-1, 1:-1], g["rotor_force_final"])
     tmp.cleanup()
+
+
+def test_wall_oracle_free_slip_fixed_point_and_closed_box_mass():
+    """Walls (an extension; the reference has none): uniform flow along x
+    between free-slip y / z walls is a fixed point, and a closed box
+    (periodic x, no-slip y / z) conserves mass exactly."""
+    u = np.array([0.03, 0.0, 0.0])
+    sim = orc.OracleSim((6, 5, 7), periodic=(True, False, False), op="cumulant", omega=1.3,
+                        walls=(2, 2, 2, 2))
+    sim.initialize_equilibrium(1.0, u, product=True)
+    f0 = sim.interior.copy()
+    for _ in range(5):
+        sim.step()
+    np.testing.assert_allclose(sim.interior, f0, rtol=0, atol=1e-15)
+    rng = np.random.default_rng(5)
+    box = orc.OracleSim((6, 5, 7), periodic=(True, False, False), op="bgk", omega=1.1,
+                        walls=(1, 1, 1, 1))
+    box.interior[...] = orc.W * (1.0 + 0.1 * rng.uniform(-1, 1, box.interior.shape))
+    m0 = box.interior.sum()
+    for _ in range(10):
+        box.step()
+    assert abs(box.interior.sum() - m0) < 1e-12 * m0
