@@ -70,6 +70,11 @@ extern "C" {
 #define LBW_WALL_NO_SLIP 1   /* halfway bounce-back                               */
 #define LBW_WALL_FREE_SLIP 2 /* specular reflection                               */
 
+/* force spreading kernel (lbw_alm_desc.spread_kernel) */
+#define LBW_SPREAD_ROMA 0      /* 3-point Roma kernel (actuator.py:100-110), the reference's */
+#define LBW_SPREAD_GAUSSIAN 1  /* isotropic Gaussian exp(-(r/eps)^2), truncated at 3 eps and
+                                * normalised per axis (extension)                          */
+
 /* outer boundary along x (halo.py:122-141, BoundarySpec.KINDS) */
 #define LBW_BC_PERIODIC 0
 #define LBW_BC_INFLOW_OUTFLOW 1
@@ -241,7 +246,10 @@ typedef struct lbw_alm_desc {
     const int32_t* ring_first;      /* (n_rings,) first point id of the ring    */
     const int32_t* ring_count;      /* (n_rings,) sectors                        */
     const double* ring_ct;          /* (n_rings,) thrust coefficient in [0, 1)   */
-    int64_t reserved[8];
+    int32_t spread_kernel;          /* LBW_SPREAD_*                               */
+    int32_t reserved32;
+    double spread_epsilon;          /* Gaussian width in lattice cells, (0, 2]    */
+    int64_t reserved[6];
 } lbw_alm_desc;
 
 int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc);

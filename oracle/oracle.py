@@ -210,18 +210,33 @@ def disk_forces(ct, axis_world, rho_samples, u_samples, areas, rings, sectors):
     return forces
 
 
-def _support_box(pos):
+def _support_box(pos, halo=1):
     lo = np.empty(3, dtype=np.int64)
     hi = np.empty(3, dtype=np.int64)
     for k in range(3):
         n0 = int(np.floor(pos[k]))
         j0 = int(np.floor(pos[k] - 0.5))
-        lo[k] = min(n0 - 1, j0)
-        hi[k] = max(n0 + 1, j0 + 1)
+        lo[k] = min(n0 - halo, j0)
+        hi[k] = max(n0 + halo, j0 + 1)
     return lo, hi
 
 
-def route_single_block(records, dims, periodic):
+def axis_weights(x, kernel="roma", eps=0.0):
+    """Deposit cells and weights along one axis: the reference's 3-point
+    Roma kernel (actuator.py:190-195), or the Gaussian extension
+    exp(-(r/eps)^2) over |r| <= 3 eps, normalised over that support."""
+    if kernel == "roma":
+        n0 = int(np.floor(x))
+        return [(n0 - 1 + q, roma(r)) for q, r in
+                enumerate((x - (n0 - 0.5), x - (n0 + 0.5), x - (n0 + 1.5)))]
+    R = 3.0 * eps
+    jlo, jhi = int(np.ceil(x - 0.5 - R)), int(np.floor(x - 0.5 + R))
+    e = [np.exp(-((x - (j + 0.5)) / eps) ** 2) for j in range(jlo, jhi + 1)]
+    inv = 1.0 / sum(e)
+    return [(j, v * inv) for j, v in zip(range(jlo, jhi + 1), e)]
+
+
+def route_single_block(records, dims, periodic, halo=1):
     """mark_and_exchange_points (actuator.py:297-341) for a 1x1x1 block grid:
     the block receives its own records plus an image, shifted by -wrap*L,
     for every periodic neighbour offset its support box touches."""
@@ -230,7 +245,7 @@ def route_single_block(records, dims, periodic):
     imgs = []
     for gid, pos, force in records:
         out.append((gid, pos, force))
-        lo, hi = _support_box(pos)
+        lo, hi = _support_box(pos, halo)
         for ox in (-1, 0, 1):
             for oy in (-1, 0, 1):
                 for oz in (-1, 0, 1):
@@ -258,7 +273,7 @@ def round_f32(a):
     return np.asarray(a, dtype=np.float64).astype(np.float32).astype(np.float64)
 
 
-def spread(records, force, dims, dt2, den, rnd=_identity):
+def spread(records, force, dims, dt2, den, rnd=_identity, kernel="roma", eps=0.0):
     """spread_forces (actuator.py:204-247) into a ghosted block at origin 0.
     rnd models the storage dtype of `force`: `+=` on a float32 array rounds
     after every addition."""
@@ -267,20 +282,19 @@ def spread(records, force, dims, dt2, den, rnd=_identity):
         f_lat = np.asarray(f_newton, dtype=np.float64) * dt2 / den
         cells, ws = [], []
         for k in range(3):
-            n0 = int(np.floor(pos[k]))
-            cells.append((n0 - 1, n0, n0 + 1))
-            ws.append([roma(r) for r in (pos[k] - (n0 - 0.5), pos[k] - (n0 + 0.5),
-                                         pos[k] - (n0 + 1.5))])
-        for i in range(3):
+            cw = axis_weights(pos[k], kernel, eps)
+            cells.append([c for c, _ in cw])
+            ws.append([w for _, w in cw])
+        for i in range(len(cells[0])):
             lx = cells[0][i]
             if not 0 <= lx < nx or ws[0][i] == 0.0:
                 continue
-            for j in range(3):
+            for j in range(len(cells[1])):
                 ly = cells[1][j]
                 if not 0 <= ly < ny or ws[1][j] == 0.0:
                     continue
                 wxy = ws[0][i] * ws[1][j]
-                for k in range(3):
+                for k in range(len(cells[2])):
                     lz = cells[2][k]
                     if not 0 <= lz < nz or ws[2][k] == 0.0:
                         continue
@@ -363,9 +377,11 @@ class OracleSim:
             self.blade[sl] = -f
         for p in range(P):
             records.append((p, kin[p, 0:3].copy(), -self.blade[p]))
-        routed = route_single_block(records, self.dims, self.periodic)
+        kernel, eps = pts.get("spreading", ("roma", 0.0))
+        halo = 1 if kernel == "roma" else int(np.ceil(3.0 * eps)) + 1
+        routed = route_single_block(records, self.dims, self.periodic, halo)
         self.force[...] = 0.0
-        spread(routed, self.force, self.dims, pts["dt2"], pts["den"], self.rnd)
+        spread(routed, self.force, self.dims, pts["dt2"], pts["den"], self.rnd, kernel, eps)
 
     def step(self, kin=None):
         if self.points is not None:

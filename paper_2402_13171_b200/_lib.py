@@ -89,7 +89,10 @@ class AlmDesc(ctypes.Structure):
         ("ring_first", _c_i32_p),
         ("ring_count", _c_i32_p),
         ("ring_ct", _c_double_p),
-        ("reserved", ctypes.c_int64 * 8),
+        ("spread_kernel", ctypes.c_int32),
+        ("reserved32", ctypes.c_int32),
+        ("spread_epsilon", ctypes.c_double),
+        ("reserved", ctypes.c_int64 * 6),
     ]
 
 

@@ -60,8 +60,12 @@ struct AlmDev {
     double* samples;       // (P,4)
     double* blade;         // (P,3)
     double* flat;          // (P,3) lattice force on the fluid
-    int32_t* dep_cell;     // (P,3 axes,3) global cell or -1
-    double* dep_w;         // (P,3,3)
+    int32_t* dep_cell;     // (P,3 axes,kw) global cell or -1
+    double* dep_w;         // (P,3,kw)
+    int32_t kw;            // deposit cells per axis (3: Roma)
+    int32_t kernel;        // LBW_SPREAD_*
+    double eps;            // Gaussian width (cells)
+    int32_t halo_x;        // support half-width in x (cells), for slab relevance
     int32_t* clamp_flags;  // (n_polars)
     const int32_t* point_ring;  // (P) disk ring id or -1
     const double* area;         // (P)
@@ -130,6 +134,8 @@ struct AlmState {
     // deposit data itself (no fill kernel, no pool); many points: K5 fills
     // per-row pools.
     bool on_the_fly = false;
+    int32_t kw = 3, kernel = 0, halo_x = 1;
+    double eps = 0.0;
     double* h_ring = nullptr;   // pinned (kRing, P, 18)
     cudaEvent_t ring_ev[kRing] = {};
     int ring_pos = 0;
@@ -185,8 +191,12 @@ struct AlmState {
         a.samples = samples + (size_t)parity * n * 4;
         a.blade = blade + (size_t)parity * n * 3;
         a.flat = flat + (size_t)parity * n * 3;
-        a.dep_cell = dep_cell + (size_t)parity * n * 9;
-        a.dep_w = dep_w + (size_t)parity * n * 9;
+        a.dep_cell = dep_cell + (size_t)parity * n * 3 * kw;
+        a.dep_w = dep_w + (size_t)parity * n * 3 * kw;
+        a.kw = kw;
+        a.kernel = kernel;
+        a.eps = eps;
+        a.halo_x = halo_x;
         a.clamp_flags = clamp_flags;
         a.step = m;
         a.ring_samples = ring_samples;
@@ -796,9 +806,27 @@ __device__ void blade_force_warp(const AlmDev& a, const PointStatic& ps, const d
 
 // per-axis deposit cells + weights, images across periodic faces computed
 // from the shifted position pos - w*L (actuator.py:190-195, 330-332)
-__device__ void deposit_axis(double x, int64_t L, int periodic, int32_t* dc, double* dw) {
+// Gaussian kernel (extension): cells j with |x - (j + 1/2)| <= 3 eps,
+// weights exp(-(r/eps)^2) normalised over that support (per axis, so the
+// deposited momentum equals the point force for interior points).
+constexpr int kMaxKw = 13;   // eps <= 2 -> at most floor(6 eps * 2) + 1 cells
+__device__ __forceinline__ void gaussian_support(double xs, double eps, int64_t& jlo,
+                                                 int64_t& jhi, double& inv_sum) {
+    const double R = 3.0 * eps;
+    jlo = (int64_t)ceil(xs - 0.5 - R);
+    jhi = (int64_t)floor(xs - 0.5 + R);
+    double sum = 0.0;
+    for (int64_t j = jlo; j <= jhi; ++j) {
+        const double r = (xs - ((double)j + 0.5)) / eps;
+        sum += exp(-r * r);
+    }
+    inv_sum = 1.0 / sum;
+}
+
+__device__ void deposit_axis(double x, int64_t L, int periodic, int kernel, double eps, int kw,
+                             int32_t* dc, double* dw) {
     int cnt = 0;
-    for (int q = 0; q < 3; ++q) {
+    for (int q = 0; q < kw; ++q) {
         dc[q] = -1;
         dw[q] = 0.0;
     }
@@ -806,6 +834,19 @@ __device__ void deposit_axis(double x, int64_t L, int periodic, int32_t* dc, dou
     for (int im = 0; im < nimg; ++im) {
         const double w = im == 0 ? 0.0 : (im == 1 ? 1.0 : -1.0);
         const double xs = im == 0 ? x : x - w * (double)L;
+        if (kernel == LBW_SPREAD_GAUSSIAN) {
+            int64_t jlo, jhi;
+            double inv_sum;
+            gaussian_support(xs, eps, jlo, jhi, inv_sum);
+            for (int64_t j = jlo; j <= jhi; ++j) {
+                if (j < 0 || j >= L || cnt >= kw) continue;
+                const double r = (xs - ((double)j + 0.5)) / eps;
+                dc[cnt] = (int32_t)j;
+                dw[cnt] = exp(-r * r) * inv_sum;
+                ++cnt;
+            }
+            continue;
+        }
         const double n0f = floor(xs);
         const int64_t n0 = (int64_t)n0f;
         const double r[3] = {xs - (n0f - 0.5), xs - (n0f + 0.5), xs - (n0f + 1.5)};
@@ -813,7 +854,7 @@ __device__ void deposit_axis(double x, int64_t L, int periodic, int32_t* dc, dou
             const int64_t c = n0 - 1 + q;
             if (c < 0 || c >= L) continue;
             const double wt = roma(r[q]);
-            if (wt == 0.0 || cnt >= 3) continue;
+            if (wt == 0.0 || cnt >= kw) continue;
             dc[cnt] = (int32_t)c;
             dw[cnt] = wt;
             ++cnt;
@@ -824,9 +865,10 @@ __device__ void deposit_axis(double x, int64_t L, int periodic, int32_t* dc, dou
 // (x,y) row of deposit pair q = p*9 + k (k: 3 x-cells x 3 y-cells of point
 // p) as a slab row index, or -1 when it is not a cell of this slab.
 __device__ __forceinline__ int32_t pair_row(const AlmDev& a, const Geom& g, int q) {
-    const int32_t* dc = a.dep_cell + (int64_t)(q / 9) * 9;
-    const int k = q % 9;
-    const int32_t cxg = dc[k / 3], cy = dc[3 + k % 3];
+    const int kw = a.kw, kk = kw * kw;
+    const int32_t* dc = a.dep_cell + (int64_t)(q / kk) * 3 * kw;
+    const int k = q % kk;
+    const int32_t cxg = dc[k / kw], cy = dc[kw + k % kw];
     const int64_t x = (int64_t)cxg - g.x0;
     if (cxg < 0 || cy < 0 || x < 0 || x >= g.nxl) return -1;
     return (int32_t)(x * g.ny + cy);
@@ -874,16 +916,18 @@ __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, co
     const double* kin = kr;
     // deposit cells / Roma weights per axis (lanes 8..10), kept in registers
     // for the row tags below and stored for the sweep / fill / next sample
-    int32_t dcl[3] = {-1, -1, -1};
+    const int kw = a.kw;
+    int32_t dcl[kMaxKw];
+    for (int q = 0; q < 3; ++q) dcl[q] = -1;
     if (phase != 1 && lane >= 8 && lane <= 10) {
         const int k = lane - 8;
         const int64_t L = k == 0 ? g.nxg : (k == 1 ? g.ny : g.nz);
         const int per = k == 0 ? m.per_x : (k == 1 ? g.per_y : g.per_z);
-        double dwl[3];
-        deposit_axis(kin[k], L, per, dcl, dwl);
-        for (int q = 0; q < 3; ++q) {
-            a.dep_cell[(int64_t)p * 9 + 3 * k + q] = dcl[q];
-            a.dep_w[(int64_t)p * 9 + 3 * k + q] = dwl[q];
+        double dwl[kMaxKw];
+        deposit_axis(kin[k], L, per, a.kernel, a.eps, kw, dcl, dwl);
+        for (int q = 0; q < kw; ++q) {
+            a.dep_cell[(int64_t)p * 3 * kw + kw * k + q] = dcl[q];
+            a.dep_w[(int64_t)p * 3 * kw + kw * k + q] = dwl[q];
         }
     }
     int64_t j0[3];
@@ -931,19 +975,27 @@ __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, co
         for (int q = 0; q < 4; ++q) acc[q] += w * vc[q];
     }
     if (s.flag_rows && phase != 1) {
-        // tag this step's rows (benign race: equal values); the x / y cells
-        // come from lanes 8 / 9 by shuffle, not back from memory
-        int32_t cx[3], cy[3];
-        for (int q = 0; q < 3; ++q) {
-            cx[q] = __shfl_sync(0xffffffffu, dcl[q], 8);
-            cy[q] = __shfl_sync(0xffffffffu, dcl[q], 9);
-        }
-        if (lane < 9) {
-            const int32_t cxg = cx[lane / 3], cyy = cy[lane % 3];
-            const int64_t x = (int64_t)cxg - g.x0;
-            LBW_CHECK(cyy < g.ny);
-            if (cxg >= 0 && cyy >= 0 && x >= 0 && x < g.nxl)
-                s.row_key[x * g.ny + cyy] = row_key_of(s.tag, 0);
+        // tag this step's rows (benign race: equal values); for the Roma
+        // kernel the x / y cells come from lanes 8 / 9 by shuffle
+        if (kw == 3) {
+            int32_t cx[3], cy[3];
+            for (int q = 0; q < 3; ++q) {
+                cx[q] = __shfl_sync(0xffffffffu, dcl[q], 8);
+                cy[q] = __shfl_sync(0xffffffffu, dcl[q], 9);
+            }
+            if (lane < 9) {
+                const int32_t cxg = cx[lane / 3], cyy = cy[lane % 3];
+                const int64_t x = (int64_t)cxg - g.x0;
+                LBW_CHECK(cyy < g.ny);
+                if (cxg >= 0 && cyy >= 0 && x >= 0 && x < g.nxl)
+                    s.row_key[x * g.ny + cyy] = row_key_of(s.tag, 0);
+            }
+        } else {
+            __syncwarp();   // the deposit cells stored above are visible to the warp
+            for (int t = lane; t < kw * kw; t += 32) {
+                const int32_t row = pair_row(a, g, p * kw * kw + t);
+                if (row >= 0) s.row_key[row] = row_key_of(s.tag, 0);
+            }
         }
     }
     // Multi-slab: only points whose Roma support reaches this slab (their
@@ -953,7 +1005,7 @@ __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, co
     const int64_t ox = n0 - g.x0;
     const bool owner = phase == 0 || (ox >= 0 && ox < g.nxl);
     bool relevant = phase == 0;
-    for (int dxc = -1; dxc <= 1 && !relevant; ++dxc) {
+    for (int dxc = -a.halo_x; dxc <= a.halo_x && !relevant; ++dxc) {
         int64_t c = n0 + dxc;
         if (m.per_x) c = (c % g.nxg + g.nxg) % g.nxg;
         relevant = c - g.x0 >= 0 && c - g.x0 < g.nxl;
@@ -990,11 +1042,11 @@ __global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s, int phase
     const ForceView& fv = m.fv;
     if (fv.row_key != nullptr && fv.pool == nullptr && fv.npts > 0 && fv.npts <= kOnTheFlyMaxPoints &&
         phase != 2) {
-        const int n = fv.npts;
-        double* w = alm_sm;                                   // (n, 9)
-        double* fl = w + n * 9;                               // (n, 3)
-        int32_t* dc = reinterpret_cast<int32_t*>(fl + n * 3); // (n, 9)
-        for (int i = threadIdx.x; i < n * 9; i += blockDim.x) {
+        const int n = fv.npts, nd = n * 3 * fv.kw;
+        double* w = alm_sm;                                   // (n, 3, kw)
+        double* fl = w + nd;                                  // (n, 3)
+        int32_t* dc = reinterpret_cast<int32_t*>(fl + n * 3); // (n, 3, kw)
+        for (int i = threadIdx.x; i < nd; i += blockDim.x) {
             w[i] = fv.dep_w[i];
             dc[i] = fv.dep_cell[i];
         }
@@ -1014,9 +1066,9 @@ __global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s, int phase
 // area_i * axis; the blade force is its negation (sim.py:236-244).
 // Slab-local view of a disk point (multi-slab): its Roma support reaches
 // this slab / floor(x) lies in it.
-__device__ bool point_relevant(const Geom& g, int per_x, double x) {
+__device__ bool point_relevant(const Geom& g, int per_x, int halo, double x) {
     const int64_t n0 = (int64_t)floor(x);
-    for (int dxc = -1; dxc <= 1; ++dxc) {
+    for (int dxc = -halo; dxc <= halo; ++dxc) {
         int64_t c = n0 + dxc;
         if (per_x) c = (c % g.nxg + g.nxg) % g.nxg;
         if (c - g.x0 >= 0 && c - g.x0 < g.nxl) return true;
@@ -1034,7 +1086,7 @@ __device__ void disk_ring(const AlmDev& a, const Geom& g, int per_x, int linked,
         for (int i = 0; i < cnt; ++i) {
             const int p = first + i;
             all_ok &= a.ring_sample_ok[p] != 0;
-            needed |= point_relevant(g, per_x, a.kin[(int64_t)p * kKin]);
+            needed |= point_relevant(g, per_x, a.halo_x, a.kin[(int64_t)p * kKin]);
         }
         if (!needed) {
             for (int i = 0; i < cnt; ++i)
@@ -1099,7 +1151,7 @@ constexpr int kFillSmemPairs = 4096;
 __global__ void k_alm_fill(AlmDev a, Geom g, ForceSet s) {
     __shared__ int32_t rows_sm[kFillSmemPairs];
     LBW_TRACE_BEGIN(4, a.step);
-    const int npairs = a.n * 9;
+    const int kw = a.kw, npairs = a.n * kw * kw;
     const bool staged = npairs <= kFillSmemPairs;
     if (staged)
         for (int q = threadIdx.x; q < npairs; q += blockDim.x) rows_sm[q] = pair_row(a, g, q);
@@ -1128,13 +1180,13 @@ __global__ void k_alm_fill(AlmDev a, Geom g, ForceSet s) {
             bool hit = false;
             double wxy = 0.0;
             if (pl < a.n) {
-                const int32_t* dc = a.dep_cell + (int64_t)pl * 9;
-                const double* dw = a.dep_w + (int64_t)pl * 9;
+                const int32_t* dc = a.dep_cell + (int64_t)pl * 3 * kw;
+                const double* dw = a.dep_w + (int64_t)pl * 3 * kw;
                 double wx = 0.0, wy = 0.0;
                 bool hx = false, hy = false;
-                for (int t = 0; t < 3; ++t) {
+                for (int t = 0; t < kw; ++t) {
                     if (dc[t] == xg) { hx = true; wx = dw[t]; }
-                    if (dc[3 + t] == y) { hy = true; wy = dw[3 + t]; }
+                    if (dc[kw + t] == y) { hy = true; wy = dw[kw + t]; }
                 }
                 hit = hx && hy;
                 wxy = wx * wy;
@@ -1146,9 +1198,9 @@ __global__ void k_alm_fill(AlmDev a, Geom g, ForceSet s) {
                 const double w2 = __shfl_sync(0xffffffffu, wxy, src);
                 const int p = c0 + src;
                 if (z < g.nz) {
-                    const int32_t* dc = a.dep_cell + (int64_t)p * 9 + 6;
-                    const double* dw = a.dep_w + (int64_t)p * 9 + 6;
-                    for (int t = 0; t < 3; ++t) {
+                    const int32_t* dc = a.dep_cell + (int64_t)p * 3 * kw + 2 * kw;
+                    const double* dw = a.dep_w + (int64_t)p * 3 * kw + 2 * kw;
+                    for (int t = 0; t < kw; ++t) {
                         if (dc[t] == z) {
                             const double w = w2 * dw[t];
                             // `force[c] += w * F_lat` on an array of the storage
@@ -1194,6 +1246,8 @@ int dev_alloc(lbw_domain* d, AlmState* s, T** p, size_t count) {
 
 bool alm_active(const lbw_domain* d) { return d->alm != nullptr && d->alm->n > 0; }
 
+int alm_support_halo(const lbw_domain* d) { return alm_active(d) ? d->alm->halo_x : 0; }
+
 double* alm_cube(const lbw_domain* d) { return alm_active(d) ? d->alm->cube : nullptr; }
 
 void alm_destroy(lbw_domain* d) {
@@ -1223,6 +1277,7 @@ ForceView alm_force_view(const lbw_domain* d, int64_t m) {
         const AlmDev a = s->dev(m);
         v.pool = nullptr;
         v.npts = s->n;
+        v.kw = s->kw;
         v.dep_cell = a.dep_cell;
         v.dep_w = a.dep_w;
         v.flat = a.flat;
@@ -1302,7 +1357,8 @@ int alm_launch(lbw_domain* d, int64_t m) {
     const int threads = 32;
     const size_t pts_smem =
         (md.fv.row_key != nullptr && md.fv.pool == nullptr && md.fv.npts <= kOnTheFlyMaxPoints)
-            ? (size_t)md.fv.npts * (12 * sizeof(double) + 9 * sizeof(int32_t))
+            ? (size_t)md.fv.npts * ((3 * md.fv.kw + 3) * sizeof(double) +
+                                    3 * md.fv.kw * sizeof(int32_t))
             : 0;
     const unsigned blocks = (unsigned)((s->n * 32 + threads - 1) / threads);
     CubeArgs cube{};
@@ -1339,7 +1395,7 @@ int alm_launch(lbw_domain* d, int64_t m) {
         count_launch();
     }
     if (!s->on_the_fly) {
-        k_alm_fill<<<(unsigned)((s->n * 9 + 3) / 4), 128, 0, st>>>(a, g, fs);
+        k_alm_fill<<<(unsigned)((s->n * s->kw * s->kw + 3) / 4), 128, 0, st>>>(a, g, fs);
         count_launch();
     }
     count_launch();
@@ -1394,6 +1450,11 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
                     "thrust coefficient must lie in [0, 1)");
         }
     }
+    LBW_REQ(desc->spread_kernel == LBW_SPREAD_ROMA || desc->spread_kernel == LBW_SPREAD_GAUSSIAN,
+            "unknown spreading kernel");
+    LBW_REQ(desc->spread_kernel != LBW_SPREAD_GAUSSIAN ||
+                (desc->spread_epsilon > 0.0 && desc->spread_epsilon <= 2.0),
+            "Gaussian spreading width must lie in (0, 2] lattice cells");
     int64_t total_rows = 0;
     for (int k = 0; k < desc->n_polars; ++k) {
         LBW_REQ(desc->polar_rows[k] >= 2, "polar needs at least 2 rows");
@@ -1407,6 +1468,12 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     s->rho_ref = desc->rho_ref;
     s->dt2 = desc->force_dt2;
     s->den = desc->force_den;
+    s->kernel = desc->spread_kernel;
+    if (s->kernel == LBW_SPREAD_GAUSSIAN) {
+        s->eps = desc->spread_epsilon;
+        s->kw = (int32_t)floor(6.0 * s->eps) + 1;      // cells within 3 eps of a point
+        s->halo_x = (int32_t)ceil(3.0 * s->eps) + 1;
+    }
     int rc = LBW_OK;
     auto A = [&](auto** p, size_t n) {
         if (rc == LBW_OK) rc = dev_alloc(d, s, p, n);
@@ -1427,8 +1494,8 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     A(&s->cube, (size_t)2 * P * 32 + (size_t)2 * P * 4);   // values, then (2,P,8) int32 tags
     A(&s->ring_samples, (size_t)P * 4);
     A(&s->ring_sample_ok, P);
-    A(&s->dep_cell, (size_t)2 * P * 9);
-    A(&s->dep_w, (size_t)2 * P * 9);
+    A(&s->dep_cell, (size_t)2 * P * 3 * s->kw);
+    A(&s->dep_w, (size_t)2 * P * 3 * s->kw);
     A(&s->clamp_flags, std::max(1, desc->n_polars));
     A(&s->error_flags, 1);
     const int R = desc->point_ring ? desc->n_rings : 0;
@@ -1442,7 +1509,7 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     // sparse force sets: a point touches at most 3x3 (x,y) rows
     const int64_t rows = (int64_t)d->g.nxl * d->g.ny;
     s->on_the_fly = P <= kOnTheFlyMaxPoints;
-    const int64_t cap = s->on_the_fly ? 0 : (int64_t)9 * P;   // slot = deposit pair index
+    const int64_t cap = s->on_the_fly ? 0 : (int64_t)s->kw * s->kw * P;   // slot = deposit pair
     for (auto& fs : s->set) {
         A(&fs.row_key, rows);
         if (cap) {

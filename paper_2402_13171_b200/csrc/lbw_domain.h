@@ -128,6 +128,7 @@ ForceView alm_force_view(const lbw_domain* d, int64_t m);
 int alm_invalidate(lbw_domain* d);
 void alm_destroy(lbw_domain* d);
 bool alm_active(const lbw_domain* d);
+int alm_support_halo(const lbw_domain* d);   // spreading support half-width in x (cells)
 // device cube buffer (2, P, 8, 4) of the actuator sampling, or nullptr
 double* alm_cube(const lbw_domain* d);
 

@@ -69,8 +69,9 @@ struct ForceView {
     // ... actuator view: a tagged row's force is summed from the points'
     // deposit cells in ascending id at the cell (few points, see lbw_alm.cu)
     int32_t npts;
-    const int32_t* dep_cell;  // (npts, 3 axes, 3) global cell or -1
-    const double* dep_w;      // (npts, 3, 3) Roma weights
+    int32_t kw;               // deposit cells per axis (3: Roma)
+    const int32_t* dep_cell;  // (npts, 3 axes, kw) global cell or -1
+    const double* dep_w;      // (npts, 3, kw) kernel weights
     const double* flat;       // (npts, 3) lattice force on the fluid
 };
 __host__ __device__ inline uint64_t row_key_of(uint32_t tag, int32_t slot) {

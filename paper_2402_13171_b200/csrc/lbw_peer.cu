@@ -13,6 +13,7 @@
 // end: no host round trip, no spinning kernel.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstring>
 
 #include "lbw_domain.h"
@@ -141,9 +142,11 @@ int lbw_domain_export_handle(lbw_domain* d, void* blob, int64_t* blob_bytes) {
 int lbw_domain_import_peers(lbw_domain* d, const void* lo_blob, const void* hi_blob) {
     LBW_REQ(d, "null domain");
     LBW_REQ(d->flags, "export this domain's handle before importing its peers");
-    // a point's sampling cube and Roma support span 3 x cells: with slabs of
-    // >= 3 planes they never reach beyond the immediate neighbours
-    LBW_REQ(!alm_active(d) || d->g.nxl >= 3, "actuator runs need slabs of >= 3 x planes");
+    // a point's sampling cube and spreading support reach halo (+1) x cells:
+    // with slabs that wide they never reach beyond the immediate neighbours
+    LBW_REQ(!alm_active(d) || d->g.nxl >= std::max(3, alm_support_halo(d) + 2),
+            "actuator runs need slabs of >= 3 x planes (support half-width + 2 with a "
+            "Gaussian spreading kernel)");
     LBW_CK(cudaSetDevice(d->device));
     LBW_CK(cudaStreamSynchronize(d->stream));
     const void* blobs[2] = {lo_blob, hi_blob};

@@ -212,21 +212,22 @@ template <class T>
 __device__ __forceinline__ void actuator_force(const ForceView& fv, int64_t xg, int y, int z,
                                             double& Fx, double& Fy, double& Fz) {
     double F[3] = {0.0, 0.0, 0.0};
+    const int kw = fv.kw;
     for (int p = 0; p < fv.npts; ++p) {
-        const int32_t* dc = fv.dep_cell + (int64_t)p * 9;
-        const double* dw = fv.dep_w + (int64_t)p * 9;
+        const int32_t* dc = fv.dep_cell + (int64_t)p * 3 * kw;
+        const double* dw = fv.dep_w + (int64_t)p * 3 * kw;
         double wx = 0.0, wy = 0.0;
         bool hx = false, hy = false;
-        for (int t = 0; t < 3; ++t) {
+        for (int t = 0; t < kw; ++t) {
             if (dc[t] == xg) { hx = true; wx = dw[t]; }
-            if (dc[3 + t] == y) { hy = true; wy = dw[3 + t]; }
+            if (dc[kw + t] == y) { hy = true; wy = dw[kw + t]; }
         }
         if (!(hx && hy)) continue;
         // explicit roundings: no FMA contraction in either flavour's TU
         const double wxy = __dmul_rn(wx, wy);
-        for (int t = 0; t < 3; ++t) {
-            if (dc[6 + t] == z) {
-                const double w = __dmul_rn(wxy, dw[6 + t]);
+        for (int t = 0; t < kw; ++t) {
+            if (dc[2 * kw + t] == z) {
+                const double w = __dmul_rn(wxy, dw[2 * kw + t]);
                 for (int c = 0; c < 3; ++c)
                     F[c] = (double)(T)__dadd_rn(F[c], __dmul_rn(w, fv.flat[p * 3 + c]));
             }

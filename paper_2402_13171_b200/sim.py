@@ -248,6 +248,8 @@ class Simulation:
         a.rho_ref = self.units.rho_ref
         a.force_dt2 = self.units.force_dt2
         a.force_den = self.units.force_den
+        a.spread_kernel = 1 if self.cfg.spread_kernel == "gaussian" else 0
+        a.spread_epsilon = float(self.cfg.spread_epsilon)
         if self._disk_groups:
             # one ring = `sectors` consecutive samples (DiskSpec.sample_offsets)
             ring_first, ring_count, ring_ct = [], [], []

@@ -178,6 +178,17 @@ def main():
     ok &= run_case("rotor-many-points",
                    lambda: rotor_config(cells=(nx, 12, 12), position=(1.5, 0.3, 0.0),
                                         arithmetic="fast", points_per_blade=30)[0], 8, False)
+    # Gaussian spreading (support half-width 4 x cells across the slab face)
+    def gaussian_cfg():
+        import tempfile
+        from tests.scenarios import rotor_raw, write_rotor_files
+        d = tempfile.mkdtemp()
+        write_rotor_files(d)
+        raw = rotor_raw((nx, 12, 12), (True, True, True), position=(1.5, 0.3, 0.0),
+                        arithmetic="fast")
+        raw["run"]["spreading"] = {"kernel": "gaussian", "epsilon": 1.0}
+        return parse_config(raw, base_dir=d)
+    ok &= run_case("rotor-gaussian", gaussian_cfg, 8, False)
     # actuator disks: an aligned disk on the slab face and a yawed one whose
     # rings spread over neighbouring slabs (ring averages across GPUs)
     for name, yaw in (("disk-aligned", 0.0), ("disk-yawed", 35.0)):

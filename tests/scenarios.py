@@ -92,7 +92,8 @@ def oracle_for(sim):
                   "den": u.rho_ref * u.dx ** 4,
                   "area": np.array([p.area for p in sim.points]),
                   "disks": [(sl.start, spec.rings, spec.sectors, spec.thrust_coefficient)
-                            for comp, spec, offs, areas, sl in sim._disk_groups]}
+                            for comp, spec, offs, areas, sl in sim._disk_groups],
+                  "spreading": (cfg.spread_kernel, cfg.spread_epsilon)}
     ref = orc.OracleSim(cfg.cells, periodic=cfg.periodicity, op=cfg.operator, omega=u.omega,
                         rates=cfg.higher_order_rates, boundary=cfg.boundary_kind,
                         u_in=sim.boundary.u_in_lat, points=points, dtype=cfg.dtype,
