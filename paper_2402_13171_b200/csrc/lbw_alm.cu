@@ -1429,7 +1429,7 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     LBW_CK(cudaSetDevice(d->device));
     d->touched = true;
     if (desc->n_points > 0) {
-        int rc_ = green_partition(d, alm_sm_count());
+        int rc_ = green_partition(d, alm_sm_count(d));
         if (rc_) return rc_;
     }
     LBW_CK(cudaStreamSynchronize(d->stream));

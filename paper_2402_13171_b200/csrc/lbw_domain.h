@@ -140,7 +140,7 @@ void peer_close(lbw_domain* d);
 int ensure_stage(lbw_domain* d, size_t bytes);
 
 // lbw_green.cu: SM partition between the sweep and the actuator chain
-int alm_sm_count();
+int alm_sm_count(const lbw_domain* d);
 int green_partition(lbw_domain* d, int alm_sms);
 cudaStream_t green_alm_stream(lbw_domain* d);   // nullptr without a partition
 void green_release(lbw_domain* d);

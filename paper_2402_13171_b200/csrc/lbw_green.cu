@@ -10,8 +10,10 @@
 // chain runs at its unloaded speed.  Streams of both green contexts share
 // the primary context's memory and events, so nothing else changes.
 //
-// LBW_ALM_SMS (env): SMs given to the chain when actuator points are
-// configured (default 8; 0 disables the partition).
+// The partition costs the sweep 8 of 148 SMs (~1.7 % at C2), so by default
+// it is used only on slabs small enough for the chain's latency to matter
+// (< 3.5 M cells: a sweep under ~230 us).  LBW_ALM_SMS (env) overrides:
+// 0 never, N > 0 always with N SMs.
 #include <cuda.h>
 
 #include <cstdlib>
@@ -58,9 +60,11 @@ const GreenApi& api() {
 
 }  // namespace
 
-int alm_sm_count() {
+int alm_sm_count(const lbw_domain* d) {
     const char* e = getenv("LBW_ALM_SMS");
-    return e ? atoi(e) : 8;
+    if (e) return atoi(e);
+    const int64_t cells = (int64_t)d->g.nxl * d->g.ny * d->g.nz;
+    return cells < 3500000 ? 8 : 0;
 }
 
 int green_partition(lbw_domain* d, int alm_sms) {
