@@ -394,7 +394,10 @@ class Simulation:
                 rc = _lib.load().lbw_alm_get(self._domain, _lib.ptr(rho), _lib.ptr(u),
                                              _lib.ptr(blade))
                 if rc == _lib.LBW_EINVAL:
-                    raise ValueError(_lib.last_error())
+                    msg = _lib.last_error()
+                    # owner_block_of_position (blocks.py:57-70) raises ConfigError;
+                    # a non-positive density is blade_element_force's ValueError
+                    raise (ConfigError if "outside" in msg or "spans" in msg else ValueError)(msg)
                 _lib.check(rc, "ALM results")
             self._results = (rho, u, blade)
         return self._results
@@ -506,6 +509,9 @@ class Simulation:
         self._poll(wait=True)
         self._warn_clamps()
         self.sync_topologies()
+        if self.points:
+            self._results = None
+            self._alm_results()   # raises for points that left the domain (device flags)
 
     # ---------------------------------------------------------- output
     def _recompute_moments(self):
