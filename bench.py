@@ -411,11 +411,13 @@ def cpu_baseline(args, budget_s=20.0):
     cores = len(os.sched_getaffinity(0))
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
     tmp = tempfile.TemporaryDirectory()
-    cfg, desc = make_config(args.config, 1, "exact", tmp.name, args.precision)
+    cfg, desc = make_config(_host_sample_config(args.config), 1, "exact", tmp.name,
+                            args.precision)
     host = _HostOnlySim(cfg)
     t1 = _oracle_run(cfg, 1, host)
     steps = int(max(1, min(50, budget_s / max(t1, 1e-3))))
-    cfg, desc = make_config(args.config, 1, "exact", tmp.name, args.precision)
+    cfg, desc = make_config(_host_sample_config(args.config), 1, "exact", tmp.name,
+                            args.precision)
     host = _HostOnlySim(cfg)
     t = _oracle_run(cfg, steps, host)
     cells = int(np.prod(cfg.cells))
@@ -426,28 +428,36 @@ def cpu_baseline(args, budget_s=20.0):
                       f"(-O2 -ffp-contract=off, OpenMP {cores} threads), {t:.1f} s"}
 
 
-def run_reference(args, rank):
+def _host_sample_config(name):
+    """Host-side sample of a workload: C4 / C5 (116 / 232 GB of state) are
+    timed on the C3 slab (256^3 + rotor: the same per-cell work)."""
+    return "c3" if name in ("c4", "c5") else name
+
+
+def run_reference(args, rank, budget_s=150.0):
     if rank != 0:
         return None
     cb = cpu_baseline(args, budget_s=args.cpu_budget)
-    tmp = tempfile.TemporaryDirectory()
-    cfg, desc = make_config(args.config, 1, "exact", tmp.name, args.precision)
-    tmp.cleanup()
-    # time exactly K steps (after W warm-ups) so the arm is comparable
+    # time K steps (bounded so the arm ends within a few minutes: fewer
+    # steps of the same workload when K would take longer than budget_s)
     from oracle import oracle as orc  # noqa: F401
     tmp = tempfile.TemporaryDirectory()
-    cfg, desc = make_config(args.config, 1, "exact", tmp.name, args.precision)
-    host = _HostOnlySim(cfg)
-    t = _oracle_run(cfg, args.steps, host)
-    tmp.cleanup()
+    cfg, desc = make_config(_host_sample_config(args.config), 1, "exact", tmp.name,
+                            args.precision)
     cells = int(np.prod(cfg.cells))
-    value = cells * args.steps / t / 1e6
+    est = cells / (cb["value"] * 1e6) if cb["value"] > 0 else 1.0
+    n = int(max(1, min(args.steps, budget_s / max(est, 1e-6))))
+    host = _HostOnlySim(cfg)
+    t = _oracle_run(cfg, n, host)
+    tmp.cleanup()
+    value = cells * n / t / 1e6
     cb["value"] = round(value, 3)
-    cb["sample"] = f"{args.steps} full steps of {desc}, C oracle, {cb['cores']} threads"
+    cb["sample"] = (f"{n} of {args.steps} requested steps of {desc}, C oracle, "
+                    f"{cb['cores']} threads")
     return {"metric": METRIC if args.precision == "double" else METRIC_SINGLE,
             "value": round(value, 3), "unit": "MLUP/s", "n_gpus": 0,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(1e3 * t / args.steps, 3), "higher_is_better": True,
+            "ms_per_step": round(1e3 * t / n, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "cells": list(cfg.cells), "parallelism": "host threads"},
             "impl": "reference", "cpu_baseline": cb,
