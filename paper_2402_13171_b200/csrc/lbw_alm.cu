@@ -592,6 +592,12 @@ __global__ void k_kinematics(KinDev k, AlmDev a, Geom g, int per_x, int advance)
     LBW_TRACE_END(1, a.step);
 }
 
+__device__ __noinline__ void load_cell_general(const void* buf, const Geom& g, bool pull, int x,
+                                               int y, int z, double (&f)[27]) {
+    if (pull) load_cell_any<true>(buf, g, x, y, z, f);
+    else load_cell_any<false>(buf, g, x, y, z, f);
+}
+
 // Macro (rho, u) of global cell (gx,gy,gz), following the ghost semantics
 // of PdfField.macro (fields.py:35-36, halo.py:144-160).  Returns MA_REMOTE
 // (nothing written) when the cell belongs to another slab, MA_OWNED for a
@@ -652,14 +658,22 @@ __device__ int macro_at_raw(const Geom& g, const MacroDev& m, int64_t gx, int64_
         put(m.dense + cell * 4);
         return MA_OWNED;
     }
-    // the force row key first, so its latency overlaps the population loads
     const uint64_t key = m.fv.row_key ? m.fv.row_key[x * g.ny + gy] : 0ull;
-    double f[27];
-    if (m.pull) load_cell_any<true>(m.buf, g, (int)x, (int)gy, (int)gz, f);
-    else load_cell_any<false>(m.buf, g, (int)x, (int)gy, (int)gz, f);
     double Fx, Fy, Fz;
     if (g.single) force_from_key<float>(m.fv, g, key, (int)x, (int)gy, (int)gz, Fx, Fy, Fz);
     else force_from_key<double>(m.fv, g, key, (int)x, (int)gy, (int)gz, Fx, Fy, Fz);
+    double f[27];
+    // interior cells take the compact branch-free pull; cells at boundaries
+    // (x faces, non-periodic y / z, walls) the general one, out of line so
+    // this kernel's code stays small
+    if (m.pull && pull_is_simple(g, (int)x, (int)gy, (int)gz)) {
+        if (g.single)
+            load_cell_simple(static_cast<const float*>(m.buf), g, (int)x, (int)gy, (int)gz, f);
+        else
+            load_cell_simple(static_cast<const double*>(m.buf), g, (int)x, (int)gy, (int)gz, f);
+    } else {
+        load_cell_general(m.buf, g, m.pull != 0, (int)x, (int)gy, (int)gz, f);
+    }
     const Macro mm = moments_exact(f, Fx, Fy, Fz, 1.0);
     out[0] = mm.rho;
     out[1] = mm.ux;
@@ -876,6 +890,20 @@ __device__ __forceinline__ int32_t pair_row(const AlmDev& a, const Geom& g, int 
 
 constexpr int kOnTheFlyMaxPoints = 64;
 
+// deposit cells of a wide (Gaussian) kernel, stored straight to the point's
+// deposit arrays; out of line to keep the Roma path of K4 compact
+__device__ __noinline__ void deposit_axis_wide(const AlmDev& a, int p, int k, double x, int64_t L,
+                                               int per) {
+    const int kw = a.kw;
+    int32_t dc[kMaxKw];
+    double dw[kMaxKw];
+    deposit_axis(x, L, per, a.kernel, a.eps, kw, dc, dw);
+    for (int q = 0; q < kw; ++q) {
+        a.dep_cell[(int64_t)p * 3 * kw + kw * k + q] = dc[q];
+        a.dep_w[(int64_t)p * 3 * kw + kw * k + q] = dw[q];
+    }
+}
+
 // K4: one warp per point
 // phase 0: single slab, everything in one pass.  Multi-slab: phase 1 only
 // computes the cube values of this slab's cells and stores them into the
@@ -917,17 +945,20 @@ __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, co
     // deposit cells / Roma weights per axis (lanes 8..10), kept in registers
     // for the row tags below and stored for the sweep / fill / next sample
     const int kw = a.kw;
-    int32_t dcl[kMaxKw];
-    for (int q = 0; q < 3; ++q) dcl[q] = -1;
+    int32_t dcl[3] = {-1, -1, -1};   // Roma: kept in registers for the row tags
     if (phase != 1 && lane >= 8 && lane <= 10) {
         const int k = lane - 8;
         const int64_t L = k == 0 ? g.nxg : (k == 1 ? g.ny : g.nz);
         const int per = k == 0 ? m.per_x : (k == 1 ? g.per_y : g.per_z);
-        double dwl[kMaxKw];
-        deposit_axis(kin[k], L, per, a.kernel, a.eps, kw, dcl, dwl);
-        for (int q = 0; q < kw; ++q) {
-            a.dep_cell[(int64_t)p * 3 * kw + kw * k + q] = dcl[q];
-            a.dep_w[(int64_t)p * 3 * kw + kw * k + q] = dwl[q];
+        if (kw == 3) {
+            double dwl[3];
+            deposit_axis(kin[k], L, per, LBW_SPREAD_ROMA, 0.0, 3, dcl, dwl);
+            for (int q = 0; q < 3; ++q) {
+                a.dep_cell[(int64_t)p * 9 + 3 * k + q] = dcl[q];
+                a.dep_w[(int64_t)p * 9 + 3 * k + q] = dwl[q];
+            }
+        } else {
+            deposit_axis_wide(a, p, k, kin[k], L, per);
         }
     }
     int64_t j0[3];

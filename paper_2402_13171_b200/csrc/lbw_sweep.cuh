@@ -47,6 +47,7 @@ struct PullSrc {
     int32_t zs[3];
     bool yok[3], zok[3];
     int8_t ywall[3], zwall[3];  // LBW_WALL_* of the face a failing source crosses
+    bool any_wall;              // some source of this cell lies beyond a wall
 };
 
 __device__ __forceinline__ void x_source(const Geom& g, int x, int cx, int64_t& off, int32_t& kind) {
@@ -64,6 +65,7 @@ __device__ __forceinline__ void x_source(const Geom& g, int x, int cx, int64_t& 
 }
 
 __device__ __forceinline__ void make_pull(const Geom& g, int x, int y, int z, PullSrc& s) {
+    s.any_wall = false;
 #pragma unroll
     for (int c = -1; c <= 1; ++c) {
         x_source(g, x, c, s.xoff[c + 1], s.xkind[c + 1]);
@@ -74,6 +76,7 @@ __device__ __forceinline__ void make_pull(const Geom& g, int x, int y, int z, Pu
         s.yoff[c + 1] = yok ? ys * g.zp : 0;
         s.yok[c + 1] = yok;
         s.ywall[c + 1] = yok ? 0 : (int8_t)g.walls[ys < 0 ? 0 : 1];
+        s.any_wall |= s.ywall[c + 1] != 0;
         int zs = z - c;
         bool zok = true;
         if (zs < 0) { if (g.per_z) zs += g.nz; else zok = false; }
@@ -81,6 +84,7 @@ __device__ __forceinline__ void make_pull(const Geom& g, int x, int y, int z, Pu
         s.zs[c + 1] = zok ? zs : 0;
         s.zok[c + 1] = zok;
         s.zwall[c + 1] = zok ? 0 : (int8_t)g.walls[zs < 0 ? 2 : 3];
+        s.any_wall |= s.zwall[c + 1] != 0;
     }
 }
 
@@ -116,26 +120,36 @@ __device__ __forceinline__ double stored(double v) {
     return (double)(T)v;
 }
 
-// Population i of cell (x,y,z) whose pull source lies beyond a y / z wall
-// (the walls are halfway between the boundary cells and the ghosts):
-// no-slip -> halfway bounce-back, f_i = f*_opp(i) of the cell itself;
-// free-slip on every crossed face -> specular reflection, f_i = f*_i' of
-// the cell (x - cx, y or y - cy, z or z - cz) with the crossed components
-// of c_i negated.  Any no-slip face crossed wins at an edge.
+// Pull of a cell with some source beyond a y / z wall (rare: cells next to
+// walled faces), a separate branch so the common path stays the plain one.
 template <class T>
-__device__ __forceinline__ double wall_pull(const T* __restrict__ src, const Geom& g,
-                                            const PullSrc& s, int x, int y, int z, int i, int a,
-                                            int b, int c) {
-    const bool yo = !s.yok[b], zo = !s.zok[c];
-    if ((yo && s.ywall[b] == 1) || (zo && s.zwall[c] == 1))
-        return ld_pop(src + buf_index(g, x + 1, 26 - i, y, z));
-    const int cx = a - 1, cy = b - 1, cz = c - 1;
-    const int ip = (cx + 1) * 9 + ((yo ? -cy : cy) + 1) * 3 + ((zo ? -cz : cz) + 1);
-    if (s.xkind[a] == 1) return g.feq_in[ip];
-    if (s.xkind[a] == 2) return 0.0;
-    const int ys = yo ? y : (int)(s.yoff[b] / g.zp);
-    const int zsrc = zo ? z : s.zs[c];
-    return ld_pop(src + s.xoff[a] + (int64_t)ip * g.dir_stride + (int64_t)ys * g.zp + zsrc);
+__device__ __forceinline__ void load_cell_walls(const T* __restrict__ src, const Geom& g,
+                                             const PullSrc& s, int x, int y, int z,
+                                             double (&f)[27]) {
+#pragma unroll
+    for (int i = 0; i < 27; ++i) {
+        const int a = cx_of(i) + 1, b = cy_of(i) + 1, c = cz_of(i) + 1;
+        const bool yo = !s.yok[b], zo = !s.zok[c];
+        const bool out = yo || zo;
+        const bool wall = out && !(yo && s.ywall[b] == 0) && !(zo && s.zwall[c] == 0);
+        const bool noslip = wall && ((yo && s.ywall[b] == 1) || (zo && s.zwall[c] == 1));
+        const bool mirror = wall && !noslip;
+        // free-slip: the crossed components of c_i negated
+        const int iy = (a * 3 + (2 - b)) * 3 + c, iz = (a * 3 + b) * 3 + (2 - c);
+        const int iyz = (a * 3 + (2 - b)) * 3 + (2 - c);
+        const int ip = !mirror ? i : (yo && zo ? iyz : (yo ? iy : iz));
+        const int xk = s.xkind[a];
+        const bool is_const = !noslip && (xk == 1 || xk == 2 || (out && !wall));
+        const double feq =
+            !mirror ? g.feq_in[i] : (yo && zo ? g.feq_in[iyz] : (yo ? g.feq_in[iy] : g.feq_in[iz]));
+        const double cval = xk == 1 ? feq : 0.0;
+        const T* p = noslip ? src + buf_index(g, x + 1, 26 - i, y, z)
+                            : src + s.xoff[a] + (int64_t)ip * g.dir_stride +
+                                  ((mirror && yo) ? y * g.zp : s.yoff[b]) +
+                                  ((mirror && zo) ? z : s.zs[c]);
+        const double v = ld_pop(is_const ? src : p);
+        f[i] = is_const ? cval : v;
+    }
 }
 
 template <bool PULL, class T>
@@ -148,21 +162,23 @@ __device__ __forceinline__ void load_cell(const T* __restrict__ src, const Geom&
     } else {
         PullSrc s;
         make_pull(g, x, y, z, s);
+        if (s.any_wall) {
+            load_cell_walls(src, g, s, x, y, z, f);
+            return;
+        }
+        // Every direction's source is selected without branches and all 27
+        // loads are issued back to back (a constant -- inflow equilibrium or
+        // a zero ghost -- loads a harmless dummy and is selected after).
 #pragma unroll
         for (int i = 0; i < 27; ++i) {
             const int a = cx_of(i) + 1, b = cy_of(i) + 1, c = cz_of(i) + 1;
             const bool out = !s.yok[b] || !s.zok[c];
-            const bool wall = out && !(!s.yok[b] && s.ywall[b] == 0) &&
-                              !(!s.zok[c] && s.zwall[c] == 0);
-            if (wall) {
-                f[i] = wall_pull(src, g, s, x, y, z, i, a, b, c);
-            } else if (s.xkind[a] == 1) {
-                f[i] = g.feq_in[i];
-            } else if (s.xkind[a] == 2 || out) {
-                f[i] = 0.0;
-            } else {
-                f[i] = ld_pop(src + s.xoff[a] + (int64_t)i * g.dir_stride + s.yoff[b] + s.zs[c]);
-            }
+            const int xk = s.xkind[a];
+            const bool is_const = xk == 1 || xk == 2 || out;
+            const double cval = xk == 1 ? g.feq_in[i] : 0.0;
+            const T* p = src + s.xoff[a] + (int64_t)i * g.dir_stride + s.yoff[b] + s.zs[c];
+            const double v = ld_pop(is_const ? src : p);
+            f[i] = is_const ? cval : v;
         }
     }
 }
@@ -208,11 +224,11 @@ __device__ __forceinline__ void load_cell_simple(const T* __restrict__ src, cons
 // the points whose 3x3x3 support holds the cell, in ascending id, each
 // adding ((wx*wy)*wz)*F_lat; with float storage every addition is rounded
 // as `+=` on the reference's float32 force array rounds it.
-template <class T>
-__device__ __forceinline__ void actuator_force(const ForceView& fv, int64_t xg, int y, int z,
-                                            double& Fx, double& Fy, double& Fz) {
+template <class T, int KW>
+__device__ __forceinline__ void actuator_force_k(const ForceView& fv, int64_t xg, int y, int z,
+                                              double& Fx, double& Fy, double& Fz) {
     double F[3] = {0.0, 0.0, 0.0};
-    const int kw = fv.kw;
+    const int kw = KW > 0 ? KW : fv.kw;   // 3 (Roma) unrolled, else the run's width
     for (int p = 0; p < fv.npts; ++p) {
         const int32_t* dc = fv.dep_cell + (int64_t)p * 3 * kw;
         const double* dw = fv.dep_w + (int64_t)p * 3 * kw;
@@ -236,6 +252,13 @@ __device__ __forceinline__ void actuator_force(const ForceView& fv, int64_t xg, 
     Fx = F[0];
     Fy = F[1];
     Fz = F[2];
+}
+
+template <class T>
+__device__ __forceinline__ void actuator_force(const ForceView& fv, int64_t xg, int y, int z,
+                                            double& Fx, double& Fy, double& Fz) {
+    if (fv.kw == 3) actuator_force_k<T, 3>(fv, xg, y, z, Fx, Fy, Fz);
+    else actuator_force_k<T, 0>(fv, xg, y, z, Fx, Fy, Fz);
 }
 
 // force of cell (x,y,z) given its row's key (ForceView)
