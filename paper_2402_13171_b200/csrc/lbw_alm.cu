@@ -1405,13 +1405,15 @@ int alm_launch(lbw_domain* d, int64_t m) {
                                       ? reinterpret_cast<int32_t*>(d->nb_cube[side] + tags) + toff
                                       : nullptr;
         }
-        // epochs are step-based, so a re-launched chain (after a state
-        // change) writes and waits for the same values on every rank
-        cube.epoch = (int32_t)(m + 1);
+        // epochs count this domain's chain launches: a chain re-launched
+        // after a state change (collective on every rank, as SlabSimulation's
+        // calls are) waits for the neighbours' re-launch, not their first
+        // launch of the same step, whose cube values may be stale
+        cube.epoch = (int32_t)(d->alm_launches + 1);
         k_alm_points<<<blocks, threads, pts_smem, st>>>(a, g, md, fs, 1, cube);
         count_launch();
         LBW_CK(cudaGetLastError());
-        const uint32_t epoch = (uint32_t)(m + 1);
+        const uint32_t epoch = (uint32_t)(d->alm_launches + 1);
         int rc = peer_signal(d, st, 1, epoch);
         if (!rc) rc = peer_wait(d, st, 1, epoch);
         if (rc) return rc;

@@ -146,7 +146,9 @@ def output_case(world, nx):
                 for f in names]
         ok = len(names) > 6 and all(same) and os.path.exists(os.path.join(multi, "report.json"))
         print(f"[output-files] world={world} {'OK' if ok else 'MISMATCH'} "
-              f"{sum(same)}/{len(names)} identical", flush=True)
+              f"{sum(same)}/{len(names)} identical"
+              + ("" if ok else f" differ: {[n for n, e in zip(names, same) if not e]}"),
+              flush=True)
     flag = torch.tensor([0 if ok else 1])
     dist.broadcast(flag, 0)
     return flag.item() == 0
