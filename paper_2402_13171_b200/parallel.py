@@ -112,6 +112,26 @@ class SlabSimulation(Simulation):
         _dist().all_gather_object(parts, mine, group=self._group)
         return np.concatenate(parts, axis=0) if self.rank == root else None
 
+    def close(self):
+        """Free this slab once every rank has finished its work: the
+        neighbours' sweeps store into this slab's ghost planes (and read
+        nothing after their own completion), so no rank frees memory a
+        neighbour may still write."""
+        if getattr(self, "_domain", None):
+            try:
+                _lib.load().lbw_domain_sync(self._domain)
+                _dist().barrier(group=self._group)
+            except Exception:
+                pass
+        super().close()
+
+    def __del__(self):
+        # no collective from a finaliser: the other ranks may be gone
+        try:
+            Simulation.close(self)
+        except Exception:
+            pass
+
     # ------------------------------------------------------------ output
     def _probe_tick(self):
         """Output tick of the whole lattice (output.py:33-167): the slabs'
