@@ -187,3 +187,40 @@ def test_topology_cycle_and_parent_errors():
                                        {"name": "c", "parent": "b"}]})
     with pytest.raises(ConfigError, match="unknown parent"):
         build_topology({"components": [{"name": "a"}, {"name": "b", "parent": "zz"}]})
+
+
+def test_extension_config_keys_validate():
+    """run.walls / run.spreading / run.precision (extensions and the
+    reference's single precision) parse, echo and reject bad values."""
+    from paper_2402_13171_b200 import ConfigError, parse_config
+    base = {"domain": {"cells": [8, 8, 8], "periodicity": [True, False, False]},
+            "fluid": {"kinematic_viscosity": 0.1, "wind": [0, 0, 0], "reference_velocity": 1.0},
+            "resolution": {"mach": 0.1}}
+    cfg = parse_config(dict(base, run={"walls": {"y_lo": "no_slip", "z_hi": "free_slip"},
+                                       "spreading": {"kernel": "gaussian", "epsilon": 1.5},
+                                       "precision": "single"}))
+    assert cfg.wall_codes() == (1, 0, 0, 2)
+    assert cfg.echo()["run"]["walls"] == {"y_lo": "no_slip", "z_hi": "free_slip"}
+    assert cfg.echo()["run"]["spreading"] == {"kernel": "gaussian", "epsilon": 1.5}
+    for bad in ({"walls": {"x_lo": "no_slip"}}, {"walls": {"y_lo": "sticky"}},
+                {"spreading": {"kernel": "gaussian"}},
+                {"spreading": {"kernel": "gaussian", "epsilon": 3.0}},
+                {"spreading": {"kernel": "tophat"}}):
+        with pytest.raises(ConfigError):
+            parse_config(dict(base, run=bad))
+    periodic = dict(base, domain={"cells": [8, 8, 8]})
+    with pytest.raises(ConfigError):
+        parse_config(dict(periodic, run={"walls": {"y_lo": "no_slip"}}))
+
+
+def test_oracle_gaussian_weights_normalised_and_roma_unchanged():
+    from oracle import oracle as orc
+    for x in (3.2, 7.5, 10.01):
+        cw = orc.axis_weights(x, "gaussian", 1.3)
+        assert abs(sum(w for _, w in cw) - 1.0) < 1e-15
+        assert all(abs(x - (c + 0.5)) <= 3.9 + 1e-12 for c, _ in cw)
+        # centred on the point up to the 3-eps truncation (exp(-9) tails)
+        assert abs(sum(w * (c + 0.5) for c, w in cw) - x) < 1e-3
+        roma = orc.axis_weights(x, "roma")
+        assert [c for c, _ in roma] == [int(np.floor(x)) - 1 + q for q in range(3)]
+        assert abs(sum(w for _, w in roma) - 1.0) < 1e-15
