@@ -24,6 +24,7 @@
 //                          float atomics.  CTA 0 also clears the other force
 //                          set (last read by this step's K4) for the next step.
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -101,6 +102,8 @@ struct KinDev {
     double* spin_hist;   // (3, nc, 9): spin state of step j in slot j % 3
     double* cs_hist;     // (3, nc, kCS)
     int32_t hist_slot;
+    int32_t* box;           // (2): x planes this step's chain reads / writes (gate)
+    int32_t box_halo;       // spreading half-width + 2
     int32_t stage_points;   // per-point constants fit in shared memory
     const int32_t* order;        // (nc) components by tree depth
     const int32_t* level_start;  // (nlevels+1) into order
@@ -146,6 +149,11 @@ struct AlmState {
     cudaEvent_t ev_kin_done = nullptr;
     cudaEvent_t ev_chain_done[2] = {nullptr, nullptr};  // chain of a step parity done
     int64_t kin_valid[3] = {-1, -1, -1};  // step whose kinematics kin[slot] holds
+    // sweep gate (alm_gate): chain-done flag, per-slot x range of each step's
+    // deposits and sampling, KK completion per slot
+    uint32_t* gate_flag = nullptr;
+    int32_t* gate_box = nullptr;     // (3, 2) local planes, inclusive
+    cudaEvent_t ev_kin_step[3] = {nullptr, nullptr, nullptr};
     // per-step blade-force series (lbw_alm_record_loads)
     double* h_loads = nullptr;   // pinned (loads_cap, P, 3)
     int64_t loads_cap = 0, loads_from = 0;
@@ -232,6 +240,8 @@ struct AlmState {
         k.spin_hist = k_spin_hist;
         k.cs_hist = k_cs_hist;
         k.hist_slot = 0;
+        k.box = nullptr;
+        k.box_halo = halo_x + 2;
         k.stage_points = kin_stage_points ? 1 : 0;
         k.order = k_order;
         k.level_start = k_level_start;
@@ -534,6 +544,12 @@ __device__ void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g, 
 #endif
     const int64_t dims[3] = {g.nxg, g.ny, g.nz};
     const int per[3] = {per_x, g.per_y, g.per_z};
+    __shared__ int box_lo, box_hi;
+    if (threadIdx.x == 0) {
+        box_lo = INT_MAX;
+        box_hi = INT_MIN;
+    }
+    __syncthreads();
     for (int p = threadIdx.x; p < a.n; p += blockDim.x) {
         const int c = point_comp[p];
         const double* s = cs + c * kCS;
@@ -570,11 +586,30 @@ __device__ void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g, 
             out[i] = lat;
             out[3 + i] = vel[i];
             out[15 + i] = pos[i];
+            if (i == 0 && k.box) {
+                // planes the chain reads (sampling cube + pull sources) or
+                // writes (deposit rows) for this point
+                const int64_t n0 = (int64_t)floor(lat);
+                int64_t lo = n0 - k.box_halo - g.x0, hi = n0 + k.box_halo - g.x0;
+                if (lo < 0 || hi >= g.nxl) {   // wraps or leaves the slab: gate all planes
+                    if (per_x || lo < 0) lo = 0;
+                    if (per_x || hi >= g.nxl) hi = g.nxl - 1;
+                }
+                atomicMin(&box_lo, (int)(lo < 0 ? 0 : lo));
+                atomicMax(&box_hi, (int)(hi > g.nxl - 1 ? g.nxl - 1 : hi));
+            }
         }
         if (disk) {
             for (int i = 0; i < 9; ++i) out[6 + i] = fr[i];
         } else {
             for (int f = 0; f < 3; ++f) mv3(fr, lframe + (int64_t)p * 9 + f * 3, out + 6 + 3 * f);
+        }
+    }
+    if (k.box) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            k.box[0] = box_lo;
+            k.box[1] = box_hi;
         }
     }
 #ifdef LBW_KK_PROF
@@ -1288,7 +1323,8 @@ void alm_destroy(lbw_domain* d) {
     for (void* p : s->allocs) cudaFree(p);
     for (auto& e : s->ring_ev)
         if (e) cudaEventDestroy(e);
-    for (cudaEvent_t e : {s->ev_kin_done, s->ev_chain_done[0], s->ev_chain_done[1]})
+    for (cudaEvent_t e : {s->ev_kin_done, s->ev_chain_done[0], s->ev_chain_done[1],
+                          s->ev_kin_step[0], s->ev_kin_step[1], s->ev_kin_step[2]})
         if (e) cudaEventDestroy(e);
     if (s->kin_stream) cudaStreamDestroy(s->kin_stream);
     if (s->h_ring) cudaFreeHost(s->h_ring);
@@ -1300,6 +1336,21 @@ void alm_destroy(lbw_domain* d) {
 bool alm_ready(const lbw_domain* d, int64_t m) { return d->alm->ready_step == m; }
 
 bool alm_can_prelaunch(const lbw_domain* d) { return d->prelaunch && d->alm->kin_device; }
+
+bool alm_gate(lbw_domain* d, int64_t m, const uint32_t** flag, uint32_t* value,
+              const int32_t** box, cudaEvent_t* kin_event) {
+    const AlmState* s = d->alm;
+    // only with the chain on its own SMs (the waiting CTAs cannot starve
+    // it), one slab, device kinematics, and the chain of step m queued last
+    if (!s || !s->gate_flag || !d->green_alm || d->linked || !s->kin_device ||
+        s->ready_step != m || s->kin_valid[m % 3] != m)
+        return false;
+    *flag = s->gate_flag;
+    *value = (uint32_t)d->alm_launches;
+    *box = s->gate_box + 2 * (m % 3);
+    *kin_event = s->ev_kin_step[m % 3];
+    return true;
+}
 
 ForceView alm_force_view(const lbw_domain* d, int64_t m) {
     const AlmState* s = d->alm;
@@ -1340,12 +1391,14 @@ static int kin_launch(lbw_domain* d, int64_t j) {
     const size_t ksm = s->kin_smem;
     KinDev kd = s->kdev();
     kd.hist_slot = (int32_t)(j % 3);
+    kd.box = s->gate_box ? s->gate_box + 2 * (j % 3) : nullptr;
     kd.skip_static = s->kin_static_ready ? 1 : 0;
     k_kinematics<<<1, 256, ksm, s->kin_stream>>>(kd, s->dev(j), d->g,
                                                   d->desc.periodic[0] ? 1 : 0, advance);
     count_launch();
     LBW_CK(cudaGetLastError());
     LBW_CK(cudaEventRecord(s->ev_kin_done, s->kin_stream));
+    if (s->ev_kin_step[j % 3]) LBW_CK(cudaEventRecord(s->ev_kin_step[j % 3], s->kin_stream));
     s->kin_static_ready = true;
     s->kin_state_step = j;
     s->kin_valid[j % 3] = j;
@@ -1434,6 +1487,10 @@ int alm_launch(lbw_domain* d, int64_t m) {
     count_launch();
     LBW_CK(cudaGetLastError());
     LBW_CK(cudaEventRecord(d->ev_alm_done, st));
+    if (s->gate_flag) {
+        int rc = stream_write32(st, s->gate_flag, (uint32_t)d->alm_launches);
+        if (rc) return rc;
+    }
     if (s->loads_cap > 0)
         LBW_CK(cudaMemcpyAsync(s->h_loads + (size_t)(m % s->loads_cap) * s->n * 3, a.blade,
                                (size_t)s->n * 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1741,6 +1798,20 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
         }
     }
     LBW_CK(cudaStreamSynchronize(s->kin_stream));
+    // sweep gate (alm_gate): only when the chain has SMs of its own
+    const char* ge = getenv("LBW_SWEEP_GATE");
+    if (d->green_alm && !(ge && ge[0] == '0') && !s->gate_flag) {
+        int rcg = LBW_OK;
+        auto G = [&](auto** p, size_t n) {
+            if (rcg == LBW_OK) rcg = dev_alloc(d, s, p, n);
+        };
+        G(&s->gate_flag, 1);
+        G(&s->gate_box, 6);
+        if (rcg) return rcg;
+        for (auto& e : s->ev_kin_step)
+            LBW_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        LBW_CK(cudaMemset(s->gate_flag, 0, sizeof(uint32_t)));
+    }
     s->nc = C;
     s->k_dx = kd->dx;
     s->kin_device = true;

@@ -615,6 +615,9 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
     LBW_CK(cudaSetDevice(d->device));
     for (int32_t s = 0; s < nsteps; ++s) {
         ForceView fv = d->user_active ? d->user.view(0) : ForceView{nullptr, nullptr, 0};
+        const uint32_t* gate_flag = nullptr;
+        const int32_t* gate_box = nullptr;
+        uint32_t gate_value = 0;
         // neighbours must have finished the previous sweep: it filled our
         // ghost planes and stopped reading theirs (which we overwrite now)
         {
@@ -640,7 +643,20 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
                 int rc = alm_launch(d, d->step);
                 if (rc) return rc;
             }
-            LBW_CK(cudaStreamWaitEvent(d->stream, d->ev_alm_done, 0));
+            const uint32_t* gflag = nullptr;
+            const int32_t* gbox = nullptr;
+            uint32_t gvalue = 0;
+            cudaEvent_t kev = nullptr;
+            if (alm_gate(d, d->step, &gflag, &gvalue, &gbox, &kev)) {
+                // the sweep starts right away; its CTAs in the chain's x range
+                // wait in-kernel for the chain (needs this step's x range)
+                LBW_CK(cudaStreamWaitEvent(d->stream, kev, 0));
+                gate_flag = gflag;
+                gate_box = gbox;
+                gate_value = gvalue;
+            } else {
+                LBW_CK(cudaStreamWaitEvent(d->stream, d->ev_alm_done, 0));
+            }
             fv = alm_force_view(d, d->step);
         }
         SweepArgs a;
@@ -654,6 +670,9 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
         a.nan_key = d->d_nan;
         a.step = d->step;
         a.halo = d->halo[1 - d->cur];
+        a.gate_flag = gate_flag;
+        a.gate_box = gate_box;
+        a.gate_value = gate_value;
         if (d->linked) {
             // the sweep itself tells the neighbours when its edge planes
             // (halo stores included) are done: flag value = sweeps completed

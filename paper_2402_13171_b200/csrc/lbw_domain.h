@@ -122,6 +122,11 @@ int alm_launch(lbw_domain* d, int64_t m);
 // Step m's chain already queued and still valid?
 bool alm_ready(const lbw_domain* d, int64_t m);
 bool alm_can_prelaunch(const lbw_domain* d);
+// Sweep m may start before the chain of step m finishes: CTAs of planes in
+// the chain's x range wait in-kernel for its completion flag (single slab,
+// device kinematics, chain on its own SMs).  Fills the gate arguments.
+bool alm_gate(lbw_domain* d, int64_t m, const uint32_t** flag, uint32_t* value,
+              const int32_t** box, cudaEvent_t* kin_event);
 ForceView alm_force_view(const lbw_domain* d, int64_t m);
 // Wait for queued actuator work and forget any prelaunched step (the
 // caller is about to change state it reads).
@@ -136,6 +141,7 @@ double* alm_cube(const lbw_domain* d);
 // (stream memory operations on flags in peer memory; no host round trip)
 int peer_wait(lbw_domain* d, cudaStream_t s, int which, uint32_t value);    // which 0: sweeps, 1: cube
 int peer_signal(lbw_domain* d, cudaStream_t s, int which, uint32_t value);
+int stream_write32(cudaStream_t s, uint32_t* ptr, uint32_t value);   // GPU front-end write
 void peer_close(lbw_domain* d);
 int ensure_stage(lbw_domain* d, size_t bytes);
 

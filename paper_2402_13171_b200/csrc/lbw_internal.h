@@ -100,6 +100,11 @@ struct SweepArgs {
     unsigned long long* nan_key;
     int64_t step;
     HaloOut halo;
+    // optional gate: CTAs of planes in [gate_box[0], gate_box[1]] wait until
+    // *gate_flag >= gate_value (the actuator chain of this step is done)
+    const uint32_t* gate_flag;
+    const int32_t* gate_box;
+    uint32_t gate_value;
 };
 
 // exact flavour (lbw_kernels_exact.cu, -fmad=false)

@@ -69,6 +69,17 @@ int peer_wait(lbw_domain* d, cudaStream_t s, int which, uint32_t value) {
     return LBW_OK;
 }
 
+int stream_write32(cudaStream_t s, uint32_t* ptr, uint32_t value) {
+    int rc = driver_entry_points();
+    if (rc) return rc;
+    const CUresult r = g_write((CUstream)s, (CUdeviceptr)ptr, value, 0);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuStreamWriteValue32 failed (" + std::to_string((int)r) + ")");
+        return LBW_ECOMM;
+    }
+    return LBW_OK;
+}
+
 int peer_signal(lbw_domain* d, cudaStream_t s, int which, uint32_t value) {
     if (!d->linked) return LBW_OK;
     for (int side = 0; side < 2; ++side) {

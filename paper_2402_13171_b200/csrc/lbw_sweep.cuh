@@ -375,6 +375,19 @@ __device__ __forceinline__ void sweep_cell(const SweepArgs& a, int x, int y, int
     }
 }
 
+// In-kernel wait for the actuator chain of this step (see SweepArgs gate):
+// bounded, so a lost signal traps instead of hanging the GPU.
+__device__ __forceinline__ void gate_wait(const uint32_t* flag, uint32_t value) {
+    long long n = 0;
+    while (true) {
+        uint32_t v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if (v >= value) break;
+        __nanosleep(128);
+        if (++n > 20000000LL) __trap();
+    }
+}
+
 // K1: fused pull-stream + collide (+Guo) over local planes [x_begin, x_end).
 // One thread per cell, z fastest.  PULL=false collides the stored state in
 // place position (first step after an upload of pre-collision data).
@@ -388,6 +401,12 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) k_sweep(SweepArgs a) {
     const int bz = (int)blockIdx.z;
     const int x = a.x_begin + (bz == 0 ? 0 : (bz == 1 ? g.nxl - 1 : bz - 1));
     const bool edge = bz < 2 && a.halo.edge_counter != nullptr;
+    if (a.gate_flag != nullptr) {   // uniform per CTA
+        if (x >= a.gate_box[0] && x <= a.gate_box[1]) {
+            if (threadIdx.x == 0 && threadIdx.y == 0) gate_wait(a.gate_flag, a.gate_value);
+            __syncthreads();
+        }
+    }
     LBW_TRACE_BEGIN(0, a.step);
     if (z < g.nz && y < g.ny) sweep_cell<OP, PULL, T>(a, x, y, z);
     if (edge) edge_done(a.halo);  // whole CTA, uniform branch
