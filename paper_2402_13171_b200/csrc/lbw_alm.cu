@@ -960,6 +960,9 @@ struct PointInputs {
     double kv;
     PointStatic ps;
     bool disk;
+#ifdef LBW_K4_PROF
+    long long t0, t1;
+#endif
 };
 __device__ __forceinline__ PointInputs load_point_inputs(const AlmDev& a, int p, int lane) {
     PointInputs in;
@@ -976,6 +979,9 @@ __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, co
     const bool disk = in.disk;
     double kr[15];
     for (int k = 0; k < 15; ++k) kr[k] = __shfl_sync(0xffffffffu, in.kv, k);
+#ifdef LBW_K4_PROF
+    const long long t2 = clock64();   // kinematics row available
+#endif
     const double* kin = kr;
     // deposit cells / Roma weights per axis (lanes 8..10), kept in registers
     // for the row tags below and stored for the sweep / fill / next sample
@@ -1029,6 +1035,9 @@ __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, co
     }
     if (phase == 1) return;
     const bool complete = __all_sync(0xffffffffu, have);
+#ifdef LBW_K4_PROF
+    const long long t3 = clock64();   // cube macro done
+#endif
     // lane 0: trilinear sum in (dx,dy,dz) lexicographic order (actuator.py:88-92)
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int c = 0; c < 8; ++c) {
@@ -1078,6 +1087,12 @@ __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, co
     }
     double blade[3] = {0.0, 0.0, 0.0};
     if (relevant && !disk) blade_force_warp(a, ps, kin, acc, blade, lane);
+#ifdef LBW_K4_PROF
+    const long long t4 = clock64();
+    if (lane == 0 && p == 0 && (a.step % 50) == 0)
+        printf("K4PROF step %lld inputs+stage %lld kin %lld cube %lld blade %lld\n", (long long)a.step,
+               in.t1 - in.t0, t2 - in.t1, t3 - t2, t4 - t3);
+#endif
     if (lane == 0) {
         for (int q = 0; q < 4; ++q) a.samples[p * 4 + q] = owner ? acc[q] : 0.0;
         for (int c = 0; c < 3; ++c) {
@@ -1104,6 +1119,9 @@ __global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s, int phase
     // latency overlaps the staging below
     const int lane = threadIdx.x & 31;
     PointInputs in{};
+#ifdef LBW_K4_PROF
+    const long long t0 = clock64();
+#endif
     if (p < a.n) in = load_point_inputs(a, p, lane);
     const ForceView& fv = m.fv;
     if (fv.row_key != nullptr && fv.pool == nullptr && fv.npts > 0 && fv.npts <= kOnTheFlyMaxPoints &&
@@ -1123,6 +1141,10 @@ __global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s, int phase
         m.fv.dep_cell = dc;
     }
     if (p >= a.n) return;  // uniform per warp
+#ifdef LBW_K4_PROF
+    in.t0 = t0;
+    in.t1 = clock64();
+#endif
     point_warp(a, g, m, s, phase, cube, p, lane, in);
     LBW_TRACE_END(2, a.step);
 }
