@@ -224,3 +224,14 @@ def test_oracle_gaussian_weights_normalised_and_roma_unchanged():
         roma = orc.axis_weights(x, "roma")
         assert [c for c, _ in roma] == [int(np.floor(x)) - 1 + q for q in range(3)]
         assert abs(sum(w for _, w in roma) - 1.0) < 1e-15
+
+
+@pytest.mark.gpu
+def test_standalone_abi_example(gpu):
+    """examples/abi_minimal.py: the ABI bound with plain ctypes (no package)."""
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "examples", "abi_minimal.py")],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "energy decay rate" in r.stdout
