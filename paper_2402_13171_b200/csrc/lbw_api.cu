@@ -262,6 +262,8 @@ int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out) {
         // (diagnostics: the serial chain + sweep time)
         const char* e = getenv("LBW_PRELAUNCH");
         d->prelaunch = !(e && e[0] == '0');
+        const char* alt = getenv("LBW_SWEEP_ALT");   // 0 disables (A/B)
+        d->sweep_alt = !(alt && alt[0] == '0');
     }
     d->device = s.device;
     if (cudaSetDevice(d->device) != cudaSuccess) {
@@ -669,6 +671,7 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
         a.x_end = d->g.nxl;
         a.nan_key = d->d_nan;
         a.step = d->step;
+        a.reverse = (d->sweep_alt && (d->step & 1)) ? 1 : 0;
         a.halo = d->halo[1 - d->cur];
         a.gate_flag = gate_flag;
         a.gate_box = gate_box;

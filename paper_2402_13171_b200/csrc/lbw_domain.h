@@ -93,6 +93,7 @@ struct lbw_domain {
     cudaEvent_t ev_ready = nullptr;   // main stream passed the neighbour waits of a step
     cudaEvent_t ev_ready_prev = nullptr;  // ... of the step before
     bool touched = true;              // state changed by a call since the last step
+    bool sweep_alt = true;            // alternate the interior plane order (LBW_SWEEP_ALT)
     // x-slab neighbours (lbw_peer.cu): side 0 = lo (x-1), side 1 = hi (x+1)
     bool linked = false;
     int nb_rank[2] = {-1, -1};

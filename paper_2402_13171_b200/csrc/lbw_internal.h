@@ -105,6 +105,7 @@ struct SweepArgs {
     const uint32_t* gate_flag;
     const int32_t* gate_box;
     uint32_t gate_value;
+    int32_t reverse;   // interior planes in descending x (alternate steps)
 };
 
 // exact flavour (lbw_kernels_exact.cu, -fmad=false)

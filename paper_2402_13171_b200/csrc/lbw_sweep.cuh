@@ -399,7 +399,11 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) k_sweep(SweepArgs a) {
     // the two edge planes come first in dispatch order so their halo stores
     // (and the completion signal) are issued at the start of the sweep
     const int bz = (int)blockIdx.z;
-    const int x = a.x_begin + (bz == 0 ? 0 : (bz == 1 ? g.nxl - 1 : bz - 1));
+    // edge planes first; the interior ascending or, on alternate steps,
+    // descending x, so a sweep starts on the planes the previous one wrote
+    // last (still in L2)
+    const int xi = a.reverse ? g.nxl - bz : bz - 1;
+    const int x = a.x_begin + (bz == 0 ? 0 : (bz == 1 ? g.nxl - 1 : xi));
     const bool edge = bz < 2 && a.halo.edge_counter != nullptr;
     if (a.gate_flag != nullptr) {   // uniform per CTA
         if (x >= a.gate_box[0] && x <= a.gate_box[1]) {
