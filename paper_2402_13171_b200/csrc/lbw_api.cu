@@ -207,8 +207,7 @@ static void free_domain(lbw_domain* d) {
     if (d->stage) cudaFree(d->stage);
     for (cudaEvent_t ev : d->ev_pool) cudaEventDestroy(ev);
     peer_close(d);
-    for (cudaEvent_t ev : {d->ev_main, d->ev_ready, d->ev_ready_prev, d->ev_alm_done,
-                           d->ev_sweep[0], d->ev_sweep[1]})
+    for (cudaEvent_t ev : {d->ev_main, d->ev_ready, d->ev_ready_prev, d->ev_alm_done})
         if (ev) cudaEventDestroy(ev);
     green_release(d);
     if (d->alm_stream) cudaStreamDestroy(d->alm_stream);
@@ -319,9 +318,7 @@ int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out) {
         cudaEventCreateWithFlags(&d->ev_main, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&d->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&d->ev_ready_prev, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&d->ev_alm_done, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&d->ev_sweep[0], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&d->ev_sweep[1], cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&d->ev_alm_done, cudaEventDisableTiming) != cudaSuccess) {
         cudaGetLastError();
         free_domain(d);
         set_error("stream/event creation failed");
@@ -708,7 +705,6 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
         d->msrc.fv = fv;
         d->last_fv = fv;
         d->shown_fv = fv;
-        LBW_CK(cudaEventRecord(d->ev_sweep[d->step & 1], d->stream));
         d->touched = false;
         d->cur = 1 - d->cur;
         d->state_pre = false;

@@ -87,7 +87,7 @@ struct lbw_domain {
     void* green_sweep = nullptr;
     void* green_alm = nullptr;
     int alm_sms = 0;
-    cudaEvent_t ev_main = nullptr, ev_alm_done = nullptr, ev_sweep[2] = {nullptr, nullptr};
+    cudaEvent_t ev_main = nullptr, ev_alm_done = nullptr;
     int64_t steps_done = 0;   // sweeps executed in this domain's lifetime
     bool prelaunch = true;
     cudaEvent_t ev_ready = nullptr;   // main stream passed the neighbour waits of a step

@@ -16,6 +16,7 @@ from tests.scenarios import write_rotor_files
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 arith = sys.argv[2] if len(sys.argv) > 2 else "fast"
+turbine = not (len(sys.argv) > 3 and sys.argv[3] == "none")
 tmp = tempfile.mkdtemp()
 write_rotor_files(tmp)
 raw = {"domain": {"cells": [n, n, n]},
@@ -24,6 +25,8 @@ raw = {"domain": {"cells": [n, n, n]},
        "run": {"arithmetic": arith, "collision": {"operator": "cumulant"}},
        "turbines": [{"file": "rotor.yaml", "position": [1.0, 1.0, 0.2]}],
        "polars": [{"id": "sym", "file": "sym.csv"}]}
+if not turbine:
+    del raw["turbines"], raw["polars"]
 sim = Simulation(parse_config(raw, base_dir=tmp))
 lib = _lib.load()
 sim.advance(40)
@@ -31,7 +34,7 @@ sim.synchronize()
 for tu in ("fast", "alm"):
     getattr(lib, f"lbw_trace_reset_{tu}")()
 s0 = sim.step_index
-sim.advance(12)
+sim.advance(40)
 sim.synchronize()
 tabs = {}
 for tu in ("fast", "alm"):
@@ -41,7 +44,20 @@ for tu in ("fast", "alm"):
 t0 = int(tabs["fast"][0, s0 & 63, 0])
 names = [("fast", 0, "sweep"), ("alm", 1, "KK"), ("alm", 2, "K4"), ("alm", 4, "K5")]
 print("step  " + "  ".join(f"{nm:>17s}" for _, _, nm in names))
-for st in range(s0, s0 + 12):
+spans = {nm: [] for _, _, nm in names}
+for st in range(s0, s0 + 40):
+    for tu, kid, nm in names:
+        b, e = tabs[tu][kid, st & 63]
+        if not (b == np.uint64(~np.uint64(0)) or e == 0):
+            spans[nm].append((int(b), int(e), st))
+for nm, sp in spans.items():
+    if len(sp) > 2:
+        dur = np.mean([e - b for b, e, _ in sp[2:]]) / 1e3
+        gap = np.mean([sp[i][0] - sp[i - 1][1] for i in range(2, len(sp))]) / 1e3
+        per = (sp[-1][0] - sp[2][0]) / (len(sp) - 3) / 1e3
+        print(f"{nm:6s} mean duration {dur:6.2f} us, gap after the previous {gap:6.2f} us, "
+              f"period {per:6.2f} us")
+for st in range(s0 + 28, s0 + 40):
     cols = []
     for tu, kid, nm in names:
         b, e = tabs[tu][kid, st & 63]
