@@ -10,6 +10,7 @@ from tests.scenarios import write_rotor_files
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 arith = sys.argv[2] if len(sys.argv) > 2 else "fast"
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 300
+alone = len(sys.argv) > 4 and sys.argv[4] == "alone"   # synchronize after every step
 tmp = tempfile.mkdtemp()
 write_rotor_files(tmp)
 raw = {"domain": {"cells": [n, n, n]},
@@ -19,6 +20,11 @@ raw = {"domain": {"cells": [n, n, n]},
        "turbines": [{"file": "rotor.yaml", "position": [1.0, 1.0, 0.2]}],
        "polars": [{"id": "sym", "file": "sym.csv"}]}
 sim = Simulation(parse_config(raw, base_dir=tmp))
-sim.advance(steps)
-sim.synchronize()
+if alone:
+    for _ in range(steps):
+        sim.step()
+        sim.synchronize()
+else:
+    sim.advance(steps)
+    sim.synchronize()
 sim.close()
