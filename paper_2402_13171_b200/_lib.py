@@ -10,9 +10,7 @@ import ctypes
 import os
 import threading
 
-import numpy as np
-
-from .errors import ConfigError, NumericalAbort
+from .errors import ConfigError
 
 LIB_PATH = os.environ.get("LBW_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "liblbw.so")   # LBW_LIB: A/B builds of the library

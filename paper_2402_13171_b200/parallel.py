@@ -25,7 +25,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from .errors import ConfigError, NumericalAbort
+from .errors import NumericalAbort
 from .sim import SlabGrid, Simulation
 
 

@@ -14,7 +14,7 @@ import pytest
 
 from oracle import oracle as orc
 from paper_2402_13171_b200 import NumericalAbort, Simulation, parse_config
-from tests.scenarios import oracle_for, rotor_config
+from tests.scenarios import rotor_config
 
 pytestmark = pytest.mark.gpu
 
