@@ -454,11 +454,12 @@ def run_reference(args, rank, budget_s=150.0):
     cb["sample"] = (f"{n} of {args.steps} requested steps of {desc}, C oracle, "
                     f"{cb['cores']} threads")
     return {"metric": METRIC if args.precision == "double" else METRIC_SINGLE,
-            "value": round(value, 3), "unit": "MLUP/s", "n_gpus": 0,
+            "value": round(value, 3), "unit": "MLUP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * t / n, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "cells": list(cfg.cells), "parallelism": "host threads"},
+            "config": {"workload": desc, "cells": list(cfg.cells), "parallelism": "host threads",
+                       "gpus_used": 0},
             "impl": "reference", "cpu_baseline": cb,
             "e2e": {"value": round(value, 3), "unit": "MLUP/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
