@@ -170,6 +170,19 @@ def main():
     ok &= run_case("nonperiodic-yz-cumulant",
                    lambda: parse_config(lbm_raw((nx, 9, 7), (True, False, False), "periodic",
                                                 "cumulant", "fast")), 6, True)
+    # walls on every y / z face (extension): bounce-back / specular sources
+    # next to the slab faces
+    def walls_cfg():
+        raw = lbm_raw((nx + 1, 9, 8), (False, False, False), "velocity_inflow_outflow",
+                      "cumulant", "exact")
+        raw["run"]["walls"] = {"y_lo": "no_slip", "y_hi": "free_slip", "z_lo": "free_slip",
+                               "z_hi": "no_slip"}
+        return parse_config(raw)
+    ok &= run_case("walls-inflow-cumulant", walls_cfg, 8, True)
+    # fp32 storage: float ghost planes across the slab faces
+    ok &= run_case("rotor-single",
+                   lambda: rotor_config(cells=(nx, 12, 12), position=(1.5, 0.3, 0.0),
+                                        arithmetic="exact", precision="single")[0], 8, False)
     # rotor plane at x = 11.6 cells: sampling cubes and Roma supports straddle
     # the face between slabs 0 and 1; blades cross the periodic y face too
     for arith, kin in (("exact", "host"), ("fast", "device")):
