@@ -297,7 +297,6 @@ int lbw_alm_set_kinematics(lbw_domain* d, const double* kin);
  * sampled rho (P,), sampled u lattice (P,3), blade force N (P,3).  Blocks
  * until that step's ALM kernels finished. */
 int lbw_alm_get(lbw_domain* d, double* rho, double* u, double* blade_force);
-/* 1 once any polar lookup clamped alpha (polars.py:68-77 warn-once). */
 /* Thrust / power time series without synchronising the step loop: every
  * step's blade forces (P x 3) are copied device->host into a pinned ring of
  * `capacity` steps owned by the domain (0 disables).  read: waits for and
@@ -306,6 +305,7 @@ int lbw_alm_get(lbw_domain* d, double* rho, double* u, double* blade_force);
 int lbw_alm_record_loads(lbw_domain* d, int64_t capacity);
 int lbw_alm_read_loads(lbw_domain* d, double* out, int64_t max_steps, int64_t* first_step,
                        int64_t* n);
+/* 1 once any polar lookup clamped alpha (polars.py:68-77 warn-once). */
 int lbw_alm_clamp_flags(lbw_domain* d, int32_t* per_polar);
 
 /* ---------------------------------------------------------------- multi-GPU
