@@ -408,7 +408,9 @@ def cpu_baseline(args, budget_s=20.0):
     from oracle import oracle as orc
     orc.build()
     cores = len(os.sched_getaffinity(0))
-    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    # every host thread, whatever OMP_NUM_THREADS a launcher set (torchrun
+    # sets 1 for each rank; only rank 0 runs this arm)
+    orc.set_threads(cores)
     tmp = tempfile.TemporaryDirectory()
     cfg, desc = make_config(_host_sample_config(args.config), 1, "exact", tmp.name,
                             args.precision)

@@ -59,11 +59,18 @@ def lib():
         L.orc_fill_ghosts.argtypes = [vp, i64, i64, i64, ctypes.c_int, vp]
         L.orc_apply_walls.argtypes = [vp, i64, i64, i64, vp, vp]
         L.orc_apply_inflow_outflow.argtypes = [vp, i64, i64, i64, vp]
+        L.orc_set_threads.argtypes = [ctypes.c_int]
+        L.orc_set_threads.restype = None
         for fn in (L.orc_collide_batch, L.orc_collide_block, L.orc_moments_block,
                    L.orc_stream_pull_block, L.orc_fill_ghosts, L.orc_apply_inflow_outflow):
             fn.restype = None
         _lib = L
     return _lib
+
+
+def set_threads(n):
+    """OpenMP threads of the oracle's loops (the CPU-baseline timing leg)."""
+    lib().orc_set_threads(int(n))
 
 
 def _p(a):
