@@ -240,6 +240,30 @@ def test_bench_size_rotor_momentum_budget(gpu):
     tmp.cleanup()
 
 
+def test_bench_config_deterministic_and_round_trip(gpu):
+    """The benchmark configuration itself (C2: 256x128x128, inflow /
+    outflow, rotor, fast arithmetic): two runs are bit-identical (no
+    float atomics anywhere in the step), and the state round-trips through
+    upload / download unchanged."""
+    cfg, tmp = rotor_config(cells=(256, 128, 128), periodic=(False, True, True),
+                            boundary="velocity_inflow_outflow", position=(2.0, 2.0, 1.2),
+                            arithmetic="fast", cpd=32, nu=0.1732, mach=0.05)
+    runs = []
+    for _ in range(2):
+        sim = Simulation(cfg)
+        sim.advance(6)
+        runs.append((sim.fields[0].interior, sim.fields[0].interior_force,
+                     sim._alm_results()[2]))
+        sim.close()
+    for a, b in zip(*runs):
+        assert np.array_equal(a, b)
+    sim = Simulation(cfg)
+    sim.fields[0].interior = runs[0][0]
+    assert np.array_equal(sim.fields[0].interior, runs[0][0])
+    sim.close()
+    tmp.cleanup()
+
+
 # ----------------------------------------------------------- actuator line
 
 @pytest.mark.parametrize("kinematics", ["host", "device"])
