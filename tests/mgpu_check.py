@@ -209,6 +209,13 @@ def main():
     for name, yaw in (("disk-aligned", 0.0), ("disk-yawed", 35.0)):
         ok &= run_case(name, lambda yaw=yaw: disk_cfg(nx, yaw), 8, False)
     ok &= output_case(world, nx)
+    # the benchmark's weak-scaled C2 configuration itself (256 planes per
+    # GPU, rotor, inflow / outflow, fast arithmetic, device kinematics)
+    ok &= run_case("bench-c2-weak",
+                   lambda: rotor_config(cells=(256 * world, 128, 128), periodic=(False, True, True),
+                                        boundary="velocity_inflow_outflow",
+                                        position=(2.0, 2.0, 1.2), arithmetic="fast", cpd=32,
+                                        nu=0.1732, mach=0.05)[0], 6, False, kinematics="device")
     if os.environ.get("LBW_MGPU_LONG"):
         # test_acceptance.py test_04 at its size: 64^3 periodic, one rotating
         # 3-blade turbine, 200 steps (slabs of 64/world planes)
