@@ -3,6 +3,8 @@
 // instantiates only its own flavour, so the exact kernels never see a
 // contracting compiler (-fmad=false is a per-TU flag).
 #pragma once
+#include <cstdlib>
+
 #include "lbw_internal.h"
 #include "lbw_trace.cuh"
 
@@ -405,6 +407,13 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) k_sweep(SweepArgs a) {
     const int xi = a.reverse ? g.nxl - bz : bz - 1;
     const int x = a.x_begin + (bz == 0 ? 0 : (bz == 1 ? g.nxl - 1 : xi));
     const bool edge = bz < 2 && a.halo.edge_counter != nullptr;
+    // Programmatic dependent launch: when this sweep directly follows the
+    // previous one in the stream it is launched before that one finishes;
+    // nothing is read or written before the previous grid has completed and
+    // its stores are visible (no-op for an ordinary launch).  The next
+    // sweep may then be scheduled as soon as every CTA of this one runs.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (a.gate_flag != nullptr) {   // uniform per CTA
         if (x >= a.gate_box[0] && x <= a.gate_box[1]) {
             if (threadIdx.x == 0 && threadIdx.y == 0) gate_wait(a.gate_flag, a.gate_value);
@@ -464,14 +473,43 @@ inline dim3 sweep_block(const Geom& g) {
 }
 
 // launch K1 for one (operator, pull, storage) combination
+// (LBW_SWEEP_PDL=0: ordinary launches, for A/B runs)
+inline bool sweep_pdl() {
+    static const bool on = [] {
+        const char* e = getenv("LBW_SWEEP_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// one K1 launch, programmatic stream serialisation allowed (see k_sweep)
+template <int OP, bool PULL, int MINB, class T>
+void launch_k_sweep_pdl(dim3 grd, dim3 blk, const SweepArgs& b, cudaStream_t s) {
+    if (!sweep_pdl()) {
+        k_sweep<OP, PULL, MINB, T><<<grd, blk, 0, s>>>(b);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grd;
+    cfg.blockDim = blk;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_sweep<OP, PULL, MINB, T>, b);
+}
+
 template <int MINB, class T>
 void launch_k_sweep(int op, bool pull, dim3 grd, dim3 blk, const SweepArgs& b, cudaStream_t s) {
     if (op == 1) {
-        if (pull) k_sweep<1, true, MINB, T><<<grd, blk, 0, s>>>(b);
-        else k_sweep<1, false, MINB, T><<<grd, blk, 0, s>>>(b);
+        if (pull) launch_k_sweep_pdl<1, true, MINB, T>(grd, blk, b, s);
+        else launch_k_sweep_pdl<1, false, MINB, T>(grd, blk, b, s);
     } else {
-        if (pull) k_sweep<0, true, MINB, T><<<grd, blk, 0, s>>>(b);
-        else k_sweep<0, false, MINB, T><<<grd, blk, 0, s>>>(b);
+        if (pull) launch_k_sweep_pdl<0, true, MINB, T>(grd, blk, b, s);
+        else launch_k_sweep_pdl<0, false, MINB, T>(grd, blk, b, s);
     }
 }
 
