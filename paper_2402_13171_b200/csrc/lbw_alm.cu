@@ -693,10 +693,9 @@ __device__ int macro_at_raw(const Geom& g, const MacroDev& m, int64_t gx, int64_
         put(m.dense + cell * 4);
         return MA_OWNED;
     }
+    // the row key and the 27 populations are loaded together (one DRAM
+    // round trip); the force sum over the staged deposit data follows
     const uint64_t key = m.fv.row_key ? m.fv.row_key[x * g.ny + gy] : 0ull;
-    double Fx, Fy, Fz;
-    if (g.single) force_from_key<float>(m.fv, g, key, (int)x, (int)gy, (int)gz, Fx, Fy, Fz);
-    else force_from_key<double>(m.fv, g, key, (int)x, (int)gy, (int)gz, Fx, Fy, Fz);
     double f[27];
     // interior cells take the compact branch-free pull; cells at boundaries
     // (x faces, non-periodic y / z, walls) the general one, out of line so
@@ -709,6 +708,9 @@ __device__ int macro_at_raw(const Geom& g, const MacroDev& m, int64_t gx, int64_
     } else {
         load_cell_general(m.buf, g, m.pull != 0, (int)x, (int)gy, (int)gz, f);
     }
+    double Fx, Fy, Fz;
+    if (g.single) force_from_key<float>(m.fv, g, key, (int)x, (int)gy, (int)gz, Fx, Fy, Fz);
+    else force_from_key<double>(m.fv, g, key, (int)x, (int)gy, (int)gz, Fx, Fy, Fz);
     const Macro mm = moments_exact(f, Fx, Fy, Fz, 1.0);
     out[0] = mm.rho;
     out[1] = mm.ux;
@@ -1130,11 +1132,32 @@ __global__ void k_alm_points(AlmDev a, Geom g, MacroDev m, ForceSet s, int phase
         double* w = alm_sm;                                   // (n, 3, kw)
         double* fl = w + nd;                                  // (n, 3)
         int32_t* dc = reinterpret_cast<int32_t*>(fl + n * 3); // (n, 3, kw)
-        for (int i = threadIdx.x; i < nd; i += blockDim.x) {
-            w[i] = fv.dep_w[i];
-            dc[i] = fv.dep_cell[i];
+        // every load of a thread is issued before its first shared store
+        // (one DRAM round trip, not one per loop iteration)
+        constexpr int U = 8;
+        const int nb = (int)blockDim.x, n3 = n * 3;
+        for (int i0 = threadIdx.x; i0 < nd || i0 < n3; i0 += U * nb) {
+            double wv[U], flv[U];
+            int32_t cv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * nb;
+                if (i < nd) {
+                    wv[u] = fv.dep_w[i];
+                    cv[u] = fv.dep_cell[i];
+                }
+                if (i < n3) flv[u] = fv.flat[i];
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * nb;
+                if (i < nd) {
+                    w[i] = wv[u];
+                    dc[i] = cv[u];
+                }
+                if (i < n3) fl[i] = flv[u];
+            }
         }
-        for (int i = threadIdx.x; i < n * 3; i += blockDim.x) fl[i] = fv.flat[i];
         __syncthreads();
         m.fv.dep_w = w;
         m.fv.flat = fl;
