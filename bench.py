@@ -453,14 +453,18 @@ def run_reference(args, rank, budget_s=150.0):
     tmp.cleanup()
     value = cells * n / t / 1e6
     cb["value"] = round(value, 3)
-    cb["sample"] = (f"{n} of {args.steps} requested steps of {desc}, C oracle, "
-                    f"{cb['cores']} threads")
+    # the line names the workload of this launch (weak-scaled with --gpus,
+    # as the GPU arm's); the timed sample is one GPU's share of it
+    raw_full, desc_full = workload(args.config, max(1, args.gpus))
+    cb["sample"] = (f"{n} of {args.steps} requested steps of {desc} (one GPU's share of "
+                    f"{desc_full}), C oracle, {cb['cores']} threads")
     return {"metric": METRIC if args.precision == "double" else METRIC_SINGLE,
             "value": round(value, 3), "unit": "MLUP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * t / n, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "cells": list(cfg.cells), "parallelism": "host threads",
+            "config": {"workload": desc_full, "cells": list(raw_full["domain"]["cells"]),
+                       "sample_cells": list(cfg.cells), "parallelism": "host threads",
                        "gpus_used": 0},
             "impl": "reference", "cpu_baseline": cb,
             "e2e": {"value": round(value, 3), "unit": "MLUP/s", "h2d_bytes_per_step": 0,
