@@ -148,7 +148,9 @@ typedef struct lbw_domain_desc {
 
 int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out);
 int lbw_domain_destroy(lbw_domain* d);
-/* raw cudaStream_t the domain launches on (for event timing by callers) */
+/* raw cudaStream_t the domain launches on (for event timing by callers).
+ * lbw_alm_configure may replace the domain's streams (an SM partition for
+ * the actuator chain on small slabs): query the stream again after it. */
 int lbw_domain_stream(lbw_domain* d, void** stream_out);
 /* device bytes held by the domain */
 int64_t lbw_domain_device_bytes(lbw_domain* d);

@@ -1380,6 +1380,17 @@ void alm_destroy(lbw_domain* d) {
 
 bool alm_ready(const lbw_domain* d, int64_t m) { return d->alm->ready_step == m; }
 
+int alm_check_gate(lbw_domain* d) {
+    if (!alm_active(d) || !d->alm->gate_flag) return LBW_OK;
+    int32_t err = 0;
+    LBW_CK(cudaMemcpy(&err, d->alm->gate_flag + 1, sizeof(err), cudaMemcpyDeviceToHost));
+    if (err) {
+        set_error("a sweep's in-kernel wait for the actuator chain expired (results invalid)");
+        return LBW_ECUDA;
+    }
+    return LBW_OK;
+}
+
 bool alm_can_prelaunch(const lbw_domain* d) { return d->prelaunch && d->alm->kin_device; }
 
 bool alm_gate(lbw_domain* d, int64_t m, const uint32_t** flag, uint32_t* value,
@@ -1850,12 +1861,12 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
         auto G = [&](auto** p, size_t n) {
             if (rcg == LBW_OK) rcg = dev_alloc(d, s, p, n);
         };
-        G(&s->gate_flag, 1);
+        G(&s->gate_flag, 2);   // [0] chain launches done, [1] sweep wait expired
         G(&s->gate_box, 6);
         if (rcg) return rcg;
         for (auto& e : s->ev_kin_step)
             LBW_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        LBW_CK(cudaMemset(s->gate_flag, 0, sizeof(uint32_t)));
+        LBW_CK(cudaMemset(s->gate_flag, 0, 2 * sizeof(uint32_t)));
     }
     s->nc = C;
     s->k_dx = kd->dx;

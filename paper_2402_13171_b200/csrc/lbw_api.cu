@@ -673,6 +673,9 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
         a.gate_flag = gate_flag;
         a.gate_box = gate_box;
         a.gate_value = gate_value;
+        a.gate_error = gate_flag ? reinterpret_cast<int32_t*>(const_cast<uint32_t*>(gate_flag) + 1)
+                                 : nullptr;
+        a.pdl = d->linked ? 0 : 1;
         if (d->linked) {
             // the sweep itself tells the neighbours when its edge planes
             // (halo stores included) are done: flag value = sweeps completed
@@ -776,7 +779,7 @@ int lbw_domain_sync(lbw_domain* d) {
     LBW_CK(cudaSetDevice(d->device));
     LBW_CK(cudaStreamSynchronize(d->stream));
     LBW_CK(cudaStreamSynchronize(d->alm_stream));
-    return LBW_OK;
+    return alm_check_gate(d);
 }
 
 int lbw_domain_sweep_timing(lbw_domain* d, int enable) {

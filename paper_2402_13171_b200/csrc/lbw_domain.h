@@ -123,6 +123,8 @@ int alm_launch(lbw_domain* d, int64_t m);
 // Step m's chain already queued and still valid?
 bool alm_ready(const lbw_domain* d, int64_t m);
 bool alm_can_prelaunch(const lbw_domain* d);
+// LBW_ECUDA when a gated sweep's bounded wait expired (after a sync)
+int alm_check_gate(lbw_domain* d);
 // Sweep m may start before the chain of step m finishes: CTAs of planes in
 // the chain's x range wait in-kernel for its completion flag (single slab,
 // device kinematics, chain on its own SMs).  Fills the gate arguments.

@@ -60,7 +60,15 @@ const GreenApi& api() {
 
 }  // namespace
 
+// A profiler or sanitizer injected into the process (ncu, compute-sanitizer)
+// serialises kernels: no partition then, so no sweep ever waits in-kernel
+// for a chain kernel that the tool has not run yet.
+static bool tool_injected() {
+    return getenv("CUDA_INJECTION64_PATH") != nullptr;
+}
+
 int alm_sm_count(const lbw_domain* d) {
+    if (tool_injected()) return 0;
     const char* e = getenv("LBW_ALM_SMS");
     if (e) return atoi(e);
     const int64_t cells = (int64_t)d->g.nxl * d->g.ny * d->g.nz;

@@ -106,6 +106,13 @@ struct SweepArgs {
     const int32_t* gate_box;
     uint32_t gate_value;
     int32_t reverse;   // interior planes in descending x (alternate steps)
+    // programmatic dependent launch allowed: only when the previous stream
+    // operation is the preceding sweep (single slab; a linked slab has a
+    // peer-flag wait between its sweeps)
+    int32_t pdl;
+    // gate timeout: set to 1 by a CTA whose bounded wait expired (the host
+    // reports it as an error instead of the kernel trapping)
+    int32_t* gate_error;
 };
 
 // exact flavour (lbw_kernels_exact.cu, -fmad=false)

@@ -378,15 +378,19 @@ __device__ __forceinline__ void sweep_cell(const SweepArgs& a, int x, int y, int
 }
 
 // In-kernel wait for the actuator chain of this step (see SweepArgs gate):
-// bounded, so a lost signal traps instead of hanging the GPU.
-__device__ __forceinline__ void gate_wait(const uint32_t* flag, uint32_t value) {
+// bounded; an expired wait raises the gate error flag (reported by the host
+// as LBW_ECUDA) and lets the CTA finish rather than trapping the context.
+__device__ __forceinline__ void gate_wait(const uint32_t* flag, uint32_t value, int32_t* err) {
     long long n = 0;
     while (true) {
         uint32_t v;
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
         if (v >= value) break;
         __nanosleep(128);
-        if (++n > 20000000LL) __trap();
+        if (++n > 20000000LL) {
+            if (err) atomicExch(err, 1);
+            break;
+        }
     }
 }
 
@@ -416,7 +420,7 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) k_sweep(SweepArgs a) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (a.gate_flag != nullptr) {   // uniform per CTA
         if (x >= a.gate_box[0] && x <= a.gate_box[1]) {
-            if (threadIdx.x == 0 && threadIdx.y == 0) gate_wait(a.gate_flag, a.gate_value);
+            if (threadIdx.x == 0 && threadIdx.y == 0) gate_wait(a.gate_flag, a.gate_value, a.gate_error);
             __syncthreads();
         }
     }
@@ -485,7 +489,7 @@ inline bool sweep_pdl() {
 // one K1 launch, programmatic stream serialisation allowed (see k_sweep)
 template <int OP, bool PULL, int MINB, class T>
 void launch_k_sweep_pdl(dim3 grd, dim3 blk, const SweepArgs& b, cudaStream_t s) {
-    if (!sweep_pdl()) {
+    if (!sweep_pdl() || !b.pdl) {
         k_sweep<OP, PULL, MINB, T><<<grd, blk, 0, s>>>(b);
         return;
     }
