@@ -361,7 +361,7 @@ class OracleSim:
         self.macro[1:-1, 1:-1, 1:-1, 1:4] = self.rnd(u_arr)
         self.force[...] = 0.0
 
-    def _actuators(self, kin):
+    def _actuators(self, kin, blade=None):
         pts = self.points
         P = kin.shape[0]
         fill_ghosts(self.macro, self.periodic)   # exchange_macro_halos (sim.py:273-274)
@@ -382,6 +382,11 @@ class OracleSim:
             f = disk_forces(ct, kin[first, 6:9], self.samples[sl, 0] * pts["rho_ref"],
                             self.samples[sl, 1:] * pts["vscale"], pts["area"][sl], rings, sectors)
             self.blade[sl] = -f
+        # blade: forces from elsewhere (the device's), spread in place of the
+        # oracle's own -- the LBM + spreading path then has identical inputs
+        self.blade_own = self.blade.copy()
+        if blade is not None:
+            self.blade = np.array(blade, dtype=np.float64)
         for p in range(P):
             records.append((p, kin[p, 0:3].copy(), -self.blade[p]))
         kernel, eps = pts.get("spreading", ("roma", 0.0))
@@ -390,9 +395,9 @@ class OracleSim:
         self.force[...] = 0.0
         spread(routed, self.force, self.dims, pts["dt2"], pts["den"], self.rnd, kernel, eps)
 
-    def step(self, kin=None):
+    def step(self, kin=None, blade=None):
         if self.points is not None:
-            self._actuators(np.asarray(kin, dtype=np.float64))
+            self._actuators(np.asarray(kin, dtype=np.float64), blade)
         collide_block(self.op, self.f, self.force, self.macro, self.omega, self.rates)
         if self.rnd is not _identity:
             self.f[...] = self.rnd(self.f)

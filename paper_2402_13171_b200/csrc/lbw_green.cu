@@ -16,7 +16,9 @@
 // 0 never, N > 0 always with N SMs.
 #include <cuda.h>
 
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "lbw_domain.h"
 
@@ -63,8 +65,23 @@ const GreenApi& api() {
 // A profiler or sanitizer injected into the process (ncu, compute-sanitizer)
 // serialises kernels: no partition then, so no sweep ever waits in-kernel
 // for a chain kernel that the tool has not run yet.
+// (ncu and compute-sanitizer load an injection library into the target:
+// look for it among the mapped objects, and for the variables they use.)
 static bool tool_injected() {
-    return getenv("CUDA_INJECTION64_PATH") != nullptr;
+    static const bool injected = [] {
+        if (getenv("CUDA_INJECTION64_PATH") || getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR"))
+            return true;
+        FILE* f = fopen("/proc/self/maps", "r");
+        if (!f) return false;
+        char line[4096];
+        bool hit = false;
+        while (!hit && fgets(line, sizeof line, f))
+            hit = strstr(line, "injection") != nullptr || strstr(line, "Injection") != nullptr ||
+                  strstr(line, "sanitizer") != nullptr;
+        fclose(f);
+        return hit;
+    }();
+    return injected;
 }
 
 int alm_sm_count(const lbw_domain* d) {

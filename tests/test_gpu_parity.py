@@ -266,13 +266,19 @@ def test_bench_config_deterministic_and_round_trip(gpu):
 
 # ----------------------------------------------------------- actuator line
 
+@pytest.mark.parametrize("arithmetic", ["exact", "fast"])
 @pytest.mark.parametrize("kinematics", ["host", "device"])
 @pytest.mark.parametrize("tag", ["periodic", "inflow"])
-def test_rotor_vs_reference(gpu, golden, tag, kinematics):
+def test_rotor_vs_reference(gpu, golden, tag, kinematics, arithmetic):
+    """The reference's own rotor runs (golden): exact arithmetic to the
+    actuator tolerances (samples 1e-12, blade forces 1e-10, populations
+    1e-14); the benchmark's fast arithmetic within 1e-10 relative."""
     g = golden(f"rotor_{tag}.npz")
     cfg, tmp = rotor_config(cells=tuple(int(c) for c in g["cells"]),
                             periodic=tuple(bool(p) for p in g["periodicity"]),
-                            boundary=str(g["boundary"]), position=tuple(g["position"]))
+                            boundary=str(g["boundary"]), position=tuple(g["position"]),
+                            arithmetic=arithmetic)
+    fast = arithmetic == "fast"
     sim = Simulation(cfg, kinematics=kinematics)
     for n in range(g["kin"].shape[0]):
         sim.step()
@@ -282,10 +288,12 @@ def test_rotor_vs_reference(gpu, golden, tag, kinematics):
         else:
             np.testing.assert_allclose(kin, g["kin"][n], rtol=1e-13, atol=1e-14)
         rho, u, blade = sim._alm_results()
-        np.testing.assert_allclose(rho, g["samples"][n, :, 0], rtol=1e-12)
-        np.testing.assert_allclose(u, g["samples"][n, :, 1:], rtol=1e-11, atol=1e-16)
+        np.testing.assert_allclose(rho, g["samples"][n, :, 0], rtol=1e-10 if fast else 1e-12)
+        np.testing.assert_allclose(u, g["samples"][n, :, 1:], rtol=1e-10 if fast else 1e-11,
+                                   atol=1e-15 if fast else 1e-16)
         np.testing.assert_allclose(blade, g["blade"][n], rtol=1e-10, atol=1e-13)
-    np.testing.assert_allclose(sim.fields[0].interior, g["f_final"], rtol=0, atol=1e-14)
+    np.testing.assert_allclose(sim.fields[0].interior, g["f_final"], rtol=0,
+                               atol=1e-13 if fast else 1e-14)
     np.testing.assert_allclose(sim.fields[0].interior_force, g["force_final"], rtol=1e-10,
                                atol=1e-18)
     sim.close()
