@@ -1,0 +1,119 @@
+// lbw_alm_dev.h — plain-data views of the actuator state shared by the host
+// driver (lbw_alm.cu) and the kernels that run the actuator chain (the
+// standalone chain kernels and the fused step kernel, lbw_fused.cuh).
+#pragma once
+#include <cstdint>
+
+#include "lbw_internal.h"
+
+namespace lbw {
+
+constexpr int kKin = 18;  // pos_lat(3) vel(3) e_chord(3) e_normal(3) e_span(3) pos_m(3)
+constexpr int kRing = 8;
+// per-component device state: world p(3) T(9) v(3) w(3) spin_axis(3) has_axis(1)
+// start_p(3) start_T(9) v_start(3) w_start(3) R(9)
+constexpr int kCS = 49;
+enum { CS_P = 0, CS_T = 3, CS_V = 12, CS_W = 15, CS_AX = 18, CS_HAX = 21, CS_SP = 22,
+       CS_ST = 25, CS_VS = 34, CS_WS = 37, CS_R = 40 };
+
+struct AlmDev {
+    int32_t n;
+    const double* chord;
+    const double* elen;
+    const double* twist;
+    const int32_t* polar_index;
+    const int32_t* polar_offset;
+    const int32_t* polar_rows;
+    const double* p_alpha;
+    const double* p_cl;
+    const double* p_cd;
+    double vscale, rho_ref, dt2, den;
+    double* kin;           // (P,18)
+    double* samples;       // (P,4)
+    double* blade;         // (P,3)
+    double* flat;          // (P,3) lattice force on the fluid
+    int32_t* dep_cell;     // (P,3 axes,kw) global cell or -1
+    double* dep_w;         // (P,3,kw)
+    int32_t kw;            // deposit cells per axis (3: Roma)
+    int32_t kernel;        // LBW_SPREAD_*
+    double eps;            // Gaussian width (cells)
+    int32_t halo_x;        // support half-width in x (cells), for slab relevance
+    int32_t* clamp_flags;  // (n_polars)
+    const int32_t* point_ring;  // (P) disk ring id or -1
+    const double* area;         // (P)
+    int32_t n_rings;
+    const int32_t* ring_first;
+    const int32_t* ring_count;
+    const double* ring_ct;
+    int32_t* error_flags;  // bit 0: non-positive density, bit 1: point outside domain,
+                           // bit 2: an actuator disk spans more than three slabs
+    int64_t step;             // the step this view serves (diagnostics)
+    double* ring_samples;     // (P,4) disk samples for the ring averages
+    int32_t* ring_sample_ok;  // (P)
+};
+
+struct KinDev {
+    int32_t nc;
+    const int32_t* parent;
+    const double* rel_p;
+    const double* rel_T;
+    const double* axis;
+    const double* rate;
+    const double* rstep;
+    double* spin;
+    const int32_t* line_first;
+    const int32_t* line_count;
+    const int32_t* point_comp;
+    const double* off;
+    const double* orient;
+    const double* lframe;
+    const int32_t* is_disk;
+    const double* disk_center;
+    double* cs;
+    double* spin_hist;   // (3, nc, 9): spin state of step j in slot j % 3
+    double* cs_hist;     // (3, nc, kCS)
+    int32_t hist_slot;
+    int32_t* box;           // (2): x planes this step's chain reads / writes (gate)
+    int32_t box_halo;       // spreading half-width + 2
+    int32_t stage_points;   // per-point constants fit in shared memory
+    const int32_t* order;        // (nc) components by tree depth
+    const int32_t* level_start;  // (nlevels+1) into order
+    int32_t nlevels;
+    const int32_t* is_static;    // (nc) world transform constant in time
+    int32_t skip_static;         // their state from the previous launch is valid
+    double dx;
+};
+
+// parameters per component in the kinematics CTA's shared memory:
+// rel_p 3, rel_T 9, axis 3, rate 1, rstep 9, spin 9, parent 1, first 1, is_disk 1, disk p 3, T 9
+constexpr int kKP = 49;
+constexpr int kMaxKw = 13;   // eps <= 2 -> at most floor(6 eps * 2) + 1 cells
+constexpr int kOnTheFlyMaxPoints = 64;
+enum { MA_REMOTE = 0, MA_OWNED = 1, MA_CONST = 2 };
+
+
+// How the macro field sampled at this step is obtained (MacroSource).
+struct MacroDev {
+    int kind;
+    double uniform[4];
+    const void* buf;   // population buffer (storage type per g.single)
+    int pull;
+    ForceView fv;
+    const double* dense;
+    int bc_set;        // the x-face BC has written its macro ghosts (after step 0)
+    double u_in[3];
+    int inflow;        // velocity_inflow_outflow
+    int per_x;
+};
+
+struct CubeArgs {
+    double* local;   // (P,8,4) of this step's parity
+    double* peer[2];
+    // per cube cell: epoch of the launch that wrote it (same allocation,
+    // after the values), so a reader knows which cells are this step's
+    int32_t* tag_local;  // (P,8)
+    int32_t* tag_peer[2];
+    int32_t epoch;
+};
+
+}  // namespace lbw

@@ -78,6 +78,18 @@ __host__ __device__ inline uint64_t row_key_of(uint32_t tag, int32_t slot) {
     return ((uint64_t)tag << 32) | (uint32_t)slot;
 }
 
+// A sparse force field: rows (x,y) of the slab that carry force own a slot
+// of [3][zp] storage elements in the pool (keys: see ForceView).
+struct ForceSet {
+    uint64_t* row_key = nullptr;   // (nxl*ny)
+    void* pool = nullptr;          // (cap, 3, zp) of the storage type
+    uint32_t tag = 0;              // tag of the filling step
+    int32_t flag_rows = 0;         // actuator set without a pool: K4 tags the rows
+    int64_t cap = 0;               // slots: user set one per row, actuator set 9 per point
+    ForceView view(uint32_t t) const { return ForceView{row_key, pool, t}; }
+};
+
+enum MacroKind { MS_UNIFORM = 0, MS_DENSE = 1, MS_GATHER = 2 };
 struct HaloOut {
     void* lo;  // receives dirs 0..8 of plane x=0   ([9][ny][zp]), or nullptr
     void* hi;  // receives dirs 18..26 of plane x=nxl-1, or nullptr
