@@ -146,58 +146,90 @@ def make_config(name, n_gpus, arithmetic, tmpdir, precision="double"):
 # ------------------------------------------------------------------ clocks
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons during the timed region."""
+    """SM clocks and throttle reasons sampled through NVML from a background
+    thread every ~1 ms while the sampler is open (warm-up + timed region);
+    mark() brackets the timed region so the summary can say how many samples
+    fell inside it.  Falls back to an nvidia-smi poll when NVML is absent."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
-    def __init__(self, index):
-        self.index = index
-        self.proc = None
-        self.path = tempfile.mktemp(suffix=".csv")
+    def __init__(self, device_index):
+        self.device_index = device_index
+        self.samples = []          # (t, sm_mhz, reason bits)
+        self.window = [None, None]
+        self.smax = None
+        self.error = None
+
+    def _handle(self, nv):
+        try:
+            import torch
+            p = torch.cuda.get_device_properties(self.device_index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return nv.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.device_index)
 
     def __enter__(self):
+        import threading
+        self.stop = threading.Event()
         try:
-            self.fh = open(self.path, "w")
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
-                stderr=subprocess.DEVNULL)
-        except (OSError, FileNotFoundError):
-            self.proc = None
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = self._handle(nv)
+            self.smax = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+        except Exception as e:           # no NVML: summary says so
+            self.nv = None
+            self.error = f"NVML unavailable: {e}"
+            return self
+
+        def poll():
+            nv, h = self.nv, self.h
+            while not self.stop.is_set():
+                try:
+                    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((time.perf_counter(), float(sm), int(rs)))
+                except Exception as e:
+                    self.error = str(e)
+                    return
+                time.sleep(0.001)
+
+        self.thread = threading.Thread(target=poll, daemon=True)
+        self.thread.start()
         return self
 
+    def mark(self, which):
+        self.window[0 if which == "start" else 1] = time.perf_counter()
+
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
-            self.fh.close()
+        self.stop.set()
+        if self.nv is not None:
+            self.thread.join(timeout=5)
 
     def summary(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm, smax, reasons = [], None, set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        with open(self.path) as fh:
-            for line in fh:
-                parts = [p.strip() for p in line.split(",")]
-                if len(parts) < 7:
-                    continue
-                try:
-                    sm.append(float(parts[0]))
-                    smax = float(parts[1])
-                except ValueError:
-                    continue
-                for nm, v in zip(names, parts[3:7]):
-                    if v.lower().startswith("active"):
-                        reasons.add(nm)
-        os.unlink(self.path)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "samples": len(sm), "reasons": sorted(reasons)}
+        if self.nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "samples": 0,
+                    "reasons": [self.error or "NVML unavailable"]}
+        t0, t1 = self.window
+        inside = [s for s in self.samples
+                  if t0 is not None and t1 is not None and t0 <= s[0] <= t1]
+        use = inside if inside else self.samples
+        reasons = set()
+        for nm, attr in self.REASONS:
+            bit = getattr(self.nv, attr, 0)
+            if any(s[2] & bit for s in use):
+                reasons.add(nm)
+        out = {"sm_mhz": statistics.median(s[1] for s in use) if use else None,
+               "sm_max_mhz": self.smax, "samples": len(use),
+               "samples_in_timed_region": len(inside),
+               "window": "timed region" if inside else "warm-up + timed region",
+               "sm_mhz_min": min(s[1] for s in use) if use else None,
+               "reasons": sorted(reasons), "source": "NVML, ~1 ms poll"}
+        return out
 
 
 # --------------------------------------------------------------- our arm
@@ -234,25 +266,34 @@ def run_ours(args, rank, world, local_rank):
         if dist is not None:
             dist.barrier()
 
+    clocks = ClockSampler(local_rank).__enter__()
     for _ in range(args.warmup):
         sim.step()
     sim.synchronize()
 
-    # ---- device-timed region (value)
+    # ---- device-timed region (value): K steps queued by one native call,
+    # nothing between the sweeps (per-sweep timing events would sit between
+    # consecutive sweeps and turn off their programmatic dependent launch)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    _lib.check(lib.lbw_domain_sweep_timing(sim._domain, 1))
     barrier()
     torch.cuda.synchronize()
     launches0 = _lib.kernel_launches()
-    with ClockSampler(local_rank) as clocks:
-        start.record(stream)
-        sim.advance(args.steps)     # K steps queued by one native call
-        stop.record(stream)
-        sim.synchronize()
+    clocks.mark("start")
+    start.record(stream)
+    sim.advance(args.steps)
+    stop.record(stream)
+    sim.synchronize()
+    clocks.mark("stop")
     launches = _lib.kernel_launches() - launches0
     torch.cuda.synchronize()
     barrier()
     ms = start.elapsed_time(stop)
+    # ---- the sweep kernel alone (roofline): the same K steps again with CUDA
+    # events recorded around every sweep launch on the domain stream
+    _lib.check(lib.lbw_domain_sweep_timing(sim._domain, 1))
+    sim.advance(args.steps)
+    sim.synchronize()
+    clocks.__exit__(None, None, None)
     sweep_ms = _lib.ctypes.c_double()
     sweep_n = _lib.ctypes.c_int64()
     _lib.check(lib.lbw_domain_sweep_time(sim._domain, _lib.ctypes.byref(sweep_ms),
@@ -435,6 +476,76 @@ def _host_sample_config(name):
     return "c3" if name in ("c4", "c5") else name
 
 
+def _numba_child(argv):
+    """Child process of the numba leg: the UNMODIFIED reference package from
+    baseline/_ref (PYTHONPATH), driven through its own public API --
+    lbwind.config.parse_config + lbwind.sim.Simulation.step() -- on the
+    host-sample workload, every host thread as a worker (x-slab blocks).
+    Prints one JSON object."""
+    name, precision, budget = argv[0], argv[1], float(argv[2])
+    import lbwind
+    from lbwind import _kernels
+    from lbwind.config import parse_config as ref_parse
+    from lbwind.sim import Simulation as RefSim
+    cores = len(os.sched_getaffinity(0))
+    tmp = tempfile.mkdtemp()
+    with open(os.path.join(tmp, "rotor.yaml"), "w") as fh:
+        fh.write(ROTOR.replace("points: 6", f"points: {POINTS_PER_BLADE}"))
+    with open(os.path.join(tmp, "sym.csv"), "w") as fh:
+        fh.write(polar_csv())
+    raw, desc = workload(name, 1)
+    nx = raw["domain"]["cells"][0]
+    nb = next(b for b in range(1, nx + 1) if nx % b == 0 and b >= min(cores, nx))
+    raw["run"].update({"precision": precision, "workers": cores,
+                       "block_dims": [nx // nb] + raw["domain"]["cells"][1:]})
+    cfg = ref_parse(raw, base_dir=tmp)
+    t0 = time.perf_counter()
+    _kernels.warm_up((cfg.dtype,))
+    sim = RefSim(cfg)
+    sim.step()                                   # untimed (JIT, first touch)
+    warm = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    sim.step()
+    t1 = time.perf_counter() - t0
+    n = int(max(1, min(50, budget / max(t1, 1e-3))))
+    t0 = time.perf_counter()
+    for _ in range(n):
+        sim.step()
+    t = time.perf_counter() - t0
+    sim.close()
+    cells = int(np.prod(cfg.cells))
+    print(json.dumps({"value": round(cells * n / t / 1e6, 3), "unit": "MLUP/s", "cores": cores,
+                      "kind": "reference",
+                      "sample": f"{n} timed steps (after 2 untimed) of {desc}, the reference "
+                                f"package lbwind {getattr(lbwind, '__version__', '0.1.0')} "
+                                f"(numba, baseline/_ref) through Simulation.step(), "
+                                f"{cores} workers on {nb} x-slab blocks, {t:.1f} s "
+                                f"(+{warm:.1f} s JIT / first step)",
+                      "cells": list(cfg.cells)}))
+
+
+def numba_reference(args, budget_s=20.0):
+    """Time the genuine reference (lbwind + numba from baseline/_ref) in a
+    child process; None when it is not installed or fails."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "lbwind")):
+        return {"unavailable": "baseline/_ref not installed"}
+    env = dict(os.environ)
+    env["PYTHONPATH"] = ref
+    env.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "lbw_numba_cache"))
+    env["NUMBA_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
+    env.pop("OMP_NUM_THREADS", None)
+    try:
+        r = subprocess.run([sys.executable, os.path.abspath(__file__), "--numba-child",
+                            _host_sample_config(args.config), args.precision, str(budget_s),
+                            str(POINTS_PER_BLADE)],
+                           env=env, capture_output=True, text=True, timeout=600,
+                           cwd=tempfile.gettempdir())
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:   # report, never fail the arm
+        return {"unavailable": f"numba reference failed: {type(e).__name__}: {e}"[:300]}
+
+
 def run_reference(args, rank, budget_s=150.0):
     if rank != 0:
         return None
@@ -443,32 +554,46 @@ def run_reference(args, rank, budget_s=150.0):
     # steps of the same workload when K would take longer than budget_s)
     from oracle import oracle as orc  # noqa: F401
     tmp = tempfile.TemporaryDirectory()
-    cfg, desc = make_config(_host_sample_config(args.config), 1, "exact", tmp.name,
-                            args.precision)
+    sample_name = _host_sample_config(args.config)
+    cfg, desc = make_config(sample_name, 1, "exact", tmp.name, args.precision)
     cells = int(np.prod(cfg.cells))
     est = cells / (cb["value"] * 1e6) if cb["value"] > 0 else 1.0
     n = int(max(1, min(args.steps, budget_s / max(est, 1e-6))))
     host = _HostOnlySim(cfg)
     t = _oracle_run(cfg, n, host)
+    P = len(host.points) if hasattr(host, "points") else None
     tmp.cleanup()
     value = cells * n / t / 1e6
     cb["value"] = round(value, 3)
-    # the line names the workload of this launch (weak-scaled with --gpus,
-    # as the GPU arm's); the timed sample is one GPU's share of it
+    # the line names the workload of this launch (weak-scaled with --gpus, as
+    # the GPU arm's) with the GPU arm's config keys; what was actually timed
+    # (one GPU's share; C4 / C5 through the C3 slab as a proxy) is measured_*
     raw_full, desc_full = workload(args.config, max(1, args.gpus))
-    cb["sample"] = (f"{n} of {args.steps} requested steps of {desc} (one GPU's share of "
-                    f"{desc_full}), C oracle, {cb['cores']} threads")
-    return {"metric": METRIC if args.precision == "double" else METRIC_SINGLE,
-            "value": round(value, 3), "unit": "MLUP/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(1e3 * t / n, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc_full, "cells": list(raw_full["domain"]["cells"]),
-                       "sample_cells": list(cfg.cells), "parallelism": "host threads",
-                       "gpus_used": 0},
-            "impl": "reference", "cpu_baseline": cb,
-            "e2e": {"value": round(value, 3), "unit": "MLUP/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+    full_cells = list(raw_full["domain"]["cells"])
+    proxy = " (C3 proxy: same per-cell work)" if sample_name != args.config else ""
+    cb["sample"] = (f"{n} of {args.steps} requested steps of {desc}{proxy}, C oracle "
+                    f"(bit-exact restatement of the reference kernels), {cb['cores']} threads")
+    cb["sample_cells"] = list(cfg.cells)
+    strong = args.config in ("c4", "c5")
+    per_gpu = int(np.prod(full_cells)) // (max(1, args.gpus))
+    out = {"metric": METRIC if args.precision == "double" else METRIC_SINGLE,
+           "value": round(value, 3), "unit": "MLUP/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(1e3 * t / n, 3), "higher_is_better": True,
+           "scaling": "strong" if strong else "weak", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic",
+           "config": {"workload": desc_full, "cells": full_cells,
+                      "cells_per_gpu": per_gpu, "actuator_points": P,
+                      "arithmetic": "exact (reference)", "storage": args.precision,
+                      "parallelism": f"host threads x{cb['cores']} (no GPU)",
+                      "l2": "n/a (host)"},
+           "measured_cells": list(cfg.cells),
+           "impl": "reference", "cpu_baseline": cb,
+           "e2e": {"value": round(value, 3), "unit": "MLUP/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    if not args.no_numba_reference:
+        out["reference_numba"] = numba_reference(args, budget_s=args.cpu_budget)
+    return out
 
 
 def main():
@@ -484,8 +609,14 @@ def main():
     ap.add_argument("--precision", choices=("double", "single"), default="double")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-numba-reference", action="store_true",
+                    help="reference arm: skip timing the numba reference package")
+    if len(sys.argv) > 1 and sys.argv[1] == "--numba-child":
+        global POINTS_PER_BLADE
+        POINTS_PER_BLADE = int(sys.argv[5])
+        _numba_child(sys.argv[2:5])
+        return
     args = ap.parse_args()
-    global POINTS_PER_BLADE
     POINTS_PER_BLADE = args.points_per_blade or (50 if args.config == "c5" else 6)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
