@@ -25,6 +25,7 @@
 //                          set (last read by this step's K4) for the next step.
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -81,6 +82,7 @@ struct AlmState {
     cudaEvent_t ev_kin_step[3] = {nullptr, nullptr, nullptr};
     // per-step blade-force series (lbw_alm_record_loads)
     double* h_loads = nullptr;   // pinned (loads_cap, P, 3)
+    double* d_loads = nullptr;   // its device mapping (the fused step writes it in-kernel)
     int64_t loads_cap = 0, loads_from = 0;
     // device kinematics
     bool kin_device = false;
@@ -100,6 +102,18 @@ struct AlmState {
     int32_t k_nlevels = 0;
     bool kin_static_ready = false;   // static components' state computed once
     size_t kin_smem = 0;
+    // fused step (lbw_fused.cuh): per-step geometry in slots j % 3, sample
+    // pools by parity, task counters of two consecutive launches
+    bool fs_alloc = false;
+    int32_t* fs_dep_cell = nullptr;   // (3,P,3,kw)
+    double* fs_dep_w = nullptr;       // (3,P,3,kw)
+    uint64_t* fs_frow = nullptr;      // (3, rows)
+    uint64_t* fs_skey = nullptr;      // (3, rows)
+    double* fs_spool = nullptr;       // (2, 4P, 4, zp)
+    uint32_t* fs_ctr = nullptr;       // (2, 2)
+    int64_t fs_next = -1;             // step the pipeline is primed for
+    unsigned long long* fs_prof = nullptr;   // (256, 8) timeline ring (LBW_FUSED_PROF)
+    int64_t fs_prof_n = 0;
     std::vector<void*> allocs;
 
     // device view for step m: outputs by parity, kinematics by m % 3
@@ -135,6 +149,7 @@ struct AlmState {
         a.ring_samples = ring_samples;
         a.ring_sample_ok = ring_sample_ok;
         a.error_flags = error_flags;
+        a.loads_row = nullptr;
         a.point_ring = point_ring;
         a.area = area;
         a.n_rings = n_rings;
@@ -183,7 +198,7 @@ namespace {
 __global__ void k_kinematics(KinDev k, AlmDev a, Geom g, int per_x, int advance) {
     extern __shared__ double ksm[];
     LBW_TRACE_BEGIN(1, a.step);
-    kinematics_cta(k, a, g, per_x, advance, ksm);
+    kinematics_cta(k, a, g, per_x, advance, ksm, (int)threadIdx.x, (int)blockDim.x);
     LBW_TRACE_END(1, a.step);
 }
 
@@ -255,6 +270,18 @@ __global__ void k_alm_disks(AlmDev a, Geom g, int per_x, int linked) {
     LBW_TRACE_BEGIN(3, a.step);
     if (r < a.n_rings) disk_ring(a, g, per_x, linked, r);
     LBW_TRACE_END(3, a.step);
+}
+
+// Fused-step priming (lbw_fused.cuh): kinematics (when not yet computed)
+// and the flow-independent geometry of step j, one CTA on the main stream.
+__global__ void k_fs_prime(KinDev k, AlmDev a, Geom g, int per_x, int advance, int do_kin,
+                           FsGeom geo) {
+    extern __shared__ double psm[];
+    if (do_kin) {
+        kinematics_cta(k, a, g, per_x, advance, psm, (int)threadIdx.x, (int)blockDim.x);
+        __syncthreads();
+    }
+    fs_geometry(geo, a, g, per_x, (int)threadIdx.x, (int)blockDim.x);
 }
 
 // K5: one warp per deposit pair q.  The lowest pair touching a row owns it:
@@ -433,6 +460,7 @@ int alm_invalidate(lbw_domain* d) {
     LBW_CK(cudaStreamSynchronize(d->alm_stream));
     if (d->alm->kin_stream) LBW_CK(cudaStreamSynchronize(d->alm->kin_stream));
     d->alm->ready_step = -1;
+    d->alm->fs_next = -1;
     return LBW_OK;
 }
 
@@ -465,6 +493,270 @@ static int kin_launch(lbw_domain* d, int64_t j) {
     return LBW_OK;
 }
 
+// sampling source of the next actuator step (the macro of the last collide)
+static MacroDev make_macro_dev(const lbw_domain* d) {
+    MacroDev md{};
+    md.kind = d->msrc.kind;
+    for (int k = 0; k < 4; ++k) md.uniform[k] = d->msrc.uniform[k];
+    md.buf = d->buf[d->msrc.buf];
+    md.pull = d->msrc.pull ? 1 : 0;
+    md.fv = d->msrc.fv;
+    md.dense = d->macro_dense;
+    md.bc_set = d->steps_done > 0 ? 1 : 0;
+    for (int k = 0; k < 3; ++k) md.u_in[k] = d->desc.u_in[k];
+    md.inflow = d->desc.boundary == LBW_BC_INFLOW_OUTFLOW ? 1 : 0;
+    md.per_x = d->desc.periodic[0] ? 1 : 0;
+    return md;
+}
+
+// ------------------------------------------------------------ fused step
+// One launch per step (lbw_fused.cuh) on a single slab with device
+// kinematics and at most 64 actuator points without disks: sweep m, the
+// point forces of step m, kinematics + geometry of step m+2.
+
+bool alm_fused_eligible(const lbw_domain* d) {
+    const AlmState* s = d->alm;
+    return d->fused && s && s->n > 0 && s->kin_device && s->on_the_fly && s->n_rings == 0 &&
+           !d->linked && !d->user_active && d->prelaunch && s->kin_smem <= 24 * 1024;
+}
+
+bool alm_after_fused(const lbw_domain* d) {
+    return alm_active(d) && d->alm->fs_next == d->step && d->step > 0;
+}
+
+static int fs_allocate(lbw_domain* d) {
+    AlmState* s = d->alm;
+    const int64_t rows = (int64_t)d->g.nxl * d->g.ny;
+    const size_t dep = (size_t)3 * s->n * 3 * s->kw;
+    int rc = LBW_OK;
+    auto A = [&](auto** p, size_t n) {
+        if (rc == LBW_OK) rc = dev_alloc(d, s, p, n);
+    };
+    A(&s->fs_dep_cell, dep);
+    A(&s->fs_dep_w, dep);
+    A(&s->fs_frow, (size_t)3 * rows);
+    A(&s->fs_skey, (size_t)3 * rows);
+    A(&s->fs_spool, (size_t)2 * 4 * s->n * 4 * d->g.zp);
+    A(&s->fs_ctr, 6);   // [task, done] x 2 launches + a scratch pair
+    if (rc) return rc;
+    // keys with tag 0xffffffff match no step (tags are step + 1)
+    LBW_CK(cudaMemset(s->fs_frow, 0xff, (size_t)3 * rows * 8));
+    LBW_CK(cudaMemset(s->fs_skey, 0xff, (size_t)3 * rows * 8));
+    LBW_CK(cudaMemset(s->fs_ctr, 0, 24));
+    if (getenv("LBW_FUSED_PROF")) {
+        rc = dev_alloc(d, s, &s->fs_prof, (size_t)256 * 8);
+        if (rc) return rc;
+    }
+    s->fs_alloc = true;
+    return LBW_OK;
+}
+
+// geometry slots of step j (written by KK(j))
+static FsGeom fs_geom(const lbw_domain* d, int64_t j) {
+    const AlmState* s = d->alm;
+    const int64_t rows = (int64_t)d->g.nxl * d->g.ny;
+    const int slot = (int)(j % 3);
+    const size_t dep = (size_t)s->n * 3 * s->kw;
+    FsGeom g;
+    g.dep_cell = s->fs_dep_cell + slot * dep;
+    g.dep_w = s->fs_dep_w + slot * dep;
+    g.frow_key = s->fs_frow + slot * rows;
+    g.skey = s->fs_skey + slot * rows;
+    g.tag = (uint32_t)(j + 1);
+    g.inflow = d->desc.boundary == LBW_BC_INFLOW_OUTFLOW ? 1 : 0;
+    return g;
+}
+
+// force of sweep m: rows tagged m+1 by KK(m), summed on the fly from the
+// deposit geometry of step m and the point forces K4(m) writes
+static ForceView fs_view(const lbw_domain* d, int64_t m) {
+    const AlmState* s = d->alm;
+    const FsGeom g = fs_geom(d, m);
+    ForceView v{g.frow_key, nullptr, g.tag};
+    v.npts = s->n;
+    v.kw = s->kw;
+    v.dep_cell = g.dep_cell;
+    v.dep_w = g.dep_w;
+    v.flat = s->flat + (size_t)(m & 1) * s->n * 3;
+    return v;
+}
+
+// kinematics (when missing) + geometry of step j, serially on the main stream
+static int fs_prime(lbw_domain* d, int64_t j) {
+    AlmState* s = d->alm;
+    int do_kin = 0, advance = 0;
+    if (s->kin_valid[j % 3] != j) {
+        if (j < s->kin_state_step || j > s->kin_state_step + 1) {
+            set_error("device kinematics can only advance one step at a time");
+            return LBW_ESTATE;
+        }
+        advance = j > s->kin_state_step ? 1 : 0;
+        do_kin = 1;
+    }
+    KinDev kd = s->kdev();
+    kd.hist_slot = (int32_t)(j % 3);
+    kd.skip_static = s->kin_static_ready ? 1 : 0;
+    k_fs_prime<<<1, 128, do_kin ? s->kin_smem : 0, d->stream>>>(
+        kd, s->dev(j), d->g, d->desc.periodic[0] ? 1 : 0, advance, do_kin, fs_geom(d, j));
+    count_launch();
+    LBW_CK(cudaGetLastError());
+    if (do_kin) {
+        s->kin_static_ready = true;
+        s->kin_state_step = j;
+        s->kin_valid[j % 3] = j;
+    }
+    return LBW_OK;
+}
+
+// LBW_FUSED_PROF: mean timeline of the last 128 complete launches (rows of
+// steps m-130 .. m-3), and the gap from each launch's last CTA to the next
+// launch's first CTA
+static void fs_prof_report(lbw_domain* d, int64_t m) {
+    AlmState* s = d->alm;
+    std::vector<unsigned long long> h(256 * 8);
+    if (cudaMemcpy(h.data(), s->fs_prof, h.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return;
+    double acc[5] = {0, 0, 0, 0, 0}, gap = 0.0, span = 0.0;
+    int n = 0, ng = 0;
+    for (int64_t j = m - 130; j < m - 2; ++j) {
+        if (j < 1) continue;
+        const unsigned long long* r = &h[(size_t)(j % 256) * 8];
+        const unsigned long long* q = &h[(size_t)((j + 1) % 256) * 8];
+        if (r[0] == ~0ull || r[5] == 0) continue;
+        const double t0 = (double)r[0];
+        for (int k = 0; k < 5; ++k) acc[k] += r[k + 1] ? (double)r[k + 1] - t0 : 0.0;
+        ++n;
+        if (q[0] != ~0ull && q[5] != 0) {
+            gap += (double)q[0] - (double)r[5];
+            span += (double)q[0] - t0;
+            ++ng;
+        }
+    }
+    if (!n) return;
+    fprintf(stderr,
+            "FUSEDPROF %d launches (us after first CTA): KK start %.2f end %.2f | tasks done %.2f "
+            "| force-tile wait end %.2f | last CTA end %.2f || next launch start-to-start %.2f, "
+            "last CTA end -> next first CTA %.2f\n",
+            n, acc[0] / n / 1e3, acc[1] / n / 1e3, acc[2] / n / 1e3, acc[3] / n / 1e3,
+            acc[4] / n / 1e3, ng ? span / ng / 1e3 : 0.0, ng ? gap / ng / 1e3 : 0.0);
+}
+
+int alm_fused_launch(lbw_domain* d, bool pull, ForceView* fv_out) {
+    AlmState* s = d->alm;
+    const int64_t m = d->step;
+    if (!s->fs_alloc) {
+        int rc = fs_allocate(d);
+        if (rc) return rc;
+    }
+    // primed: the previous launch was fused step m-1 (pool of step m filled,
+    // kinematics + geometry of m and m+1 done, counters of m zeroed)
+    const bool primed = s->fs_next == m && s->kin_state_step == m + 1 &&
+                        s->kin_valid[(m + 1) % 3] == m + 1 && s->kin_valid[m % 3] == m;
+    if (!primed) {
+        // whatever the standalone chain queued is finished before its
+        // outputs are rewritten here
+        LBW_CK(cudaStreamSynchronize(d->alm_stream));
+        if (s->kin_stream) LBW_CK(cudaStreamSynchronize(s->kin_stream));
+        int rc = fs_prime(d, m);
+        if (!rc) rc = fs_prime(d, m + 1);
+        if (rc) return rc;
+        LBW_CK(cudaMemsetAsync(s->fs_ctr, 0, 4 * sizeof(uint32_t), d->stream));
+    }
+    const int per_x = d->desc.periodic[0] ? 1 : 0;
+    const int64_t rows = (int64_t)d->g.nxl * d->g.ny;
+    FusedArgs A{};
+    SweepArgs& w = A.sw;
+    w.src = d->buf[d->cur];
+    w.dst = d->buf[1 - d->cur];
+    w.g = d->g;
+    w.fv = fs_view(d, m);
+    w.r = d->relax;
+    w.x_begin = 0;
+    w.x_end = d->g.nxl;
+    w.nan_key = d->d_nan;
+    w.step = m;
+    w.halo = HaloOut{nullptr, nullptr, {nullptr, nullptr}, nullptr, 0u, 0u};
+    w.gate_flag = nullptr;
+    w.gate_box = nullptr;
+    w.gate_value = 0;
+    w.reverse = (d->sweep_alt && (m & 1)) ? 1 : 0;
+    w.pdl = 1;
+    w.gate_error = nullptr;
+    A.a = s->dev(m);
+    if (s->loads_cap > 0 && s->d_loads)
+        A.a.loads_row = s->d_loads + (size_t)(m % s->loads_cap) * s->n * 3;
+    A.md = make_macro_dev(d);
+    A.use_pool = primed ? 1 : 0;
+    A.pool.skey = s->fs_skey + (size_t)(m % 3) * rows;
+    A.pool.spool = s->fs_spool + (size_t)(m & 1) * 4 * s->n * 4 * d->g.zp;
+    A.pool.tag = (uint32_t)(m + 1);
+    A.pool.inflow = d->desc.boundary == LBW_BC_INFLOW_OUTFLOW ? 1 : 0;
+    for (int k = 0; k < 3; ++k) A.pool.u_in[k] = d->desc.u_in[k];
+    A.pool.error_flags = s->error_flags;
+    A.ctr = s->fs_ctr + 2 * (m & 1);
+    A.ctr_next = s->fs_ctr + 2 * ((m + 1) & 1);
+    A.skey_next = s->fs_skey + (size_t)((m + 1) % 3) * rows;
+    A.spool_next = s->fs_spool + (size_t)((m + 1) & 1) * 4 * s->n * 4 * d->g.zp;
+    A.store_tag = (uint32_t)(m + 2);
+    // KK(m+2) rewrites the geometry slot of step m-1, which a priming
+    // launch's sampling reads (the force view of sweep m-1): not then
+    A.kk_on = primed ? 1 : 0;
+    A.k = s->kdev();
+    A.k.hist_slot = (int32_t)((m + 2) % 3);
+    A.k.skip_static = s->kin_static_ready ? 1 : 0;
+    A.a_kk = s->dev(m + 2);
+    A.geo = fs_geom(d, m + 2);
+    A.per_x = per_x;
+    A.n_kk = primed ? 1 : 0;
+    A.n_help = (s->n + 3) / 4;
+    A.prof = nullptr;
+    A.prof_next = nullptr;
+    if (s->fs_prof) {
+        A.prof = s->fs_prof + (size_t)(m % 256) * 8;
+        A.prof_next = s->fs_prof + (size_t)((m + 1) % 256) * 8;
+        if (!primed) {
+            unsigned long long init[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
+            LBW_CK(cudaMemcpyAsync(A.prof, init, sizeof init, cudaMemcpyHostToDevice, d->stream));
+        }
+        if (++s->fs_prof_n % 200 == 0) {
+            LBW_CK(cudaStreamSynchronize(d->stream));
+            fs_prof_report(d, m);
+        }
+    }
+    const size_t smem = primed ? s->kin_smem : 0;
+    auto launch = [&](const FusedArgs& X, size_t sm) {
+        return d->desc.mode == LBW_MODE_FAST ? launch_fused_fast(d->desc.op, pull, X, sm, d->stream)
+                                             : launch_fused_exact(d->desc.op, pull, X, sm, d->stream);
+    };
+    if (!primed) {
+        // Priming: K4(m) samples by recomputation from buffers this sweep
+        // may overwrite (the sampling source is the previous sweep's input,
+        // i.e. this sweep's output buffer): it runs first, as a launch of
+        // the point tasks alone, which leaves the counters of step m at
+        // [n, n] -- the sweep launch then neither claims nor waits.
+        FusedArgs T = A;
+        T.sw.x_end = T.sw.x_begin;    // no sweep tiles
+        T.n_kk = 0;
+        T.kk_on = 0;
+        T.ctr_next = s->fs_ctr + 4;   // scratch: nothing to reset for a successor
+        LBW_CK(launch(T, 0));
+        A.n_help = 0;
+    }
+    LBW_CK(launch(A, smem));
+    if (primed) {
+        s->kin_static_ready = true;
+        s->kin_state_step = m + 2;
+        s->kin_valid[(m + 2) % 3] = m + 2;
+    } else {
+        int rc = fs_prime(d, m + 2);
+        if (rc) return rc;
+    }
+    s->fs_next = m + 1;
+    s->ready_step = -1;
+    *fv_out = w.fv;
+    return LBW_OK;
+}
+
 int alm_launch(lbw_domain* d, int64_t m) {
     AlmState* s = d->alm;
     const Geom& g = d->g;
@@ -486,17 +778,7 @@ int alm_launch(lbw_domain* d, int64_t m) {
         set_error("actuator step without kinematics: call lbw_alm_set_kinematics first");
         return LBW_ESTATE;
     }
-    MacroDev md{};
-    md.kind = d->msrc.kind;
-    for (int k = 0; k < 4; ++k) md.uniform[k] = d->msrc.uniform[k];
-    md.buf = d->buf[d->msrc.buf];
-    md.pull = d->msrc.pull ? 1 : 0;
-    md.fv = d->msrc.fv;
-    md.dense = d->macro_dense;
-    md.bc_set = d->steps_done > 0 ? 1 : 0;
-    for (int k = 0; k < 3; ++k) md.u_in[k] = d->desc.u_in[k];
-    md.inflow = d->desc.boundary == LBW_BC_INFLOW_OUTFLOW ? 1 : 0;
-    md.per_x = per_x;
+    MacroDev md = make_macro_dev(d);
     // one warp per CTA: fits in the registers a full sweep leaves free
     const int threads = 32;
     const size_t pts_smem =
@@ -578,7 +860,11 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     LBW_REQ(desc->n_polars >= 0, "n_polars must be >= 0");
     LBW_CK(cudaSetDevice(d->device));
     d->touched = true;
-    if (desc->n_points > 0) {
+    // no SM partition when the fused step will carry the chain (it runs on
+    // every SM; lbw_fused.cuh)
+    const bool fused_likely = d->fused && !d->linked && desc->n_points <= kOnTheFlyMaxPoints &&
+                              !desc->point_ring;
+    if (desc->n_points > 0 && !(fused_likely && !getenv("LBW_ALM_SMS"))) {
         int rc_ = green_partition(d, alm_sm_count(d));
         if (rc_) return rc_;
     }
@@ -879,6 +1165,7 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
     s->kin_valid[0] = s->kin_valid[1] = s->kin_valid[2] = -1;
     s->kin_static_ready = false;
     s->ready_step = -1;
+    s->fs_next = -1;
     return LBW_OK;
 }
 
@@ -970,6 +1257,10 @@ int lbw_alm_get(lbw_domain* d, double* rho, double* u, double* blade_force) {
                   "samples from beyond the neighbouring slabs)");
         return LBW_EINVAL;
     }
+    if (err & 8) {
+        set_error("internal: a sampled row of the fused step had no pooled macro");
+        return LBW_ECUDA;
+    }
     if (err & 1) {
         set_error("density must be positive at an actuator point");
         return LBW_EINVAL;
@@ -983,12 +1274,19 @@ int lbw_alm_record_loads(lbw_domain* d, int64_t capacity) {
     AlmState* s = d->alm;
     LBW_CK(cudaSetDevice(d->device));
     LBW_CK(cudaStreamSynchronize(d->alm_stream));
+    LBW_CK(cudaStreamSynchronize(d->stream));
     if (s->h_loads) cudaFreeHost(s->h_loads);
     s->h_loads = nullptr;
+    s->d_loads = nullptr;
     s->loads_cap = 0;
     if (capacity > 0) {
         LBW_REQ(capacity >= 2, "capacity must be >= 2");
         LBW_CK(cudaMallocHost(&s->h_loads, (size_t)capacity * s->n * 3 * sizeof(double)));
+        void* dp = nullptr;
+        s->d_loads = cudaHostGetDevicePointer(&dp, s->h_loads, 0) == cudaSuccess
+                         ? static_cast<double*>(dp)
+                         : nullptr;
+        cudaGetLastError();
         s->loads_cap = capacity;
     }
     s->loads_from = d->step;
@@ -1007,6 +1305,7 @@ int lbw_alm_read_loads(lbw_domain* d, double* out, int64_t max_steps, int64_t* f
     LBW_REQ(avail < s->loads_cap || avail == 0,
             "load ring overflow: read the loads at least every capacity-1 steps");
     LBW_CK(cudaStreamSynchronize(d->alm_stream));
+    LBW_CK(cudaStreamSynchronize(d->stream));   // the fused step writes loads in-kernel
     const int64_t k = std::min(avail, max_steps);
     const size_t row = (size_t)s->n * 3;
     for (int64_t i = 0; i < k; ++i) {

@@ -50,6 +50,7 @@ struct AlmDev {
     int64_t step;             // the step this view serves (diagnostics)
     double* ring_samples;     // (P,4) disk samples for the ring averages
     int32_t* ring_sample_ok;  // (P)
+    double* loads_row;        // (P,3) this step's row of the device loads ring, or nullptr
 };
 
 struct KinDev {
@@ -115,5 +116,67 @@ struct CubeArgs {
     int32_t* tag_peer[2];
     int32_t epoch;
 };
+
+// ---------------------------------------------------------------- fused step
+// Per-step actuator data of the fused step kernel live in three slots
+// (step j in slot j % 3): KK(j) writes them two steps ahead, K4(j) and
+// sweep j read them, nothing of step j is overwritten before sweep j+1.
+
+// Geometry of step j, written by KK(j): deposit cells / weights, the force
+// rows it tags (tag j+1, read by sweep j), and the rows holding its
+// sampling cubes (sample keys, tag j+1, slot = point*4 + corner row: sweep
+// j-1 stores the macro of those rows into the sample pool for K4(j)).
+struct FsGeom {
+    int32_t* dep_cell;     // (P,3,kw)
+    double* dep_w;         // (P,3,kw)
+    uint64_t* frow_key;    // (nxl*ny)
+    uint64_t* skey;        // (nxl*ny)
+    uint32_t tag;          // j+1
+    int32_t inflow;        // velocity_inflow_outflow x faces
+};
+
+// Sampling of step j from the pool sweep j-1 filled.
+struct FsPool {
+    const uint64_t* skey;  // sample row keys of step j
+    const double* spool;   // (4P, 4, zp): rho, ux, uy, uz of each keyed row
+    uint32_t tag;          // j+1
+    int32_t inflow;
+    double u_in[3];
+    int32_t* error_flags;  // bit 3: a sampled row without a pool entry
+};
+
+// One launch of the fused step kernel (lbw_fused.cuh): sweep m, the point
+// forces of step m (K4, claimed as tasks by helper CTAs and by any sweep CTA
+// that needs them) and the kinematics + geometry of step m+2 (KK, one CTA).
+struct FusedArgs {
+    SweepArgs sw;          // sweep m; sw.fv = the on-the-fly force view of step m
+    AlmDev a;              // K4(m): kin slot m%3, flat = fused slot, outputs by parity
+    MacroDev md;           // general sampling source (use_pool == 0)
+    int32_t use_pool;
+    FsPool pool;           // use_pool: the cube values from the pool of step m
+    uint32_t* ctr;         // [task, done] of this launch (zeroed by the previous launch)
+    uint32_t* ctr_next;    // zeroed here for the next launch
+    const uint64_t* skey_next;  // sample keys of step m+1 (tag store_tag)
+    double* spool_next;         // its pool, filled by this sweep
+    uint32_t store_tag;         // m+2
+    int32_t kk_on;              // KK(m+2) runs in CTA 0
+    KinDev k;
+    AlmDev a_kk;                // kin slot (m+2)%3
+    FsGeom geo;                 // geometry of step m+2
+    int32_t per_x;
+    int32_t n_kk, n_help;       // leading CTAs: KK, point-task helpers
+    uint32_t tiles_x, tiles_y;  // sweep tiles per plane (z blocks, y blocks)
+    // optional timeline (LBW_FUSED_PROF): %globaltimer of this launch's
+    // [first CTA start, KK start, KK end, last point task done, last
+    // force-tile wait end, last CTA end]; nullptr = off.  prof_next: the
+    // next launch's row, reset here
+    unsigned long long* prof;
+    unsigned long long* prof_next;
+};
+
+// one fused step launch (lbw_fused.cuh), per arithmetic flavour
+cudaError_t launch_fused_exact(int op, bool pull, const FusedArgs& a, size_t smem,
+                               cudaStream_t s);
+cudaError_t launch_fused_fast(int op, bool pull, const FusedArgs& a, size_t smem, cudaStream_t s);
 
 }  // namespace lbw

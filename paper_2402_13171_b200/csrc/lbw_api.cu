@@ -263,6 +263,10 @@ int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out) {
         d->prelaunch = !(e && e[0] == '0');
         const char* alt = getenv("LBW_SWEEP_ALT");   // 0 disables (A/B)
         d->sweep_alt = !(alt && alt[0] == '0');
+        // LBW_FUSED=1: one fused launch per actuator step (lbw_fused.cuh);
+        // off by default until its chain latency beats the standalone chain
+        const char* fu = getenv("LBW_FUSED");
+        d->fused = fu && fu[0] == '1';
     }
     d->device = s.device;
     if (cudaSetDevice(d->device) != cudaSuccess) {
@@ -625,6 +629,37 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
         }
         std::swap(d->ev_ready, d->ev_ready_prev);
         LBW_CK(cudaEventRecord(d->ev_ready, d->stream));
+        if (alm_active(d) && alm_fused_eligible(d)) {
+            // one launch: sweep + this step's point forces + the kinematics
+            // of step+2 (lbw_fused.cuh)
+            const bool pull = !d->state_pre;
+            if (d->timing) {
+                while (d->ev_pool.size() < d->ev_used + 2) {
+                    cudaEvent_t ev;
+                    LBW_CK(cudaEventCreate(&ev));
+                    d->ev_pool.push_back(ev);
+                }
+                LBW_CK(cudaEventRecord(d->ev_pool[d->ev_used], d->stream));
+            }
+            int rc = alm_fused_launch(d, pull, &fv);
+            if (rc) return rc;
+            if (d->timing) {
+                LBW_CK(cudaEventRecord(d->ev_pool[d->ev_used + 1], d->stream));
+                d->ev_used += 2;
+            }
+            d->msrc.kind = MS_GATHER;
+            d->msrc.buf = d->cur;
+            d->msrc.pull = pull;
+            d->msrc.fv = fv;
+            d->last_fv = fv;
+            d->shown_fv = fv;
+            d->touched = false;
+            d->cur = 1 - d->cur;
+            d->state_pre = false;
+            d->step += 1;
+            d->steps_done += 1;
+            continue;
+        }
         if (alm_active(d)) {
             // The actuator chain of this step normally was queued on the
             // actuator stream while the previous sweep ran.  Otherwise (host
@@ -633,7 +668,7 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
             // unless a call changed state since the last step, in which case
             // it waits for everything already on the main stream.
             if (!alm_ready(d, d->step)) {
-                if (d->touched) {
+                if (d->touched || alm_after_fused(d)) {
                     LBW_CK(cudaEventRecord(d->ev_main, d->stream));
                     LBW_CK(cudaStreamWaitEvent(d->alm_stream, d->ev_main, 0));
                 } else {

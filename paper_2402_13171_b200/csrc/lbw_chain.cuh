@@ -8,6 +8,7 @@
 #pragma once
 #include <climits>
 
+#include "../../include/lbw.h"
 #include "lbw_alm_dev.h"
 
 namespace lbw {
@@ -197,7 +198,7 @@ __device__ void walk_component(const KinDev& k, double* prm, double* cs, int c, 
 // parallel.  Layout per component in smem: params[kKP] then state[kCS].
 // rel_p 3, rel_T 9, axis 3, rate 1, rstep 9, spin 9, parent 1, first 1, is_disk 1, disk p 3, T 9
 __device__ void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g, int per_x,
-                               int advance, double* ksm) {
+                               int advance, double* ksm, int tid, int nthr) {
 #ifdef LBW_KK_PROF
     long long t0 = clock64();
 #endif
@@ -214,27 +215,27 @@ __device__ void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g, 
                                        : reinterpret_cast<int32_t*>(cs + (size_t)k.nc * kCS);
     int32_t* sm_static = sm_order + k.nc;
     int32_t* sm_lstart = sm_static + k.nc;
-    for (int i = threadIdx.x; i < k.nc; i += blockDim.x) {
+    for (int i = tid; i < k.nc; i += nthr) {
         sm_order[i] = k.order[i];
         sm_static[i] = k.is_static[i];
     }
-    for (int i = threadIdx.x; i <= k.nlevels; i += blockDim.x) sm_lstart[i] = k.level_start[i];
+    for (int i = tid; i <= k.nlevels; i += nthr) sm_lstart[i] = k.level_start[i];
     if (k.skip_static)
-        for (int i = threadIdx.x; i < k.nc * kCS; i += blockDim.x)
+        for (int i = tid; i < k.nc * kCS; i += nthr)
             if (k.is_static[i / kCS]) cs[i] = k.cs[i];
     const double* off = k.stage_points ? sm_off : k.off;
     const double* orient = k.stage_points ? sm_orient : k.orient;
     const double* lframe = k.stage_points ? sm_lframe : k.lframe;
     const int32_t* point_comp = k.stage_points ? sm_comp : k.point_comp;
     if (k.stage_points) {
-        for (int i = threadIdx.x; i < a.n * 3; i += blockDim.x) sm_off[i] = k.off[i];
-        for (int i = threadIdx.x; i < a.n * 9; i += blockDim.x) {
+        for (int i = tid; i < a.n * 3; i += nthr) sm_off[i] = k.off[i];
+        for (int i = tid; i < a.n * 9; i += nthr) {
             sm_orient[i] = k.orient[i];
             sm_lframe[i] = k.lframe[i];
         }
-        for (int i = threadIdx.x; i < a.n; i += blockDim.x) sm_comp[i] = k.point_comp[i];
+        for (int i = tid; i < a.n; i += nthr) sm_comp[i] = k.point_comp[i];
     }
-    for (int i = threadIdx.x; i < k.nc * kKP; i += blockDim.x) {
+    for (int i = tid; i < k.nc * kKP; i += nthr) {
         const int c = i / kKP, j = i % kKP;
         double v;
         if (j < 3) v = k.rel_p[c * 3 + j];
@@ -259,9 +260,9 @@ __device__ void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g, 
         // rotation on their path) keep the state of the first launch.
         __shared__ double I3s[9], zero3s[3];
         __shared__ double wtmp[8][24];
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-        if (threadIdx.x < 9) I3s[threadIdx.x] = (threadIdx.x % 4 == 0) ? 1.0 : 0.0;
-        if (threadIdx.x < 3) zero3s[threadIdx.x] = 0.0;
+        const int lane = tid & 31, warp = tid >> 5, nwarp = nthr >> 5;
+        if (tid < 9) I3s[tid] = (tid % 4 == 0) ? 1.0 : 0.0;
+        if (tid < 3) zero3s[tid] = 0.0;
         __syncthreads();
         for (int L = 0; L < k.nlevels; ++L) {
             for (int j = sm_lstart[L] + warp; j < sm_lstart[L + 1]; j += nwarp) {
@@ -276,10 +277,10 @@ __device__ void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g, 
     long long t2 = clock64();
 #endif
     // persist spin + component state (downloadable), evaluate the points
-    for (int i = threadIdx.x; i < k.nc * 9; i += blockDim.x)
+    for (int i = tid; i < k.nc * 9; i += nthr)
         k.spin[i] = k.spin_hist[(int64_t)k.hist_slot * k.nc * 9 + i] =
             prm[(i / 9) * kKP + 25 + i % 9];
-    for (int i = threadIdx.x; i < k.nc * kCS; i += blockDim.x)
+    for (int i = tid; i < k.nc * kCS; i += nthr)
         k.cs[i] = k.cs_hist[(int64_t)k.hist_slot * k.nc * kCS + i] = cs[i];
 #ifdef LBW_KK_PROF
     long long t3 = clock64();
@@ -287,12 +288,12 @@ __device__ void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g, 
     const int64_t dims[3] = {g.nxg, g.ny, g.nz};
     const int per[3] = {per_x, g.per_y, g.per_z};
     __shared__ int box_lo, box_hi;
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
         box_lo = INT_MAX;
         box_hi = INT_MIN;
     }
     __syncthreads();
-    for (int p = threadIdx.x; p < a.n; p += blockDim.x) {
+    for (int p = tid; p < a.n; p += nthr) {
         const int c = point_comp[p];
         const double* s = cs + c * kCS;
         const int kk = p - k.line_first[c];
@@ -349,14 +350,14 @@ __device__ void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g, 
     }
     if (k.box) {
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (tid == 0) {
             k.box[0] = box_lo;
             k.box[1] = box_hi;
         }
     }
 #ifdef LBW_KK_PROF
     __syncthreads();
-    if (threadIdx.x == 0)
+    if (tid == 0)
         printf("KKPROF stage %lld walk %lld persist %lld points %lld\n", t1 - t0, t2 - t1, t3 - t2,
                clock64() - t3);
 #endif
@@ -679,6 +680,62 @@ __device__ __noinline__ void deposit_axis_wide(const AlmDev& a, int p, int k, do
 // local and both neighbours' cube buffers; phase 2 (after the neighbours'
 // stores are visible) continues from the cube buffer.
 
+// Where the sampled macro of global cell (gx,gy,gz) comes from, with the
+// ghost rules of macro_at_raw in steady state (the x-face BC has run):
+// MA_CONST with its value in out, or MA_OWNED with the slab-local cell.
+__device__ __forceinline__ int corner_map(const Geom& g, int per_x, int inflow, const double* u_in,
+                                          int64_t gx, int64_t gy, int64_t gz, int& x, int& y,
+                                          int& z, double out[4]) {
+    out[0] = 1.0;
+    out[1] = out[2] = out[3] = 0.0;
+    if (gx < 0 || gx >= g.nxg) {
+        if (per_x) {
+            gx = gx < 0 ? gx + g.nxg : gx - g.nxg;
+        } else if (inflow && gx < 0) {
+            out[1] = u_in[0];
+            out[2] = u_in[1];
+            out[3] = u_in[2];
+            return MA_CONST;
+        } else if (inflow && gx >= g.nxg) {
+            gx = g.nxg - 1;
+        } else {
+            return MA_CONST;
+        }
+    }
+    if (gy < 0 || gy >= g.ny) {
+        if (!g.per_y) return MA_CONST;
+        gy = gy < 0 ? gy + g.ny : gy - g.ny;
+    }
+    if (gz < 0 || gz >= g.nz) {
+        if (!g.per_z) return MA_CONST;
+        gz = gz < 0 ? gz + g.nz : gz - g.nz;
+    }
+    x = (int)(gx - g.x0);
+    y = (int)gy;
+    z = (int)gz;
+    return MA_OWNED;
+}
+
+// Sampled macro from the pool the previous sweep filled (fused step):
+// the (rho, u) its collide computed for the keyed rows, already rounded
+// to the storage type as the reference's macro array holds them.
+__device__ __forceinline__ int pool_macro(const Geom& g, const FsPool& pl, int per_x, int64_t gx,
+                                          int64_t gy, int64_t gz, double out[4]) {
+    int x = 0, y = 0, z = 0;
+    const int code = corner_map(g, per_x, pl.inflow, pl.u_in, gx, gy, gz, x, y, z, out);
+    if (code != MA_OWNED) return code;
+    const uint64_t key = __ldcg(reinterpret_cast<const unsigned long long*>(pl.skey) +
+                                (int64_t)x * g.ny + y);
+    if ((uint32_t)(key >> 32) != pl.tag) {
+        atomicOr(pl.error_flags, 8);
+        return code;
+    }
+    const double* b = pl.spool + (int64_t)(uint32_t)key * 4 * g.zp + z;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) out[q] = __ldcg(b + (int64_t)q * g.zp);
+    return MA_OWNED;
+}
+
 // Flow-independent per-point inputs, loaded by the kernel before anything
 // that waits (kinematics row one value per lane, polar / chord data).
 struct PointInputs {
@@ -699,7 +756,8 @@ __device__ __forceinline__ PointInputs load_point_inputs(const AlmDev& a, int p,
 
 __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, const ForceSet& s,
                            int phase, const CubeArgs& cube, int p, int lane,
-                           const PointInputs& in) {
+                           const PointInputs& in, const FsPool* pool = nullptr,
+                           bool geometry = true) {
     const PointStatic& ps = in.ps;
     const bool disk = in.disk;
     double kr[15];
@@ -712,7 +770,7 @@ __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, co
     // for the row tags below and stored for the sweep / fill / next sample
     const int kw = a.kw;
     int32_t dcl[3] = {-1, -1, -1};   // Roma: kept in registers for the row tags
-    if (phase != 1 && lane >= 8 && lane <= 10) {
+    if (geometry && phase != 1 && lane >= 8 && lane <= 10) {
         const int k = lane - 8;
         const int64_t L = k == 0 ? g.nxg : (k == 1 ? g.ny : g.nz);
         const int per = k == 0 ? m.per_x : (k == 1 ? g.per_y : g.per_z);
@@ -742,8 +800,10 @@ __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, co
             have = cube.tag_local[(int64_t)p * 8 + lane] == cube.epoch;
         }
     } else if (lane < 8) {
-        const int code = macro_at(g, m, j0[0] + ((lane >> 2) & 1), j0[1] + ((lane >> 1) & 1),
-                                  j0[2] + (lane & 1), v);
+        const int64_t cgx = j0[0] + ((lane >> 2) & 1), cgy = j0[1] + ((lane >> 1) & 1),
+                      cgz = j0[2] + (lane & 1);
+        const int code = pool ? pool_macro(g, *pool, m.per_x, cgx, cgy, cgz, v)
+                              : macro_at(g, m, cgx, cgy, cgz, v);
         if (phase == 1) {
             const int64_t o = ((int64_t)p * 8 + lane) * 4;
             if (code != MA_REMOTE) {
@@ -823,6 +883,7 @@ __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, co
         for (int c = 0; c < 3; ++c) {
             a.blade[p * 3 + c] = owner ? blade[c] : 0.0;
             a.flat[p * 3 + c] = -blade[c] * a.dt2 / a.den;  // units.py:69
+            if (a.loads_row) a.loads_row[p * 3 + c] = owner ? blade[c] : 0.0;
         }
         if (disk) {
             // ring averages need every sample of the ring, owned or not
@@ -902,6 +963,51 @@ __device__ void disk_ring(const AlmDev& a, const Geom& g, int per_x, int linked,
             const double f = direction * per_area * a.area[p] * axis[c];
             a.blade[p * 3 + c] = owner ? -f : 0.0;
             a.flat[p * 3 + c] = f * a.dt2 / a.den;
+        }
+    }
+}
+
+// Flow-independent geometry of step j for the fused step (KK, after the
+// CTA's kinematics): per point the per-axis deposit cells and weights
+// (actuator.py:190-195), the force rows its deposit touches (tag j+1, the
+// rows sweep j sums point forces in), and the rows of its sampling cube
+// (sample keys: sweep j-1 stores its macro there for K4(j)).  Rows shared
+// by several points get one key each write; any writer's slot is valid.
+__device__ void fs_geometry(const FsGeom& geo, const AlmDev& a, const Geom& g, int per_x, int tid,
+                            int nthr) {
+    const int kw = a.kw;
+    const double zero3[3] = {0.0, 0.0, 0.0};
+    for (int p = tid; p < a.n; p += nthr) {
+        const double* kr = a.kin + (int64_t)p * kKin;
+        const double xl[3] = {kr[0], kr[1], kr[2]};
+        int32_t dcx[kMaxKw], dcy[kMaxKw];
+        for (int k = 0; k < 3; ++k) {
+            const int64_t L = k == 0 ? g.nxg : (k == 1 ? g.ny : g.nz);
+            const int per = k == 0 ? per_x : (k == 1 ? g.per_y : g.per_z);
+            int32_t dc[kMaxKw];
+            double dw[kMaxKw];
+            deposit_axis(xl[k], L, per, a.kernel, a.eps, kw, dc, dw);
+            for (int q = 0; q < kw; ++q) {
+                geo.dep_cell[((int64_t)p * 3 + k) * kw + q] = dc[q];
+                geo.dep_w[((int64_t)p * 3 + k) * kw + q] = dw[q];
+                if (k == 0) dcx[q] = dc[q];
+                if (k == 1) dcy[q] = dc[q];
+            }
+        }
+        for (int i = 0; i < kw; ++i)
+            for (int l = 0; l < kw; ++l) {
+                const int32_t cxg = dcx[i], cy = dcy[l];
+                const int64_t x = (int64_t)cxg - g.x0;
+                if (cxg >= 0 && cy >= 0 && x >= 0 && x < g.nxl)
+                    geo.frow_key[x * g.ny + cy] = row_key_of(geo.tag, 0);
+            }
+        const int64_t j0x = (int64_t)floor(xl[0] - 0.5), j0y = (int64_t)floor(xl[1] - 0.5);
+        for (int c = 0; c < 4; ++c) {
+            int x = 0, y = 0, z = 0;
+            double v[4];
+            if (corner_map(g, per_x, geo.inflow, zero3, j0x + (c >> 1), j0y + (c & 1), 0, x, y, z,
+                           v) == MA_OWNED)
+                geo.skey[(int64_t)x * g.ny + y] = row_key_of(geo.tag, p * 4 + c);
         }
     }
 }

@@ -82,6 +82,7 @@ struct lbw_domain {
     cudaEvent_t ev_ready_prev = nullptr;  // ... of the step before
     bool touched = true;              // state changed by a call since the last step
     bool sweep_alt = true;            // alternate the interior plane order (LBW_SWEEP_ALT)
+    bool fused = false;               // one fused launch per actuator step when eligible (LBW_FUSED=1)
     // x-slab neighbours (lbw_peer.cu): side 0 = lo (x-1), side 1 = hi (x+1)
     bool linked = false;
     int nb_rank[2] = {-1, -1};
@@ -119,6 +120,14 @@ int alm_check_gate(lbw_domain* d);
 bool alm_gate(lbw_domain* d, int64_t m, const uint32_t** flag, uint32_t* value,
               const int32_t** box, cudaEvent_t* kin_event);
 ForceView alm_force_view(const lbw_domain* d, int64_t m);
+// Fused step (lbw_fused.cuh): one launch per step -- sweep m, point forces
+// of step m, kinematics + geometry of step m+2 -- on a single slab with
+// device kinematics and <= 64 points (no disks, no caller body force).
+bool alm_fused_eligible(const lbw_domain* d);
+int alm_fused_launch(lbw_domain* d, bool pull, ForceView* fv_out);
+// the previous step was a fused launch (its point forces are written inside
+// that launch: a standalone chain must wait for all of it)
+bool alm_after_fused(const lbw_domain* d);
 // Wait for queued actuator work and forget any prelaunched step (the
 // caller is about to change state it reads).
 int alm_invalidate(lbw_domain* d);

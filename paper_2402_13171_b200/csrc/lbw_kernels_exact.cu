@@ -2,8 +2,16 @@
 // Compiled with -fmad=false: no FMA contraction anywhere in this TU.
 #define LBW_FAST 0
 #include "lbw_sweep.cuh"
+#include "lbw_fused.cuh"
 
 namespace lbw {
+
+cudaError_t launch_fused_exact(int op, bool pull, const FusedArgs& a, size_t smem,
+                               cudaStream_t s) {
+    const cudaError_t e = launch_fused<4>(op, pull, a, smem, s);
+    count_launch();
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
 
 cudaError_t launch_sweep_exact(int op, bool pull, const SweepArgs& a, cudaStream_t s) {
     const dim3 blk = sweep_block(a.g);

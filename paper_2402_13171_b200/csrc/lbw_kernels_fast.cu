@@ -4,8 +4,15 @@
 #include <cstdlib>
 
 #include "lbw_sweep.cuh"
+#include "lbw_fused.cuh"
 
 namespace lbw {
+
+cudaError_t launch_fused_fast(int op, bool pull, const FusedArgs& a, size_t smem, cudaStream_t s) {
+    const cudaError_t e = launch_fused<5>(op, pull, a, smem, s);
+    count_launch();
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
 
 cudaError_t launch_sweep_fast(int op, bool pull, const SweepArgs& a, cudaStream_t s) {
     const dim3 blk = sweep_block(a.g);

@@ -247,7 +247,11 @@ __device__ __forceinline__ void actuator_force_k(const ForceView& fv, int64_t xg
             if (dc[2 * kw + t] == z) {
                 const double w = __dmul_rn(wxy, dw[2 * kw + t]);
                 for (int c = 0; c < 3; ++c)
-                    F[c] = (double)(T)__dadd_rn(F[c], __dmul_rn(w, fv.flat[p * 3 + c]));
+                    // flat may have been written earlier in this very launch
+                    // (fused step): a volatile load never hits a stale L1
+                    // line (generic: the K4 copy of the view is in smem)
+                    F[c] = (double)(T)__dadd_rn(
+                        F[c], __dmul_rn(w, *(const volatile double*)(fv.flat + p * 3 + c)));
             }
         }
     }

@@ -11,7 +11,7 @@ mkdir -p $out
 nvidia-smi topo -m > $out/topo.txt 2>&1
 for n in 2 4 8; do
   [ $n -gt $N ] && break
-  /usr/bin/time -f "%e s" timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$n \
+  timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$n \
     --master-addr=127.0.0.1 --master-port=$((29500+n)) tests/mgpu_check.py > $out/mgpu_check_$n.log 2>&1
   echo "mgpu_check n=$n rc=$?" | tee -a $out/summary.txt
 done

@@ -1,6 +1,7 @@
 """Per-step wall time on a small domain (64^3, the reference's test_07
 case): Python step() loop vs one lbw_domain_step(n) call, with and without
 the rotor."""
+import os
 import sys
 import time
 
@@ -28,7 +29,8 @@ def make(turbine, arithmetic, n=64):
 N = 400
 for n in ([int(a) for a in sys.argv[1:]] or (64, 128)):
     for arith in ("exact", "fast"):
-        for turb in (False, True):
+        for turb, fused in ((False, "1"), (True, "0"), (True, "1")):
+            os.environ["LBW_FUSED"] = fused   # read at domain creation
             sim = make(turb, arith, n)
             lib = _lib.load()
             for _ in range(20):
@@ -47,6 +49,6 @@ for n in ([int(a) for a in sys.argv[1:]] or (64, 128)):
             lib.lbw_domain_step(sim._domain, 10)
             lib.lbw_domain_sync(sim._domain)
             launches = (lib.lbw_kernel_launches() - l0) / 10
-            print(f"{n}^3 {arith:5s} turbine={turb!s:5s}: step() {py:7.1f} us/step  "
+            print(f"{n}^3 {arith:5s} turbine={turb!s:5s} fused={fused}: step() {py:7.1f} us/step  "
                   f"domain_step(N) {c:7.1f} us/step  launches/step {launches:.1f}", flush=True)
             sim.close()
