@@ -209,6 +209,12 @@ int lbw_domain_set_step_index(lbw_domain* d, int64_t step);
  * when a non-finite macro was seen, 0 when none (so far), <0 on error. */
 int lbw_domain_poll_nonfinite(lbw_domain* d, int wait, int64_t* step, int64_t* cell3,
                               int32_t* field);
+/* After a non-finite report of the last step: present the state the
+ * reference leaves when _check_finite raises right after the collide
+ * (sim.py:254-262, 281; run.abort: immediate) -- downloads return that
+ * step's post-collision populations, not streamed.  Waits for queued work
+ * and drops any actuator step queued ahead. */
+int lbw_domain_hold_collided(lbw_domain* d);
 int lbw_domain_sync(lbw_domain* d);
 
 /* Sweep (K1) timing with CUDA events on the domain stream, for roofline

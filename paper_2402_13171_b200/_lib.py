@@ -153,6 +153,7 @@ SIGNATURES = {
     "lbw_domain_step_index": (_I64, [_VP]),
     "lbw_domain_set_step_index": (_I, [_VP, _I64]),
     "lbw_domain_poll_nonfinite": (_I, [_VP, _I, _c_i64_p, _c_i64_p, _c_i32_p]),
+    "lbw_domain_hold_collided": (_I, [_VP]),
     "lbw_domain_sync": (_I, [_VP]),
     "lbw_domain_sweep_timing": (_I, [_VP, _I]),
     "lbw_domain_sweep_time": (_I, [_VP, _c_double_p, _c_i64_p]),

@@ -809,6 +809,20 @@ int lbw_domain_poll_nonfinite(lbw_domain* d, int wait, int64_t* step, int64_t* c
     return 1;
 }
 
+int lbw_domain_hold_collided(lbw_domain* d) {
+    LBW_REQ(d, "null domain");
+    LBW_CK(cudaSetDevice(d->device));
+    LBW_CK(cudaStreamSynchronize(d->stream));
+    int rc = alm_invalidate(d);
+    if (rc) return rc;
+    // buf[cur] holds the last collide's output; marking it pre-collision
+    // makes downloads return it as is (no stream) -- the reference's f after
+    // the abort -- and a further step collides it again, as the reference's
+    // next step() would.  The sampled macro (msrc) stays that collide's.
+    d->state_pre = true;
+    return LBW_OK;
+}
+
 int lbw_domain_sync(lbw_domain* d) {
     LBW_REQ(d, "null domain");
     LBW_CK(cudaSetDevice(d->device));

@@ -46,13 +46,40 @@ def ghosted_macro(sim, macro):
     return g
 
 
-def interpolate(gmacro, x_lat):
-    """Trilinear sample of a ghosted single-block macro (actuator.py:70-93)."""
+class CubeSource:
+    """A sparse ghosted macro field: only the cells of given sampling cubes,
+    keyed by ghosted global index (i, j, k) (interior cell x <-> i = x + 1).
+    Multi-GPU output ticks gather just these cells to rank 0 instead of the
+    whole lattice; cubes come out as the same (2,2,2,4) arrays a dense
+    ghosted field gives, so the samples are bit-identical."""
+
+    def __init__(self, cells):
+        self.cells = cells
+
+    def cube(self, lx, ly, lz):
+        out = np.empty((2, 2, 2, 4))
+        for a in range(2):
+            for b in range(2):
+                for c in range(2):
+                    out[a, b, c] = self.cells[(lx + a, ly + b, lz + c)]
+        return out
+
+
+def _cube_origin(x_lat):
     x = np.asarray(x_lat, dtype=np.float64)
     j0 = np.floor(x - 0.5).astype(np.int64)
-    t = x - 0.5 - j0
-    lx, ly, lz = j0 + 1
-    cube = gmacro[lx:lx + 2, ly:ly + 2, lz:lz + 2, :]
+    return x, j0, x - 0.5 - j0
+
+
+def interpolate(gmacro, x_lat):
+    """Trilinear sample of a ghosted single-block macro (actuator.py:70-93);
+    gmacro is a dense ghosted array or a CubeSource."""
+    x, j0, t = _cube_origin(x_lat)
+    lx, ly, lz = (int(v) for v in j0 + 1)
+    if isinstance(gmacro, CubeSource):
+        cube = gmacro.cube(lx, ly, lz)
+    else:
+        cube = gmacro[lx:lx + 2, ly:ly + 2, lz:lz + 2, :]
     wx = np.array([1.0 - t[0], t[0]])
     wy = np.array([1.0 - t[1], t[1]])
     wz = np.array([1.0 - t[2], t[2]])
@@ -69,6 +96,67 @@ def _sample_velocity(sim, gmacro, pos_m):
     sim.grid.owner_block_of_position(lat)
     _, u_lat = interpolate(gmacro, lat)
     return sim.units.velocity_to_physical(u_lat)
+
+
+def _probe_lattice_positions(sim, probe):
+    """Lattice positions (wrapped on periodic axes) a position probe samples,
+    in the order probe_rows visits them."""
+    Lx, Ly, Lz = sim.cfg.domain_length_m()
+    if probe.kind == "axial_line":
+        y0 = probe.y_m if probe.y_m is not None else 0.5 * Ly
+        z0 = probe.z_m if probe.z_m is not None else 0.5 * Lz
+        pos = [((i + 0.5) * Lx / probe.samples, y0, z0) for i in range(probe.samples)]
+    elif probe.kind == "radial_profile":
+        z0 = probe.z_m if probe.z_m is not None else 0.5 * Lz
+        pos = [(probe.x_m, (j + 0.5) * Ly / probe.samples, z0) for j in range(probe.samples)]
+    else:
+        return []
+    L = np.asarray(sim.grid.global_dims, dtype=np.float64)
+    periodic = np.asarray(sim.grid.periodicity, dtype=bool)
+    out = []
+    for p in pos:
+        lat = np.asarray(p, dtype=np.float64) / sim.units.dx
+        out.append(np.where(periodic, np.mod(lat, L), lat))
+    return out
+
+
+def probe_cube_cells(sim):
+    """Ghosted global indices of every cell the position probes' sampling
+    cubes read (sorted)."""
+    need = set()
+    for probe in sim.cfg.probes:
+        for lat in _probe_lattice_positions(sim, probe):
+            _, j0, _ = _cube_origin(lat)
+            lx, ly, lz = (int(v) for v in j0 + 1)
+            for a in range(2):
+                for b in range(2):
+                    for c in range(2):
+                        need.add((lx + a, ly + b, lz + c))
+    return sorted(need)
+
+
+def ghost_source(sim, key):
+    """Where ghosted_macro takes cell `key` (ghosted global index) from:
+    ("cell", (x, y, z)) of the interior, or ("const", 4-vector) -- the same
+    periodic-wrap / inflow / outflow / (1,0,0,0) rules."""
+    dims = tuple(sim.grid.global_dims)
+    per = sim.grid.periodicity
+    gi, gj, gk = key
+    if sim.boundary.kind == "velocity_inflow_outflow" and sim.step_index > 0:
+        if gi == 0:
+            return "const", np.concatenate([[1.0], np.asarray(sim.boundary.u_in_lat, float)])
+        if gi == dims[0] + 1:
+            gi = dims[0]
+    idx = []
+    for axis, g in enumerate((gi, gj, gk)):
+        i = g - 1
+        if 0 <= i < dims[axis]:
+            idx.append(i)
+        elif per[axis]:
+            idx.append(i % dims[axis])
+        else:
+            return "const", np.array([1.0, 0.0, 0.0, 0.0])
+    return "cell", tuple(idx)
 
 
 def probe_rows(sim, probe, gmacro=None):
@@ -195,14 +283,18 @@ def write_field_vtk(path, sim):
     return path
 
 
-def probe_tick(sim):
+def probe_tick(sim, gmacro=None):
+    """Probe CSVs (+ running averages) and the VTK dump of one output tick
+    (sim.py:304-333).  gmacro: the sampled field (dense ghosted array or
+    CubeSource); default: this simulation's macro, downloaded and ghosted."""
     cfg = sim.cfg
     if not (cfg.probes or cfg.vtk):
         return
     if not sim._macro_fresh:
         sim._recompute_moments()
     os.makedirs(cfg.output_dir, exist_ok=True)
-    gmacro = ghosted_macro(sim, sim.fields[0].download_macro())
+    if gmacro is None and any(p.kind != "blade_loads" for p in cfg.probes):
+        gmacro = ghosted_macro(sim, sim.fields[0].download_macro())
     for probe in cfg.probes:
         header, rows = probe_rows(sim, probe, gmacro)
         write_probe_csv(os.path.join(cfg.output_dir, f"{probe.name}_{sim.step_index:08d}.csv"),

@@ -51,6 +51,41 @@ def _dist():
     return dist
 
 
+def exchange_neighbour_blobs(blob, rank, nranks, periodic_x, group=None):
+    """Every rank publishes its handle blob; returns the (lo, hi) neighbours'
+    blobs (None across a non-periodic face)."""
+    blobs = [None] * nranks
+    _dist().all_gather_object(blobs, blob, group=group)
+    lo, hi = slab_neighbours(rank, nranks, periodic_x)
+    return (blobs[lo] if lo >= 0 else None), (blobs[hi] if hi >= 0 else None)
+
+
+def gather_probe_cells(sim, macro, x0, rank, nranks, group=None):
+    """The cells of the position probes' sampling cubes, each sent by the
+    rank owning it (macro: this rank's slab, first global plane x0), merged
+    with the constant ghost values on rank 0 into an output.CubeSource
+    (None on the other ranks)."""
+    from . import output
+    keys = output.probe_cube_cells(sim)
+    mine = {}
+    for key in keys:
+        kind, src = output.ghost_source(sim, key)
+        if kind == "cell" and x0 <= src[0] < x0 + macro.shape[0]:
+            mine[key] = np.array(macro[src[0] - x0, src[1], src[2]])
+    parts = [None] * nranks if rank == 0 else None
+    _dist().gather_object(mine, parts, dst=0, group=group)
+    if rank != 0:
+        return None
+    cells = {}
+    for part in parts:
+        cells.update(part)
+    for key in keys:
+        kind, src = output.ghost_source(sim, key)
+        if kind == "const":
+            cells[key] = src
+    return output.CubeSource(cells)
+
+
 class SlabSimulation(Simulation):
     """Simulation of one x-slab, linked to its neighbours on other GPUs."""
 
@@ -67,11 +102,10 @@ class SlabSimulation(Simulation):
         buf = (ctypes.c_char * n)()
         size = ctypes.c_int64(n)
         _lib.check(lib.lbw_domain_export_handle(self._domain, buf, ctypes.byref(size)), "export")
-        blobs = [None] * self.nranks
-        dist.all_gather_object(blobs, bytes(buf[:size.value]), group=self._group)
-        lo, hi = slab_neighbours(self.rank, self.nranks, self.cfg.periodicity[0])
-        lo_b = ctypes.create_string_buffer(blobs[lo], len(blobs[lo])) if lo >= 0 else None
-        hi_b = ctypes.create_string_buffer(blobs[hi], len(blobs[hi])) if hi >= 0 else None
+        lo, hi = exchange_neighbour_blobs(bytes(buf[:size.value]), self.rank, self.nranks,
+                                          self.cfg.periodicity[0], self._group)
+        lo_b = ctypes.create_string_buffer(lo, len(lo)) if lo is not None else None
+        hi_b = ctypes.create_string_buffer(hi, len(hi)) if hi is not None else None
         _lib.check(lib.lbw_domain_import_peers(self._domain, lo_b, hi_b), "import peers")
         dist.barrier(group=self._group)
 
@@ -134,26 +168,36 @@ class SlabSimulation(Simulation):
 
     # ------------------------------------------------------------ output
     def _probe_tick(self):
-        """Output tick of the whole lattice (output.py:33-167): the slabs'
-        macro (and force, for VTK) fields and the owners' actuator results
-        are gathered on rank 0, which writes the same files a single-GPU run
-        writes."""
+        """Output tick of the whole lattice (output.py:33-167) written by
+        rank 0, files identical to a single-GPU run.  Position probes only
+        need the cells of their sampling cubes: each rank sends rank 0 the
+        ones it owns (a few kB), not its field.  The VTK dump is the whole
+        field by definition: the slabs' macro and force fields are gathered
+        to rank 0 only."""
         from . import output
         cfg = self.cfg
         if not (cfg.probes or cfg.vtk):
             return
+        dist = _dist()
         if not self._macro_fresh:
             self._recompute_moments()
         macro = self.fields[0].download_macro()
-        force = self.fields[0].download_force() if cfg.vtk else None
         results = self.alm_results_global() if self.points else None
-        parts = [None] * self.nranks
-        _dist().all_gather_object(parts, (macro, force), group=self._group)
+        cubes = gather_probe_cells(self, macro, int(self.grid.bounds[self.rank]), self.rank,
+                                   self.nranks, self._group)
+        fields = None
+        if cfg.vtk:
+            force = self.fields[0].download_force()
+            fields = [None] * self.nranks if self.rank == 0 else None
+            dist.gather_object((macro, force), fields, dst=0, group=self._group)
         if self.rank == 0:
-            gm = np.concatenate([p[0] for p in parts], axis=0)
-            gf = np.concatenate([p[1] for p in parts], axis=0) if cfg.vtk else None
-            output.probe_tick(_GlobalView(self, gm, gf, results))
-        _dist().barrier(group=self._group)
+            gm = gf = None
+            if cfg.vtk:
+                gm = np.concatenate([f[0] for f in fields], axis=0)
+                gf = np.concatenate([f[1] for f in fields], axis=0)
+            view = _GlobalView(self, gm, gf, results)
+            output.probe_tick(view, gmacro=cubes)
+        dist.barrier(group=self._group)
 
     def _write_report(self, report):
         if self.rank == 0:
@@ -219,5 +263,5 @@ def run_slab_simulation(cfg, group=None, kinematics=None):
         sim.close()
 
 
-__all__ = ["SlabGrid", "SlabSimulation", "first_nonfinite", "run_slab_simulation",
-           "slab_neighbours"]
+__all__ = ["SlabGrid", "SlabSimulation", "exchange_neighbour_blobs", "first_nonfinite",
+           "gather_probe_cells", "run_slab_simulation", "slab_neighbours"]

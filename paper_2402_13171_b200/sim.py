@@ -414,6 +414,18 @@ class Simulation:
             raise NumericalAbort(int(step.value), tuple(int(c) for c in cell),
                                  "density" if field.value == 0 else "velocity")
 
+    def _abort_now(self):
+        """run.abort: immediate -- wait for this step's collide and, when it
+        produced a non-finite macro value, leave the state the reference
+        leaves (sim.py:254-262, 281): the post-collision populations of the
+        aborted step, not streamed, step_index not advanced."""
+        try:
+            self._poll(wait=True)
+        except NumericalAbort:
+            _lib.check(_lib.load().lbw_domain_hold_collided(self._domain), "abort")
+            self._macro_fresh = False
+            raise
+
     def _warn_clamps(self):
         if not self.points or not self._polar_list:
             return
@@ -436,7 +448,10 @@ class Simulation:
         _lib.check(lib.lbw_domain_step(self._domain, 1), "step")
         t.stop_phase()
         self._results = None
-        self._poll(wait=False)
+        if self.cfg.abort == "immediate":
+            self._abort_now()
+        else:
+            self._poll(wait=False)
         if self.cfg.topologies:
             if host_kin or not self.points:
                 t.start_phase("turbine")
@@ -458,7 +473,7 @@ class Simulation:
         n = int(n)
         if n <= 0:
             return
-        if self.points and self.kinematics == "host":
+        if (self.points and self.kinematics == "host") or self.cfg.abort == "immediate":
             for _ in range(n):
                 self.step()
             return

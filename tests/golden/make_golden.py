@@ -21,6 +21,10 @@ Fixtures (numpy .npz, fp64):
   single.npz     precision: single TGV, inflow/outflow BGK and rotor runs
   disk_wake.npz  (--wake) test_05's reduced wake case at 8 and 12 cells per
                  diameter: deficit, axis / plane-mean u_x, ring forces
+  output.npz     (--output) the files Simulation.run() writes (output.py:44-167):
+                 probe CSVs (axial_line, radial_profile, running averages) and
+                 the VTK dump of a perturbed inflow/outflow run, and the
+                 blade_loads CSVs of a rotor run, verbatim (text)
 """
 
 import os
@@ -425,8 +429,78 @@ def gen_disk_wake(tmp):
     np.savez_compressed(os.path.join(HERE, "disk_wake.npz"), **out)
 
 
+OUTPUT_FLOW = {
+    "name": "outcase",
+    "domain": {"cells": [12, 10, 8], "periodicity": [False, True, True]},
+    "fluid": {"kinematic_viscosity": 0.3, "wind": [8.0, 0.5, -0.25]},
+    "resolution": {"cells_per_diameter": 8, "reference_diameter": 1.0, "mach": 0.1},
+    "run": {"steps": 6, "boundary": "velocity_inflow_outflow",
+            "collision": {"operator": "cumulant"}},
+    "output": {"cadence": 3, "vtk": True,
+               "probes": [{"kind": "axial_line", "name": "axial", "samples": 12,
+                           "average_from_step": 3},
+                          {"kind": "radial_profile", "name": "radial", "samples": 10,
+                           "x_m": 0.8, "z_m": 0.4},
+                          {"kind": "axial_line", "name": "offaxis", "samples": 7,
+                           "y_m": 0.3, "z_m": 0.9}]}}
+
+OUTPUT_ROTOR = {
+    "name": "outrotor",
+    "domain": {"cells": [16, 12, 12], "periodicity": [False, True, True]},
+    "fluid": {"kinematic_viscosity": 0.866, "wind": [8.0, 0.0, 0.0]},
+    "resolution": {"cells_per_diameter": 8, "reference_diameter": 1.0, "mach": 0.1},
+    "run": {"steps": 8, "boundary": "velocity_inflow_outflow",
+            "collision": {"operator": "cumulant"}},
+    "turbines": [{"file": "rotor.yaml", "position": [0.9, 0.75, 0.0]}],
+    "polars": [{"id": "sym", "file": "sym.csv"}],
+    "output": {"cadence": 4,
+               "probes": [{"kind": "blade_loads", "name": "loads", "turbine": 0,
+                           "component": "blade2", "average_from_step": 4},
+                          {"kind": "axial_line", "name": "wake", "samples": 16,
+                           "y_m": 0.75, "z_m": 0.0}]}}
+
+
+def gen_output(tmp):
+    """Simulation.run() of the reference with probes and VTK output; every
+    file it writes (except report.json, which holds timings) is stored as
+    text under '<case>/<file name>'."""
+    import copy
+    import json
+    out = {"rotor_yaml": np.array(ROTOR_YAML), "polar_csv": np.array(sym_polar_csv())}
+    for case, raw0 in (("flow", OUTPUT_FLOW), ("rotor", OUTPUT_ROTOR)):
+        out[f"{case}_raw"] = np.array(json.dumps(raw0))
+        raw = copy.deepcopy(raw0)
+        odir = os.path.join(tmp, "out_" + case)
+        raw["output"]["directory"] = odir
+        if case == "rotor":
+            with open(os.path.join(tmp, "rotor.yaml"), "w") as fh:
+                fh.write(ROTOR_YAML)
+            with open(os.path.join(tmp, "sym.csv"), "w") as fh:
+                fh.write(sym_polar_csv())
+        cfg = parse_config(raw, base_dir=tmp)
+        sim = Simulation(cfg)
+        if case == "flow":
+            rng = np.random.default_rng(29)
+            fld = sim.fields[0]
+            fld.interior[...] *= 1.0 + 0.02 * rng.uniform(-1, 1, fld.interior.shape)
+            out["flow_f0"] = _gather(sim)
+        sim.run()
+        sim.close()
+        for fn in sorted(os.listdir(odir)):
+            if fn == "report.json":
+                continue
+            with open(os.path.join(odir, fn)) as fh:
+                out[f"{case}/{fn}"] = np.array(fh.read())
+    np.savez_compressed(os.path.join(HERE, "output.npz"), **out)
+
+
 def main():
     import tempfile
+    if "--output" in sys.argv:
+        _kernels.warm_up()
+        with tempfile.TemporaryDirectory() as tmp:
+            gen_output(tmp)
+        return
     if "--single" in sys.argv:
         with tempfile.TemporaryDirectory() as tmp:
             gen_single(tmp)

@@ -515,3 +515,50 @@ def test_pdffield_collide_and_stream(gpu, dtype):
     dst = np.zeros_like(ref_f)
     orc.stream_pull_block(fld.f_next.astype(np.float64), dst)
     assert np.array_equal(fld.f[inner], dst[inner].astype(dtype))
+
+
+def test_immediate_abort_leaves_reference_state(gpu, tmp_path):
+    """run.abort: immediate -- the step that produces a non-finite macro
+    raises right after its collide (sim.py:254-262, 281): step_index not
+    advanced, populations post-collision and not streamed, exactly the
+    oracle's state when its collide trips the same check (the reference's
+    chord: 1e308 fault, test_sim.py:116-138, here on a fast-growing blade
+    so the fault appears after a few healthy steps)."""
+    from tests.scenarios import oracle_for
+    (tmp_path / "blow.yaml").write_text("""
+name: blow
+components:
+  - name: hub
+    position: [1.0, 1.0, 1.0]
+    rotation: {axis: [1.0, 0.0, 0.0], rate_rad_per_s: 40.0}
+  - name: blade
+    parent: hub
+    discretization: {type: line, points: 3, r_end: 0.5, chord: 1.0e+308, polar: flat}
+""")
+    (tmp_path / "flat.csv").write_text("alpha_deg,cl,cd\n-10,1.0,0.0\n10,1.0,0.0\n")
+    raw = {"domain": {"cells": [16, 16, 16]},
+           "fluid": {"kinematic_viscosity": 5.0, "wind": [8.0, 0.0, 0.0]},
+           "resolution": {"cells_per_diameter": 8, "reference_diameter": 2.0, "mach": 0.1},
+           "run": {"steps": 10, "abort": "immediate"},
+           "output": {"directory": str(tmp_path / "out")},
+           "turbines": [{"file": "blow.yaml"}], "polars": [{"id": "flat", "file": "flat.csv"}]}
+    cfg = parse_config(raw, base_dir=str(tmp_path))
+    sim = Simulation(cfg, kinematics="host")
+    ref = oracle_for(sim)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        with pytest.raises(NumericalAbort) as exc:
+            for _ in range(10):
+                sim.refresh_points()
+                kin = sim._kin.copy()
+                try:
+                    ref.step(kin)
+                except FloatingPointError as e:
+                    ref_abort = e.args[0]
+                sim.step()
+    assert exc.value.step == ref_abort[0] == sim.step_index
+    assert tuple(exc.value.cell) == tuple(ref_abort[1])
+    got = sim.fields[0].interior
+    np.testing.assert_array_equal(got, ref.interior)      # NaN where the oracle has NaN
+    assert np.isnan(got).any()
+    sim.close()

@@ -83,6 +83,74 @@ def test_gloo_two_rank_consensus():
         np.testing.assert_array_equal(blade[1::2], 2.0)
 
 
+def _wiring_worker(rank, world, port, q):
+    """Handle-blob exchange and neighbour wiring (SlabSimulation._link) and
+    the sparse probe-cube gather of an output tick (SlabSimulation.
+    _probe_tick), over gloo with fake blobs and a host macro field."""
+    import types
+
+    import torch.distributed as dist
+
+    from paper_2402_13171_b200 import output, parse_config
+    from paper_2402_13171_b200.halo import BoundarySpec
+    from paper_2402_13171_b200.parallel import exchange_neighbour_blobs, gather_probe_cells
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = {}
+    for periodic in (False, True):
+        blob = f"handle-of-rank-{rank}".encode() * (rank + 1)
+        out[periodic] = exchange_neighbour_blobs(blob, rank, world, periodic)
+    raw = {"domain": {"cells": [3 * world + 2, 9, 7], "periodicity": [False, True, True]},
+           "fluid": {"kinematic_viscosity": 0.3, "wind": [8.0, 0.5, -0.25]},
+           "resolution": {"cells_per_diameter": 8, "reference_diameter": 1.0, "mach": 0.1},
+           "run": {"boundary": "velocity_inflow_outflow"},
+           "output": {"probes": [{"kind": "axial_line", "name": "a", "samples": 23},
+                                 {"kind": "radial_profile", "name": "r", "samples": 9,
+                                  "x_m": 0.31}]}}
+    cfg = parse_config(raw)
+    grid = SlabGrid(cfg.cells, cfg.periodicity, world, rank)
+    sim = types.SimpleNamespace(cfg=cfg, units=cfg.units, grid=grid, step_index=4,
+                                boundary=BoundarySpec("velocity_inflow_outflow",
+                                                      u_in_lat=(0.03, 0.0, 0.0)))
+    macro = np.random.default_rng(11).uniform(0.5, 1.5, tuple(cfg.cells) + (4,))
+    x0, x1 = grid.bounds[rank], grid.bounds[rank + 1]
+    cubes = gather_probe_cells(sim, macro[x0:x1], x0, rank, world)
+    ok = None
+    if rank == 0:
+        dense = output.ghosted_macro(sim, macro)
+        ok = all(np.array_equal(output.probe_rows(sim, p, dense)[1],
+                                output.probe_rows(sim, p, cubes)[1]) for p in cfg.probes)
+    q.put((rank, out, ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_neighbour_wiring_and_probe_gather(world):
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    procs = [ctx.Process(target=_wiring_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        rank, out, ok = q.get(timeout=120)
+        res[rank] = (out, ok)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    blob = lambda r: f"handle-of-rank-{r}".encode() * (r + 1)   # noqa: E731
+    for rank in range(world):
+        for periodic in (False, True):
+            lo, hi = slab_neighbours(rank, world, periodic)
+            got = res[rank][0][periodic]
+            assert got == (blob(lo) if lo >= 0 else None, blob(hi) if hi >= 0 else None)
+    assert res[0][1] is True
+
+
 @pytest.mark.gpu
 def test_slabs_bitwise_equal_single_gpu(gpu):
     n = gpu.lbw_device_count()
@@ -97,3 +165,47 @@ def test_slabs_bitwise_equal_single_gpu(gpu):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0
+
+
+# ------------------------------------------------ multi-GPU output ticks
+# SlabSimulation._probe_tick sends rank 0 only the cells of the position
+# probes' sampling cubes (output.CubeSource); the samples must equal the
+# ones a dense ghosted field gives, bit for bit, for every ghost rule.
+
+@pytest.mark.parametrize("boundary,periodic,step", [
+    ("velocity_inflow_outflow", (False, True, True), 3),
+    ("velocity_inflow_outflow", (False, True, False), 0),
+    ("periodic", (True, True, True), 5),
+    ("periodic", (True, False, True), 2),
+])
+def test_sparse_probe_cubes_equal_dense_ghosted_field(boundary, periodic, step):
+    import types
+
+    from paper_2402_13171_b200 import output, parse_config
+    from paper_2402_13171_b200.halo import BoundarySpec
+    raw = {"domain": {"cells": [13, 9, 7], "periodicity": list(periodic)},
+           "fluid": {"kinematic_viscosity": 0.3, "wind": [8.0, 0.5, -0.25]},
+           "resolution": {"cells_per_diameter": 8, "reference_diameter": 1.0, "mach": 0.1},
+           "run": {"boundary": boundary},
+           "output": {"probes": [
+               {"kind": "axial_line", "name": "a", "samples": 29},
+               {"kind": "axial_line", "name": "b", "samples": 11, "y_m": 0.05, "z_m": 0.83},
+               {"kind": "radial_profile", "name": "r", "samples": 17, "x_m": 1.59, "z_m": 0.02},
+               {"kind": "radial_profile", "name": "s", "samples": 5, "x_m": 0.01}]}}
+    cfg = parse_config(raw)
+    sim = types.SimpleNamespace(
+        cfg=cfg, units=cfg.units, grid=SlabGrid(cfg.cells, cfg.periodicity, 1, 0),
+        boundary=BoundarySpec(boundary, u_in_lat=(0.03, -0.01, 0.002)), step_index=step)
+    rng = np.random.default_rng(5)
+    macro = rng.uniform(0.5, 1.5, tuple(cfg.cells) + (4,))
+    dense = output.ghosted_macro(sim, macro)
+    cells = {}
+    for key in output.probe_cube_cells(sim):
+        kind, src = output.ghost_source(sim, key)
+        cells[key] = macro[src] if kind == "cell" else src
+        assert np.array_equal(cells[key], dense[key]), key
+    sparse = output.CubeSource(cells)
+    for probe in cfg.probes:
+        h1, r1 = output.probe_rows(sim, probe, dense)
+        h2, r2 = output.probe_rows(sim, probe, sparse)
+        assert h1 == h2 and np.array_equal(r1, r2)
