@@ -35,6 +35,8 @@
 
 #define LBW_FAST 0
 #include "lbw_sweep.cuh"
+#define LBW_CHAIN_FN __device__ __forceinline__
+#define LBW_CHAIN_COLD __device__ __forceinline__
 #include "lbw_chain.cuh"
 
 namespace lbw {
@@ -44,7 +46,7 @@ struct AlmState {
     double *chord = nullptr, *elen = nullptr, *twist = nullptr;
     int32_t *polar_index = nullptr, *polar_offset = nullptr, *polar_rows = nullptr;
     double *p_alpha = nullptr, *p_cl = nullptr, *p_cd = nullptr;
-    double* kin = nullptr;       // (3,P,18): slot m % 3 (kinematics run a step ahead)
+    double* kin = nullptr;       // (kSlots,P,18): slot m % kSlots (kinematics run ahead)
     double *samples = nullptr;   // (2,P,4)
     double *blade = nullptr;     // (2,P,3)
     double *flat = nullptr;      // (P,3)
@@ -74,12 +76,12 @@ struct AlmState {
     cudaStream_t kin_stream = nullptr;
     cudaEvent_t ev_kin_done = nullptr;
     cudaEvent_t ev_chain_done[2] = {nullptr, nullptr};  // chain of a step parity done
-    int64_t kin_valid[3] = {-1, -1, -1};  // step whose kinematics kin[slot] holds
+    int64_t kin_valid[kSlots] = {-1, -1, -1, -1, -1, -1};  // step whose kinematics kin[slot] holds
     // sweep gate (alm_gate): chain-done flag, per-slot x range of each step's
     // deposits and sampling, KK completion per slot
     uint32_t* gate_flag = nullptr;
     int32_t* gate_box = nullptr;     // (3, 2) local planes, inclusive
-    cudaEvent_t ev_kin_step[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t ev_kin_step[kSlots] = {};
     // per-step blade-force series (lbw_alm_record_loads)
     double* h_loads = nullptr;   // pinned (loads_cap, P, 3)
     double* d_loads = nullptr;   // its device mapping (the fused step writes it in-kernel)
@@ -102,7 +104,10 @@ struct AlmState {
     int32_t k_nlevels = 0;
     bool kin_static_ready = false;   // static components' state computed once
     size_t kin_smem = 0;
-    // fused step (lbw_fused.cuh): per-step geometry in slots j % 3, sample
+    long long* k_img_prm = nullptr;    // constant smem image of the kinematics CTA (kinematics_cta)
+    long long* k_img_tail = nullptr;
+    int32_t k_img_words = 0;
+    // fused step (lbw_fused.cuh): per-step geometry in slots j % kSlots, sample
     // pools by parity, task counters of two consecutive launches
     bool fs_alloc = false;
     int32_t* fs_dep_cell = nullptr;   // (3,P,3,kw)
@@ -113,10 +118,18 @@ struct AlmState {
     uint32_t* fs_ctr = nullptr;       // (2, 2)
     int64_t fs_next = -1;             // step the pipeline is primed for
     unsigned long long* fs_prof = nullptr;   // (256, 8) timeline ring (LBW_FUSED_PROF)
+    // chain B (flag-ordered, alm_chainb_*): flags [0] KK done (j+1), [1] K4
+    // done (j+1), [2] samples of step j stored (j), [3] pool-tile count,
+    // [4] K4 count, [5] a bounded wait expired; pool tiles per geometry slot
+    uint32_t* cb_flags = nullptr;
+    int32_t* cb_pool_tiles = nullptr;   // (kSlots)
+    int32_t* cb_box_h = nullptr;        // (kSlots, 2) pinned, device-mapped: [x_first, x_len] hint per KK
+    int32_t* cb_box_d = nullptr;
+    int64_t cb_next = -1;               // step the chain-B pipeline is primed for
     int64_t fs_prof_n = 0;
     std::vector<void*> allocs;
 
-    // device view for step m: outputs by parity, kinematics by m % 3
+    // device view for step m: outputs by parity, kinematics by m % kSlots
     AlmDev dev(int64_t m) const {
         const int parity = (int)(m & 1);
         AlmDev a;
@@ -134,7 +147,7 @@ struct AlmState {
         a.rho_ref = rho_ref;
         a.dt2 = dt2;
         a.den = den;
-        a.kin = kin + (size_t)(m % 3) * n * kKin;
+        a.kin = kin + (size_t)(m % kSlots) * n * kKin;
         a.samples = samples + (size_t)parity * n * 4;
         a.blade = blade + (size_t)parity * n * 3;
         a.flat = flat + (size_t)parity * n * 3;
@@ -189,6 +202,9 @@ struct AlmState {
         k.is_static = k_static;
         k.skip_static = 0;
         k.dx = k_dx;
+        k.img_prm = k_img_prm;
+        k.img_tail = k_img_tail;
+        k.img_tail_words = k_img_words;
         return k;
     }
 };
@@ -282,6 +298,245 @@ __global__ void k_fs_prime(KinDev k, AlmDev a, Geom g, int per_x, int advance, i
         __syncthreads();
     }
     fs_geometry(geo, a, g, per_x, (int)threadIdx.x, (int)blockDim.x);
+}
+
+// ---------------------------------------------------------------- chain B
+// Flags of the flag-ordered chain (AlmState::cb_flags): [0] kinematics of
+// step j done = j+1, [1] point forces (K4) of step j done = j+1, [2] force-
+// free sample sums of step j stored by sweep j-1 = j, [3] sample-tile count
+// of the running sweep, [4] K4 warp count, [5] a bounded wait expired,
+// [6] geometry of step j done = j+1 (published in step order).
+
+// Geometry of step j (one CTA, kinematics of j done): deposit geometry and
+// row keys (fs_geometry), the number of sweep tiles holding rows of step j's
+// sampling cubes, the plane-order hint, then "geometry(j) done" = j+1 once
+// geometry(j-1) has published (flags are maxima: publish in step order).
+__device__ __forceinline__ void cb_geometry_body(const AlmDev& a, const Geom& g, int per_x,
+                                                 const FsGeom& geo, int ty, int tiles_x,
+                                                 int32_t* pool_tiles, uint32_t* flags,
+                                                 uint32_t value, int32_t* box_hint) {
+    __shared__ uint32_t pairs[4 * kOnTheFlyMaxPoints];
+    __shared__ uint32_t dup[4 * kOnTheFlyMaxPoints];
+    __shared__ int cnt, blo, bhi;
+    const int tid = (int)threadIdx.x, nthr = (int)blockDim.x;
+    const int nq = 4 * a.n;
+    if (tid == 0) {
+        cnt = 0;
+        blo = INT_MAX;
+        bhi = INT_MIN;
+    }
+    fs_geometry(geo, a, g, per_x, tid, nthr);   // synchronises the CTA
+    // sampling rows -> sweep tiles (x plane, y block), and the plane range
+    // of the points relative to point 0 (wrapped on a periodic x axis)
+    const double zero3[3] = {0.0, 0.0, 0.0};
+    const int64_t c0 = (int64_t)floor(a.kin[0]);
+    for (int q = tid; q < nq; q += nthr) {
+        const double* kr = a.kin + (int64_t)(q >> 2) * kKin;
+        const int c = q & 3;
+        const int64_t j0x = (int64_t)floor(kr[0] - 0.5), j0y = (int64_t)floor(kr[1] - 0.5);
+        int x = 0, y = 0, z = 0;
+        double v[4];
+        pairs[q] = corner_map(g, per_x, geo.inflow, zero3, j0x + (c >> 1), j0y + (c & 1), 0, x, y,
+                              z, v) == MA_OWNED
+                       ? ((uint32_t)x << 16) | (uint32_t)(y / ty)
+                       : 0xffffffffu;
+        dup[q] = 0u;
+        if (c == 0) {
+            int64_t dlt = (int64_t)floor(kr[0]) - c0;
+            if (per_x) dlt = ((dlt + g.nxg / 2) % g.nxg + g.nxg) % g.nxg - g.nxg / 2;
+            atomicMin(&blo, (int)dlt);
+            atomicMax(&bhi, (int)dlt);
+        }
+    }
+    __syncthreads();
+    // distinct tiles: every pair (r < q) compared once, spread over the CTA
+    const int npair = nq * (nq - 1) / 2;
+    for (int t = tid; t < npair; t += nthr) {
+        int q = (int)((1.0 + sqrt(1.0 + 8.0 * (double)t)) * 0.5);
+        while (q * (q - 1) / 2 > t) --q;
+        while ((q + 1) * q / 2 <= t) ++q;
+        const int r = t - q * (q - 1) / 2;
+        if (pairs[q] == pairs[r]) dup[q] = 1u;
+    }
+    __syncthreads();
+    for (int q = tid; q < nq; q += nthr)
+        if (pairs[q] != 0xffffffffu && !dup[q]) atomicAdd(&cnt, 1);
+    __syncthreads();
+    if (tid == 0) {
+        *pool_tiles = cnt * tiles_x;
+        gate_wait(flags + 6, value - 1u, reinterpret_cast<int32_t*>(flags + 5));
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags + 6), "r"(value) : "memory");
+        if (box_hint) {   // a hint in mapped host memory: after the release, no fence
+            const int h = a.halo_x + 1;
+            const int64_t first = c0 + blo - h - g.x0;
+            const int len = (int)min((int64_t)(bhi - blo + 2 * h + 1), (int64_t)g.nxl);
+            box_hint[0] = (int32_t)(((first % g.nxl) + g.nxl) % g.nxl);
+            box_hint[1] = len;
+        }
+    }
+}
+
+// Kinematics of step j (one CTA), then "kinematics(j) done" = j+1.
+__device__ __forceinline__ void cb_kin_body(const KinDev& k, const AlmDev& a, const Geom& g,
+                                            int per_x, int advance, int do_kin, uint32_t* flags,
+                                            uint32_t value, double* csm) {
+    const int tid = (int)threadIdx.x, nthr = (int)blockDim.x;
+    if (do_kin) kinematics_cta(k, a, g, per_x, advance, csm, tid, nthr);
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags), "r"(value) : "memory");
+    }
+}
+
+// priming: kinematics + geometry of step j in one CTA, serially
+__global__ void k_cb_kk(KinDev k, AlmDev a, Geom g, int per_x, int advance, int do_kin,
+                        FsGeom geo, int ty, int tiles_x, int32_t* pool_tiles, uint32_t* flags,
+                        uint32_t value, int32_t* box_hint) {
+    extern __shared__ double csm[];
+    LBW_TRACE_BEGIN(1, a.step);
+    cb_kin_body(k, a, g, per_x, advance, do_kin, flags, value, csm);
+    __syncthreads();
+    cb_geometry_body(a, g, per_x, geo, ty, tiles_x, pool_tiles, flags, value, box_hint);
+    LBW_TRACE_END(1, a.step);
+}
+
+struct CbChainArgs {
+    Geom g;
+    int32_t role;               // 0: K4(j), 1: kinematics(jk), 2: geometry(jk)
+    // K4(j): 4 points (warps) per CTA
+    AlmDev a;
+    MacroDev md;
+    FsPool pool;
+    int32_t use_pool;
+    const uint32_t* box_flag;   // sums of step j stored: *box_flag >= box_value
+    uint32_t box_value;
+    const int32_t* pool_tiles;  // of step j (0: nothing to wait for)
+    uint32_t* flags;            // chain-B flags
+    uint32_t k4_value;
+    // kinematics / geometry of step jk (one CTA)
+    int32_t kk_advance, kk_do_kin;
+    KinDev k;
+    AlmDev akk;
+    FsGeom geo;
+    int32_t per_x, ty, tiles_x;
+    int32_t* pool_tiles_kk;
+    uint32_t kin_value;         // jk + 1
+    uint32_t slot_value;        // the slot of step jk is free once box >= slot_value
+    int32_t* box_hint;          // (2) plane-order hint of step jk (mapped host memory)
+};
+
+// The chain of step j: three launches on the actuator stream -- K4(j),
+// kinematics(j+4), geometry(j+3) -- ordered only by the flags: each waits
+// in-kernel for what it reads, then lets the next launch on the stream be
+// scheduled (griddepcontrol.launch_dependents; never griddepcontrol.wait),
+// so only the kinematics (the turbine state advances step by step) and the
+// point forces (each step samples the previous step's forces) form serial
+// chains; the geometry of different steps overlaps.
+//   K4(j):     geometry(j) done; sums of step j stored by sweep j-1; before
+//              its force part, K4(j-1) done
+//   kin(jk):   kin(jk-1) done; the slot of step jk free (box >= jk-4: sweep
+//              jk-5 started, so sweep jk-6 -- the slot's last reader -- is done)
+//   geo(jk):   kin(jk) done; slot free as above
+__global__ void __launch_bounds__(128) k_cb_chain(CbChainArgs A) {
+    extern __shared__ double csm[];
+    const int tid = (int)threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int32_t* err = reinterpret_cast<int32_t*>(A.flags + 5);
+    if (A.role == 1) {
+        if (tid == 0) {
+            gate_wait(A.flags, A.kin_value - 1u, err);
+            gate_wait(A.box_flag, A.slot_value, err);
+        }
+        __syncthreads();
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        LBW_TRACE_BEGIN(1, A.akk.step);
+        cb_kin_body(A.k, A.akk, A.g, A.per_x, A.kk_advance, A.kk_do_kin, A.flags, A.kin_value, csm);
+        LBW_TRACE_END(5, A.akk.step);
+        return;
+    }
+    if (A.role == 2) {
+        if (tid == 0) {
+            gate_wait(A.flags, A.kin_value, err);
+            gate_wait(A.box_flag, A.slot_value, err);
+        }
+        __syncthreads();
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        cb_geometry_body(A.akk, A.g, A.per_x, A.geo, A.ty, A.tiles_x, A.pool_tiles_kk, A.flags,
+                         A.kin_value, A.box_hint);
+        LBW_TRACE_END(1, A.akk.step);
+        return;
+    }
+    // K4(j).  The force view of step j-1 (it completes the pooled sums) is
+    // staged in shared memory while the samples are being waited for.
+    double* sw = csm;                                          // (n, 3, kw) weights
+    double* sfl = sw + (size_t)A.a.n * 3 * A.a.kw;             // (n, 3) forces
+    int32_t* sdc = reinterpret_cast<int32_t*>(sfl + (size_t)A.a.n * 3);  // (n, 3, kw) cells
+    const bool stage = A.use_pool && A.pool.fv.npts > 0;
+    if (tid == 0) {
+        gate_wait(A.flags + 6, A.k4_value, err);   // geometry(j) done: flag >= j+1
+        if (A.use_pool && *(const volatile int32_t*)A.pool_tiles > 0)
+            gate_wait(A.box_flag, A.box_value, err);
+    }
+    __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int nd = stage ? A.a.n * 3 * A.a.kw : 0;
+    for (int i = tid; i < nd; i += (int)blockDim.x) {
+        sw[i] = A.pool.fv.dep_w[i];
+        sdc[i] = A.pool.fv.dep_cell[i];
+    }
+    const int p = (int)blockIdx.x * 4 + warp;
+    PointInputs in{};
+    if (p < A.a.n) in = load_point_inputs(A.a, p, lane);
+    if (A.use_pool) {
+        if (tid == 0) gate_wait(A.flags + 1, A.k4_value - 1u, err);   // K4(j-1): its forces
+        __syncthreads();
+        for (int i = tid; i < A.a.n * 3; i += (int)blockDim.x) sfl[i] = A.pool.fv.flat[i];
+        __syncthreads();
+    }
+    if (p >= A.a.n) return;   // uniform per warp
+    LBW_TRACE_BEGIN(2, A.a.step);
+#ifdef LBW_K4_PROF
+    in.t0 = in.t1 = clock64();
+#endif
+    FsPool pool = A.pool;
+    if (stage) {
+        pool.fv.dep_w = sw;
+        pool.fv.dep_cell = sdc;
+        pool.fv.flat = sfl;
+    }
+    ForceSet none{};
+    CubeArgs cube{};
+    point_warp(A.a, A.g, A.md, none, 0, cube, p, lane, in, A.use_pool ? &pool : nullptr, false);
+    __syncwarp();
+    if (lane == 0) {
+        // the last point's warp publishes "K4(j) done"
+        __threadfence();
+        const uint32_t done = atomicAdd(A.flags + 4, 1u) + 1u;
+        if (done == (uint32_t)A.a.n) {
+            A.flags[4] = 0u;
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(A.flags + 1), "r"(A.k4_value)
+                         : "memory");
+        }
+    }
+    LBW_TRACE_END(2, A.a.step);
+}
+
+// one chain launch; pdl: programmatic stream serialisation (actuator stream)
+static cudaError_t launch_cb_chain(const CbChainArgs& A, unsigned grid, size_t smem,
+                                   cudaStream_t st, bool pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(128, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_cb_chain, A);
 }
 
 // K5: one warp per deposit pair q.  The lowest pair touching a row owns it:
@@ -399,11 +654,13 @@ void alm_destroy(lbw_domain* d) {
     for (void* p : s->allocs) cudaFree(p);
     for (auto& e : s->ring_ev)
         if (e) cudaEventDestroy(e);
-    for (cudaEvent_t e : {s->ev_kin_done, s->ev_chain_done[0], s->ev_chain_done[1],
-                          s->ev_kin_step[0], s->ev_kin_step[1], s->ev_kin_step[2]})
+    for (cudaEvent_t e : {s->ev_kin_done, s->ev_chain_done[0], s->ev_chain_done[1]})
+        if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : s->ev_kin_step)
         if (e) cudaEventDestroy(e);
     if (s->kin_stream) cudaStreamDestroy(s->kin_stream);
     if (s->h_ring) cudaFreeHost(s->h_ring);
+    if (s->cb_box_h) cudaFreeHost(s->cb_box_h);
     if (s->h_loads) cudaFreeHost(s->h_loads);
     delete s;
     d->alm = nullptr;
@@ -411,7 +668,12 @@ void alm_destroy(lbw_domain* d) {
 
 bool alm_ready(const lbw_domain* d, int64_t m) { return d->alm->ready_step == m; }
 
+int alm_chainb_check(lbw_domain* d);
 int alm_check_gate(lbw_domain* d) {
+    {
+        int rc = alm_chainb_check(d);
+        if (rc) return rc;
+    }
     if (!alm_active(d) || !d->alm->gate_flag) return LBW_OK;
     int32_t err = 0;
     LBW_CK(cudaMemcpy(&err, d->alm->gate_flag + 1, sizeof(err), cudaMemcpyDeviceToHost));
@@ -430,12 +692,12 @@ bool alm_gate(lbw_domain* d, int64_t m, const uint32_t** flag, uint32_t* value,
     // only with the chain on its own SMs (the waiting CTAs cannot starve
     // it), one slab, device kinematics, and the chain of step m queued last
     if (!s || !s->gate_flag || !d->green_alm || d->linked || !s->kin_device ||
-        s->ready_step != m || s->kin_valid[m % 3] != m)
+        s->ready_step != m || s->kin_valid[m % kSlots] != m)
         return false;
     *flag = s->gate_flag;
     *value = (uint32_t)d->alm_launches;
-    *box = s->gate_box + 2 * (m % 3);
-    *kin_event = s->ev_kin_step[m % 3];
+    *box = s->gate_box + 2 * (m % kSlots);
+    *kin_event = s->ev_kin_step[m % kSlots];
     return true;
 }
 
@@ -461,6 +723,7 @@ int alm_invalidate(lbw_domain* d) {
     if (d->alm->kin_stream) LBW_CK(cudaStreamSynchronize(d->alm->kin_stream));
     d->alm->ready_step = -1;
     d->alm->fs_next = -1;
+    d->alm->cb_next = -1;
     return LBW_OK;
 }
 
@@ -478,18 +741,18 @@ static int kin_launch(lbw_domain* d, int64_t j) {
     LBW_CK(cudaStreamWaitEvent(s->kin_stream, s->ev_chain_done[j & 1], 0));
     const size_t ksm = s->kin_smem;
     KinDev kd = s->kdev();
-    kd.hist_slot = (int32_t)(j % 3);
-    kd.box = s->gate_box ? s->gate_box + 2 * (j % 3) : nullptr;
+    kd.hist_slot = (int32_t)(j % kSlots);
+    kd.box = s->gate_box ? s->gate_box + 2 * (j % kSlots) : nullptr;
     kd.skip_static = s->kin_static_ready ? 1 : 0;
     k_kinematics<<<1, 256, ksm, s->kin_stream>>>(kd, s->dev(j), d->g,
                                                   d->desc.periodic[0] ? 1 : 0, advance);
     count_launch();
     LBW_CK(cudaGetLastError());
     LBW_CK(cudaEventRecord(s->ev_kin_done, s->kin_stream));
-    if (s->ev_kin_step[j % 3]) LBW_CK(cudaEventRecord(s->ev_kin_step[j % 3], s->kin_stream));
+    if (s->ev_kin_step[j % kSlots]) LBW_CK(cudaEventRecord(s->ev_kin_step[j % kSlots], s->kin_stream));
     s->kin_static_ready = true;
     s->kin_state_step = j;
-    s->kin_valid[j % 3] = j;
+    s->kin_valid[j % kSlots] = j;
     return LBW_OK;
 }
 
@@ -527,21 +790,21 @@ bool alm_after_fused(const lbw_domain* d) {
 static int fs_allocate(lbw_domain* d) {
     AlmState* s = d->alm;
     const int64_t rows = (int64_t)d->g.nxl * d->g.ny;
-    const size_t dep = (size_t)3 * s->n * 3 * s->kw;
+    const size_t dep = (size_t)kSlots * s->n * 3 * s->kw;
     int rc = LBW_OK;
     auto A = [&](auto** p, size_t n) {
         if (rc == LBW_OK) rc = dev_alloc(d, s, p, n);
     };
     A(&s->fs_dep_cell, dep);
     A(&s->fs_dep_w, dep);
-    A(&s->fs_frow, (size_t)3 * rows);
-    A(&s->fs_skey, (size_t)3 * rows);
+    A(&s->fs_frow, (size_t)kSlots * rows);
+    A(&s->fs_skey, (size_t)kSlots * rows);
     A(&s->fs_spool, (size_t)2 * 4 * s->n * 4 * d->g.zp);
     A(&s->fs_ctr, 6);   // [task, done] x 2 launches + a scratch pair
     if (rc) return rc;
     // keys with tag 0xffffffff match no step (tags are step + 1)
-    LBW_CK(cudaMemset(s->fs_frow, 0xff, (size_t)3 * rows * 8));
-    LBW_CK(cudaMemset(s->fs_skey, 0xff, (size_t)3 * rows * 8));
+    LBW_CK(cudaMemset(s->fs_frow, 0xff, (size_t)kSlots * rows * 8));
+    LBW_CK(cudaMemset(s->fs_skey, 0xff, (size_t)kSlots * rows * 8));
     LBW_CK(cudaMemset(s->fs_ctr, 0, 24));
     if (getenv("LBW_FUSED_PROF")) {
         rc = dev_alloc(d, s, &s->fs_prof, (size_t)256 * 8);
@@ -555,7 +818,7 @@ static int fs_allocate(lbw_domain* d) {
 static FsGeom fs_geom(const lbw_domain* d, int64_t j) {
     const AlmState* s = d->alm;
     const int64_t rows = (int64_t)d->g.nxl * d->g.ny;
-    const int slot = (int)(j % 3);
+    const int slot = (int)(j % kSlots);
     const size_t dep = (size_t)s->n * 3 * s->kw;
     FsGeom g;
     g.dep_cell = s->fs_dep_cell + slot * dep;
@@ -585,7 +848,7 @@ static ForceView fs_view(const lbw_domain* d, int64_t m) {
 static int fs_prime(lbw_domain* d, int64_t j) {
     AlmState* s = d->alm;
     int do_kin = 0, advance = 0;
-    if (s->kin_valid[j % 3] != j) {
+    if (s->kin_valid[j % kSlots] != j) {
         if (j < s->kin_state_step || j > s->kin_state_step + 1) {
             set_error("device kinematics can only advance one step at a time");
             return LBW_ESTATE;
@@ -594,7 +857,7 @@ static int fs_prime(lbw_domain* d, int64_t j) {
         do_kin = 1;
     }
     KinDev kd = s->kdev();
-    kd.hist_slot = (int32_t)(j % 3);
+    kd.hist_slot = (int32_t)(j % kSlots);
     kd.skip_static = s->kin_static_ready ? 1 : 0;
     k_fs_prime<<<1, 128, do_kin ? s->kin_smem : 0, d->stream>>>(
         kd, s->dev(j), d->g, d->desc.periodic[0] ? 1 : 0, advance, do_kin, fs_geom(d, j));
@@ -603,7 +866,7 @@ static int fs_prime(lbw_domain* d, int64_t j) {
     if (do_kin) {
         s->kin_static_ready = true;
         s->kin_state_step = j;
-        s->kin_valid[j % 3] = j;
+        s->kin_valid[j % kSlots] = j;
     }
     return LBW_OK;
 }
@@ -651,7 +914,7 @@ int alm_fused_launch(lbw_domain* d, bool pull, ForceView* fv_out) {
     // primed: the previous launch was fused step m-1 (pool of step m filled,
     // kinematics + geometry of m and m+1 done, counters of m zeroed)
     const bool primed = s->fs_next == m && s->kin_state_step == m + 1 &&
-                        s->kin_valid[(m + 1) % 3] == m + 1 && s->kin_valid[m % 3] == m;
+                        s->kin_valid[(m + 1) % kSlots] == m + 1 && s->kin_valid[m % kSlots] == m;
     if (!primed) {
         // whatever the standalone chain queued is finished before its
         // outputs are rewritten here
@@ -687,7 +950,7 @@ int alm_fused_launch(lbw_domain* d, bool pull, ForceView* fv_out) {
         A.a.loads_row = s->d_loads + (size_t)(m % s->loads_cap) * s->n * 3;
     A.md = make_macro_dev(d);
     A.use_pool = primed ? 1 : 0;
-    A.pool.skey = s->fs_skey + (size_t)(m % 3) * rows;
+    A.pool.skey = s->fs_skey + (size_t)(m % kSlots) * rows;
     A.pool.spool = s->fs_spool + (size_t)(m & 1) * 4 * s->n * 4 * d->g.zp;
     A.pool.tag = (uint32_t)(m + 1);
     A.pool.inflow = d->desc.boundary == LBW_BC_INFLOW_OUTFLOW ? 1 : 0;
@@ -695,14 +958,14 @@ int alm_fused_launch(lbw_domain* d, bool pull, ForceView* fv_out) {
     A.pool.error_flags = s->error_flags;
     A.ctr = s->fs_ctr + 2 * (m & 1);
     A.ctr_next = s->fs_ctr + 2 * ((m + 1) & 1);
-    A.skey_next = s->fs_skey + (size_t)((m + 1) % 3) * rows;
+    A.skey_next = s->fs_skey + (size_t)((m + 1) % kSlots) * rows;
     A.spool_next = s->fs_spool + (size_t)((m + 1) & 1) * 4 * s->n * 4 * d->g.zp;
     A.store_tag = (uint32_t)(m + 2);
     // KK(m+2) rewrites the geometry slot of step m-1, which a priming
     // launch's sampling reads (the force view of sweep m-1): not then
     A.kk_on = primed ? 1 : 0;
     A.k = s->kdev();
-    A.k.hist_slot = (int32_t)((m + 2) % 3);
+    A.k.hist_slot = (int32_t)((m + 2) % kSlots);
     A.k.skip_static = s->kin_static_ready ? 1 : 0;
     A.a_kk = s->dev(m + 2);
     A.geo = fs_geom(d, m + 2);
@@ -746,7 +1009,7 @@ int alm_fused_launch(lbw_domain* d, bool pull, ForceView* fv_out) {
     if (primed) {
         s->kin_static_ready = true;
         s->kin_state_step = m + 2;
-        s->kin_valid[(m + 2) % 3] = m + 2;
+        s->kin_valid[(m + 2) % kSlots] = m + 2;
     } else {
         int rc = fs_prime(d, m + 2);
         if (rc) return rc;
@@ -754,6 +1017,240 @@ int alm_fused_launch(lbw_domain* d, bool pull, ForceView* fv_out) {
     s->fs_next = m + 1;
     s->ready_step = -1;
     *fv_out = w.fv;
+    return LBW_OK;
+}
+
+// ------------------------------------------------------------ chain B
+// The actuator chain ordered by in-kernel flags instead of per-step stream
+// events (single slab, device kinematics, <= 64 points, no disks):
+//
+//   actuator stream: chain(m+1) = K4(m+1) + KK(m+5): waits in-kernel until
+//                    sweep m has stored the (rho, u) of step m+1's sampling
+//                    rows, then point forces of step m+1 from those samples,
+//                    and kinematics + geometry four steps ahead (slot j % 6)
+//   main stream:     sweep m: tiles read the geometry once KK(m+1) is done,
+//                    force tiles wait for K4(m); sampling-row tiles store
+//                    their macro; consecutive sweeps stay PDL-chained
+//
+// so the chain of step m+1 starts as soon as sweep m has passed the rotor's
+// planes, and the main stream never waits for another stream.
+
+// Used on slabs below 1.5 M cells, where the chain's latency sets the step
+// time; on larger slabs the sweep hides the event-ordered chain and its
+// plainer kernel is faster (C2: 0.275 vs 0.291 ms per sweep).
+// LBW_CHAIN_FLAGS: 0 never, 1 always (when eligible), unset: by size.
+bool alm_chainb_eligible(const lbw_domain* d) {
+    const AlmState* s = d->alm;
+    if (!(d->chainb && s && s->n > 0 && s->kin_device && s->on_the_fly && s->n_rings == 0 &&
+          !d->linked && !d->user_active && d->prelaunch && !tool_injected() &&
+          s->kin_smem <= 48 * 1024))
+        return false;
+    if (d->chainb_forced) return true;
+    return (int64_t)d->g.nxl * d->g.ny * d->g.nz < 1500000;
+}
+
+bool alm_after_chainb(const lbw_domain* d) {
+    return alm_active(d) && d->alm->cb_next == d->step && d->step > 0;
+}
+
+static int cb_allocate(lbw_domain* d) {
+    AlmState* s = d->alm;
+    if (!s->fs_alloc) {
+        int rc = fs_allocate(d);
+        if (rc) return rc;
+    }
+    if (!s->cb_flags) {
+        int rc = dev_alloc(d, s, &s->cb_flags, 8);
+        if (!rc) rc = dev_alloc(d, s, &s->cb_pool_tiles, kSlots);
+        if (rc) return rc;
+        LBW_CK(cudaMemset(s->cb_flags, 0, 8 * sizeof(uint32_t)));
+        LBW_CK(cudaMemset(s->cb_pool_tiles, 0, kSlots * sizeof(int32_t)));
+        LBW_CK(cudaHostAlloc(&s->cb_box_h, kSlots * 2 * sizeof(int32_t), cudaHostAllocMapped));
+        for (int k = 0; k < 2 * kSlots; ++k) s->cb_box_h[k] = 0;
+        void* dp = nullptr;
+        LBW_CK(cudaHostGetDevicePointer(&dp, s->cb_box_h, 0));
+        s->cb_box_d = static_cast<int32_t*>(dp);
+    }
+    return LBW_OK;
+}
+
+// KK(j) of chain B on stream st
+static int cb_kk(lbw_domain* d, int64_t j, cudaStream_t st) {
+    AlmState* s = d->alm;
+    int do_kin = 0, advance = 0;
+    if (s->kin_valid[j % kSlots] != j) {
+        if (j < s->kin_state_step || j > s->kin_state_step + 1) {
+            set_error("device kinematics can only advance one step at a time");
+            return LBW_ESTATE;
+        }
+        advance = j > s->kin_state_step ? 1 : 0;
+        do_kin = 1;
+    }
+    KinDev kd = s->kdev();
+    kd.hist_slot = (int32_t)(j % kSlots);
+    kd.skip_static = s->kin_static_ready ? 1 : 0;
+    const dim3 blk = sweep_block(d->g);
+    const int tiles_x = (int)((d->g.nz + blk.x - 1) / blk.x);
+    k_cb_kk<<<1, 128, do_kin ? s->kin_smem : 0, st>>>(
+        kd, s->dev(j), d->g, d->desc.periodic[0] ? 1 : 0, advance, do_kin, fs_geom(d, j),
+        (int)blk.y, tiles_x, s->cb_pool_tiles + j % kSlots, s->cb_flags, (uint32_t)(j + 1),
+        s->cb_box_d + 2 * (j % kSlots));
+    count_launch();
+    LBW_CK(cudaGetLastError());
+    if (do_kin) {
+        s->kin_static_ready = true;
+        s->kin_state_step = j;
+        s->kin_valid[j % kSlots] = j;
+    }
+    return LBW_OK;
+}
+
+// The chain launch of step j (K4(j) [+ KK(j+4) when kk]) on stream st;
+// use_pool: samples stored by sweep j-1, else recomputed from msrc (priming)
+static int cb_chain(lbw_domain* d, int64_t j, cudaStream_t st, bool use_pool, bool kk) {
+    AlmState* s = d->alm;
+    const int64_t rows = (int64_t)d->g.nxl * d->g.ny;
+    CbChainArgs A{};
+    A.g = d->g;
+    A.a = s->dev(j);
+    if (s->loads_cap > 0 && s->d_loads)
+        A.a.loads_row = s->d_loads + (size_t)(j % s->loads_cap) * s->n * 3;
+    A.md = make_macro_dev(d);
+    A.pool.skey = s->fs_skey + (size_t)(j % kSlots) * rows;
+    A.pool.spool = s->fs_spool + (size_t)(j & 1) * 4 * s->n * 4 * d->g.zp;
+    A.pool.tag = (uint32_t)(j + 1);
+    A.pool.inflow = d->desc.boundary == LBW_BC_INFLOW_OUTFLOW ? 1 : 0;
+    for (int k = 0; k < 3; ++k) A.pool.u_in[k] = d->desc.u_in[k];
+    A.pool.error_flags = s->error_flags;
+    A.pool.raw = 1;
+    A.pool.fv = fs_view(d, j - 1);
+    A.use_pool = use_pool ? 1 : 0;
+    A.box_flag = s->cb_flags + 2;
+    A.box_value = (uint32_t)j;
+    A.pool_tiles = s->cb_pool_tiles + j % kSlots;
+    A.flags = s->cb_flags;
+    A.k4_value = (uint32_t)(j + 1);
+    A.per_x = d->desc.periodic[0] ? 1 : 0;
+    const dim3 blk = sweep_block(d->g);
+    A.ty = (int32_t)blk.y;
+    A.tiles_x = (int32_t)((d->g.nz + blk.x - 1) / blk.x);
+    // K4(j); priming (on the main stream) is an ordinary launch: it samples
+    // by recomputation from buffers the previous sweep wrote
+    A.role = 0;
+    const size_t k4_smem = (size_t)s->n * (3 * s->kw * 12 + 24);
+    LBW_CK(launch_cb_chain(A, (unsigned)((s->n + 3) / 4), k4_smem, st, use_pool));
+    count_launch();
+    if (kk) {
+        // kinematics of step j+4 (serial chain) and geometry of step j+3
+        const int64_t jk = j + 4;
+        CbChainArgs B = A;
+        B.role = 1;
+        if (s->kin_valid[jk % kSlots] != jk) {
+            if (jk < s->kin_state_step || jk > s->kin_state_step + 1) {
+                set_error("device kinematics can only advance one step at a time");
+                return LBW_ESTATE;
+            }
+            B.kk_do_kin = 1;
+            B.kk_advance = jk > s->kin_state_step ? 1 : 0;
+        }
+        B.k = s->kdev();
+        B.k.hist_slot = (int32_t)(jk % kSlots);
+        B.k.skip_static = s->kin_static_ready ? 1 : 0;
+        B.akk = s->dev(jk);
+        B.kin_value = (uint32_t)(jk + 1);
+        B.slot_value = (uint32_t)(jk - 4);
+        LBW_CK(launch_cb_chain(B, 1, B.kk_do_kin ? s->kin_smem : 0, st, true));
+        count_launch();
+        if (B.kk_do_kin) {
+            s->kin_static_ready = true;
+            s->kin_state_step = jk;
+            s->kin_valid[jk % kSlots] = jk;
+        }
+        const int64_t jg = j + 3;
+        CbChainArgs C = A;
+        C.role = 2;
+        C.akk = s->dev(jg);
+        C.geo = fs_geom(d, jg);
+        C.pool_tiles_kk = s->cb_pool_tiles + jg % kSlots;
+        C.kin_value = (uint32_t)(jg + 1);
+        C.slot_value = (uint32_t)(jg - 4);
+        C.box_hint = s->cb_box_d + 2 * (jg % kSlots);
+        LBW_CK(launch_cb_chain(C, 1, 0, st, true));
+        count_launch();
+    }
+    s->ready_step = -1;
+    return LBW_OK;
+}
+
+int alm_chainb_before(lbw_domain* d, SweepArgs* a) {
+    AlmState* s = d->alm;
+    const int64_t m = d->step;
+    int rc = cb_allocate(d);
+    if (rc) return rc;
+    if (s->cb_next != m) {
+        // priming: anything the standalone chain queued finishes first; the
+        // geometry of steps m .. m+4 and the forces of step m (sampled by
+        // recomputation from the last collide's input) go on the main stream
+        LBW_CK(cudaStreamSynchronize(d->alm_stream));
+        if (s->kin_stream) LBW_CK(cudaStreamSynchronize(s->kin_stream));
+        LBW_CK(cudaMemsetAsync(s->cb_flags + 3, 0, 2 * sizeof(uint32_t), d->stream));
+        // kinematics + geometry of m .. m+4 (geometry publishes in step
+        // order: restart its flag at m)
+        rc = stream_write32(d->stream, s->cb_flags + 6, (uint32_t)m);
+        for (int64_t j = m; j <= m + 4 && !rc; ++j) rc = cb_kk(d, j, d->stream);
+        if (!rc) rc = cb_chain(d, m, d->stream, false, false);
+        if (rc) return rc;
+        // the chains queued from now on (actuator stream) read what these
+        // priming kernels wrote: kinematics, geometry, pool-tile counts
+        LBW_CK(cudaEventRecord(d->ev_main, d->stream));
+        LBW_CK(cudaStreamWaitEvent(d->alm_stream, d->ev_main, 0));
+    }
+    const int64_t rows = (int64_t)d->g.nxl * d->g.ny;
+    a->fv = fs_view(d, m);
+    a->gate_flag = nullptr;
+    a->gate_box = nullptr;
+    a->gate_value = 0;
+    a->gate_error = reinterpret_cast<int32_t*>(s->cb_flags + 5);
+    a->pdl = 1;
+    a->kin_flag = s->cb_flags + 6;      // geometry of step m+1 done
+    a->kin_value = (uint32_t)(m + 2);
+    a->k4_flag = s->cb_flags + 1;
+    a->k4_value = (uint32_t)(m + 1);
+    a->skey = s->fs_skey + (size_t)((m + 1) % kSlots) * rows;
+    a->spool = s->fs_spool + (size_t)((m + 1) & 1) * 4 * s->n * 4 * d->g.zp;
+    a->store_tag = (uint32_t)(m + 2);
+    a->pool_cnt = s->cb_flags + 3;
+    a->pool_tiles = s->cb_pool_tiles + (m + 1) % kSlots;
+    a->box_flag = s->cb_flags + 2;
+    a->box_value = (uint32_t)(m + 1);
+    // plane order: the rotor's planes first.  A hint only -- whatever KK
+    // wrote into the mapped host copy most recently for step m+1's slot
+    // (possibly a few steps old while the host runs ahead of the GPU);
+    // every dependency is guarded by the flags, not by the order
+    const volatile int32_t* hb = s->cb_box_h + 2 * ((m + 1) % kSlots);
+    a->x_first = hb[0];
+    a->x_len = hb[1] > 0 ? hb[1] : d->g.nxl;
+    return LBW_OK;
+}
+
+int alm_chainb_after(lbw_domain* d, int64_t m) {
+    AlmState* s = d->alm;
+    // the chain of step m+1 (K4(m+1) + KK(m+5)) on the actuator stream: it
+    // waits in-kernel for sweep m's samples; nothing else orders it
+    int rc = cb_chain(d, m + 1, d->alm_stream, true, true);
+    if (rc) return rc;
+    s->cb_next = m + 1;
+    return LBW_OK;
+}
+
+int alm_chainb_check(lbw_domain* d) {
+    if (!alm_active(d) || !d->alm->cb_flags) return LBW_OK;
+    uint32_t err = 0;
+    LBW_CK(cudaMemcpy(&err, d->alm->cb_flags + 5, sizeof(err), cudaMemcpyDeviceToHost));
+    if (err) {
+        set_error("an in-kernel wait of the flag-ordered actuator chain expired (results invalid)");
+        return LBW_ECUDA;
+    }
     return LBW_OK;
 }
 
@@ -769,7 +1266,7 @@ int alm_launch(lbw_domain* d, int64_t m) {
     fs.tag = (uint32_t)(m + 1);
     fs.flag_rows = s->on_the_fly ? 1 : 0;
     if (s->kin_device) {
-        if (s->kin_valid[m % 3] != m) {
+        if (s->kin_valid[m % kSlots] != m) {
             int rc = kin_launch(d, m);
             if (rc) return rc;
         }
@@ -923,7 +1420,7 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     A(&s->p_alpha, std::max<int64_t>(1, total_rows));
     A(&s->p_cl, std::max<int64_t>(1, total_rows));
     A(&s->p_cd, std::max<int64_t>(1, total_rows));
-    A(&s->kin, (size_t)3 * P * kKin);
+    A(&s->kin, (size_t)kSlots * P * kKin);
     A(&s->samples, (size_t)2 * P * 4);
     A(&s->blade, (size_t)2 * P * 3);
     A(&s->flat, (size_t)2 * P * 3);
@@ -1001,7 +1498,7 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
             cudaMemset(s->cube, 0, ((size_t)2 * P * 32 + (size_t)2 * P * 4) * 8) != cudaSuccess ||
             cudaMemset(s->samples, 0, (size_t)2 * P * 32) != cudaSuccess ||
             cudaMemset(s->blade, 0, (size_t)2 * P * 24) != cudaSuccess ||
-            cudaMemset(s->kin, 0, (size_t)3 * P * kKin * 8) != cudaSuccess ||
+            cudaMemset(s->kin, 0, (size_t)kSlots * P * kKin * 8) != cudaSuccess ||
             cudaMallocHost(&s->h_ring, (size_t)kRing * P * kKin * 8) != cudaSuccess) {
             cudaGetLastError();
             set_error("ALM initialisation failed");
@@ -1058,8 +1555,8 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
     A(&s->k_orient, (size_t)P * 9);
     A(&s->k_lframe, (size_t)P * 9);
     A(&s->k_cs, (size_t)C * kCS);
-    A(&s->k_spin_hist, (size_t)3 * C * 9);
-    A(&s->k_cs_hist, (size_t)3 * C * kCS);
+    A(&s->k_spin_hist, (size_t)kSlots * C * 9);
+    A(&s->k_cs_hist, (size_t)kSlots * C * kCS);
     A(&s->k_is_disk, C);
     A(&s->k_disk_center, (size_t)C * 12);
     A(&s->k_order, C);
@@ -1117,7 +1614,7 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
         H(s->k_disk_center, dcen.data(), (size_t)C * 96);
     }
     if (rc) return rc;
-    size_t ksm = (size_t)C * (kKP + kCS) * sizeof(double) + (size_t)(3 * C + 1) * 4;
+    size_t ksm = (size_t)C * (kKP + kCS) * sizeof(double) + (size_t)(3 * C + 1) * 4 + 8;  // +8: the staged image is padded to 8 B
     const size_t kpts = (size_t)P * 21 * sizeof(double) + (size_t)P * sizeof(int32_t);
     s->kin_stage_points = ksm + kpts <= 160 * 1024;
     if (s->kin_stage_points) ksm += kpts;
@@ -1129,6 +1626,47 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
         return LBW_EINVAL;
     }
     s->kin_smem = ksm;
+    {
+        // the constant part of the CTA's shared-memory image (kinematics_cta)
+        std::vector<double> ip((size_t)C * kKP, 0.0);
+        for (int c = 0; c < C; ++c) {
+            double* q = ip.data() + (size_t)c * kKP;
+            for (int i = 0; i < 3; ++i) q[i] = kd->rel_p[c * 3 + i];
+            for (int i = 0; i < 9; ++i) q[3 + i] = kd->rel_T[c * 9 + i];
+            for (int i = 0; i < 3; ++i) q[12 + i] = kd->axis[c * 3 + i];
+            q[15] = kd->rate[c];
+            for (int i = 0; i < 9; ++i) q[16 + i] = kd->step_rotation[c * 9 + i];
+            for (int i = 0; i < 9; ++i) q[25 + i] = kd->spin[c * 9 + i];   // rewritten per launch
+            q[34] = (double)kd->parent[c];
+            q[35] = (double)kd->line_first[c];
+            const bool disk = kd->is_disk && kd->is_disk[c];
+            q[36] = disk ? 1.0 : 0.0;
+            for (int i = 0; i < 12; ++i)
+                q[37 + i] = (disk && kd->disk_center) ? kd->disk_center[(size_t)c * 12 + i] : 0.0;
+        }
+        std::vector<char> tail;
+        auto put = [&](const void* src, size_t bytes) {
+            const char* b = static_cast<const char*>(src);
+            tail.insert(tail.end(), b, b + bytes);
+        };
+        if (s->kin_stage_points) {
+            put(kd->offsets, (size_t)P * 24);
+            put(kd->orientations, (size_t)P * 72);
+            put(kd->local_frames, (size_t)P * 72);
+            put(point_comp.data(), (size_t)P * 4);
+        }
+        put(order.data(), (size_t)C * 4);
+        put(stat.data(), (size_t)C * 4);
+        put(lstart.data(), lstart.size() * 4);
+        tail.resize((tail.size() + 7) / 8 * 8, 0);
+        rc = dev_alloc(d, s, &s->k_img_prm, ip.size());
+        if (!rc) rc = dev_alloc(d, s, &s->k_img_tail, tail.size() / 8);
+        if (rc) return rc;
+        H(s->k_img_prm, ip.data(), ip.size() * 8);
+        H(s->k_img_tail, tail.data(), tail.size());
+        if (rc) return rc;
+        s->k_img_words = (int32_t)(tail.size() / 8);
+    }
     if (!s->kin_stream) {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -1152,7 +1690,7 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
             if (rcg == LBW_OK) rcg = dev_alloc(d, s, p, n);
         };
         G(&s->gate_flag, 2);   // [0] chain launches done, [1] sweep wait expired
-        G(&s->gate_box, 6);
+        G(&s->gate_box, 2 * kSlots);
         if (rcg) return rcg;
         for (auto& e : s->ev_kin_step)
             LBW_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1162,10 +1700,11 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
     s->k_dx = kd->dx;
     s->kin_device = true;
     s->kin_state_step = d->step - (kd->advance_first ? 1 : 0);
-    s->kin_valid[0] = s->kin_valid[1] = s->kin_valid[2] = -1;
+    for (auto& v : s->kin_valid) v = -1;
     s->kin_static_ready = false;
     s->ready_step = -1;
     s->fs_next = -1;
+    s->cb_next = -1;
     return LBW_OK;
 }
 
@@ -1187,18 +1726,18 @@ int lbw_alm_download_kinematics(lbw_domain* d, double* kin, double* spin, double
     LBW_CK(cudaStreamSynchronize(d->alm_stream));
     if (s->kin_stream) LBW_CK(cudaStreamSynchronize(s->kin_stream));
     if (kin)
-        LBW_CK(cudaMemcpy(kin, s->kin + (size_t)(d->step > 0 ? (d->step - 1) % 3 : 0) * s->n * kKin,
+        LBW_CK(cudaMemcpy(kin, s->kin + (size_t)(d->step > 0 ? (d->step - 1) % kSlots : 0) * s->n * kKin,
                           (size_t)s->n * kKin * 8, cudaMemcpyDeviceToHost));
     // the turbine state of step d->step (what the host objects hold after
     // d->step advances), even when the next step's kinematics already ran
     const int64_t v = kin_view_step(d);
-    const bool hist = s->kin_valid[v % 3] == v;
+    const bool hist = s->kin_valid[v % kSlots] == v;
     if (spin && s->kin_device)
-        LBW_CK(cudaMemcpy(spin, hist ? s->k_spin_hist + (size_t)(v % 3) * s->nc * 9 : s->k_spin,
+        LBW_CK(cudaMemcpy(spin, hist ? s->k_spin_hist + (size_t)(v % kSlots) * s->nc * 9 : s->k_spin,
                           (size_t)s->nc * 72, cudaMemcpyDeviceToHost));
     if (comp_state && s->kin_device)
         LBW_CK(cudaMemcpy(comp_state,
-                          hist ? s->k_cs_hist + (size_t)(v % 3) * s->nc * kCS : s->k_cs,
+                          hist ? s->k_cs_hist + (size_t)(v % kSlots) * s->nc * kCS : s->k_cs,
                           (size_t)s->nc * kCS * 8, cudaMemcpyDeviceToHost));
     return LBW_OK;
 }
@@ -1220,7 +1759,7 @@ int lbw_alm_set_kinematics(lbw_domain* d, const double* kin) {
     double* h = s->h_ring + (size_t)slot * s->n * kKin;
     std::memcpy(h, kin, (size_t)s->n * kKin * 8);
     const int64_t m = d->step;
-    LBW_CK(cudaMemcpyAsync(s->kin + (size_t)(m % 3) * s->n * kKin, h, (size_t)s->n * kKin * 8,
+    LBW_CK(cudaMemcpyAsync(s->kin + (size_t)(m % kSlots) * s->n * kKin, h, (size_t)s->n * kKin * 8,
                            cudaMemcpyHostToDevice, d->alm_stream));
     LBW_CK(cudaEventRecord(s->ring_ev[slot], d->alm_stream));
     s->kin_queued_step = m;

@@ -8,7 +8,13 @@
 
 namespace lbw {
 
-constexpr int kKin = 18;  // pos_lat(3) vel(3) e_chord(3) e_normal(3) e_span(3) pos_m(3)
+constexpr int kKin = 18;
+// per-step actuator data computed ahead of the step that uses it
+// (kinematics, spin / component history, deposit geometry, row keys) live
+// in slots j % kSlots: the flag-ordered chain computes them four steps
+// ahead, and slot j is last read by the sweep of step j (and its row keys by
+// the sweep of step j-1), so kSlots = 6 leaves one step of margin
+constexpr int kSlots = 6;  // pos_lat(3) vel(3) e_chord(3) e_normal(3) e_span(3) pos_m(3)
 constexpr int kRing = 8;
 // per-component device state: world p(3) T(9) v(3) w(3) spin_axis(3) has_axis(1)
 // start_p(3) start_T(9) v_start(3) w_start(3) R(9)
@@ -71,8 +77,8 @@ struct KinDev {
     const int32_t* is_disk;
     const double* disk_center;
     double* cs;
-    double* spin_hist;   // (3, nc, 9): spin state of step j in slot j % 3
-    double* cs_hist;     // (3, nc, kCS)
+    double* spin_hist;   // (kSlots, nc, 9): spin state of step j in slot j % kSlots
+    double* cs_hist;     // (kSlots, nc, kCS)
     int32_t hist_slot;
     int32_t* box;           // (2): x planes this step's chain reads / writes (gate)
     int32_t box_halo;       // spreading half-width + 2
@@ -83,6 +89,14 @@ struct KinDev {
     const int32_t* is_static;    // (nc) world transform constant in time
     int32_t skip_static;         // their state from the previous launch is valid
     double dx;
+    // the constant part of the CTA's shared-memory image, packed once by the
+    // host in the exact layout (kinematics_cta): the parameter block (spin
+    // slots excepted) and the tail from the point block / walk schedule on;
+    // staged with independent 8-byte loads (one round trip, not one per
+    // field and loop iteration)
+    const long long* img_prm;    // (nc * kKP) doubles
+    const long long* img_tail;   // img_tail_words 8-byte words
+    int32_t img_tail_words;
 };
 
 // parameters per component in the kinematics CTA's shared memory:
@@ -143,6 +157,12 @@ struct FsPool {
     int32_t inflow;
     double u_in[3];
     int32_t* error_flags;  // bit 3: a sampled row without a pool entry
+    // raw != 0 (flag-ordered chain): the pool holds the force-free sums
+    // (rho, sum f c) the sweep of step j-1 stored before its force was
+    // known; the macro is completed here with that sweep's force at the
+    // cell, u = (sum f c + F dt / 2) / rho -- moments_exact's arithmetic
+    int32_t raw;
+    ForceView fv;          // the force of sweep j-1
 };
 
 // One launch of the fused step kernel (lbw_fused.cuh): sweep m, the point

@@ -267,6 +267,9 @@ int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out) {
         // off by default until its chain latency beats the standalone chain
         const char* fu = getenv("LBW_FUSED");
         d->fused = fu && fu[0] == '1';
+        const char* cb = getenv("LBW_CHAIN_FLAGS");  // 0: event-ordered chain (A/B)
+        d->chainb = !(cb && cb[0] == '0');
+        d->chainb_forced = cb && cb[0] == '1';
     }
     d->device = s.device;
     if (cudaSetDevice(d->device) != cudaSuccess) {
@@ -660,7 +663,9 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
             d->steps_done += 1;
             continue;
         }
-        if (alm_active(d)) {
+        // flag-ordered actuator chain (chain B): no stream waits on the main stream
+        const bool cb = alm_active(d) && alm_chainb_eligible(d);
+        if (alm_active(d) && !cb) {
             // The actuator chain of this step normally was queued on the
             // actuator stream while the previous sweep ran.  Otherwise (host
             // kinematics, first step) queue it now: it needs the sweep two
@@ -668,7 +673,7 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
             // unless a call changed state since the last step, in which case
             // it waits for everything already on the main stream.
             if (!alm_ready(d, d->step)) {
-                if (d->touched || alm_after_fused(d)) {
+                if (d->touched || alm_after_fused(d) || alm_after_chainb(d)) {
                     LBW_CK(cudaEventRecord(d->ev_main, d->stream));
                     LBW_CK(cudaStreamWaitEvent(d->alm_stream, d->ev_main, 0));
                 } else {
@@ -693,7 +698,7 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
             }
             fv = alm_force_view(d, d->step);
         }
-        SweepArgs a;
+        SweepArgs a{};
         a.src = d->buf[d->cur];
         a.dst = d->buf[1 - d->cur];
         a.g = d->g;
@@ -718,6 +723,11 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
             a.halo.peer_flag[1] = d->nb_rank[1] >= 0 ? d->nb_flags[1] + 0 : nullptr;
             a.halo.edge_counter = d->edge_counter;
             a.halo.value = (uint32_t)(d->steps_done + 1);
+        }
+        if (cb) {
+            int rc = alm_chainb_before(d, &a);
+            if (rc) return rc;
+            fv = a.fv;
         }
         const bool pull = !d->state_pre;
         if (d->timing) {
@@ -753,7 +763,10 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
         // read-only during the sweep, and rewrites the force set of the sweep
         // before — exactly the preconditions of this sweep (ev_ready) — so it
         // overlaps this sweep.
-        if (alm_active(d) && alm_can_prelaunch(d)) {
+        if (cb) {
+            int rc = alm_chainb_after(d, d->step - 1);
+            if (rc) return rc;
+        } else if (alm_active(d) && alm_can_prelaunch(d)) {
             LBW_CK(cudaStreamWaitEvent(d->alm_stream, d->ev_ready, 0));
             int rc = alm_launch(d, d->step);
             if (rc) return rc;

@@ -69,6 +69,25 @@ __device__ __forceinline__ Macro moments_exact(const double (&f)[27], double Fx,
     return m;
 }
 
+// The force-free half of moments_exact: rho and sum_i f_i c_i with its
+// summation order (a flag-ordered chain stores these before the cell's
+// force is known and completes u = (m + F dt/2) / rho in the sampling).
+__device__ __forceinline__ void raw_sums_exact(const double (&f)[27], double& rho, double& mx,
+                                               double& my, double& mz) {
+    rho = 0.0;
+    mx = my = mz = 0.0;
+#pragma unroll
+    for (int i = 0; i < 27; ++i) {
+        rho += f[i];
+        if (cx_of(i) > 0) mx += f[i];
+        if (cx_of(i) < 0) mx -= f[i];
+        if (cy_of(i) > 0) my += f[i];
+        if (cy_of(i) < 0) my -= f[i];
+        if (cz_of(i) > 0) mz += f[i];
+        if (cz_of(i) < 0) mz -= f[i];
+    }
+}
+
 // Guo source (_kernels.py:44-52), exact expression order.  Callers skip it
 // when F == 0 exactly: every term is then a signed zero.
 __device__ __forceinline__ void guo_add_exact(double (&f)[27], double Fx, double Fy, double Fz,

@@ -7,6 +7,21 @@
 // the fused step kernel the copy of its own translation unit.
 #pragma once
 #include <climits>
+#include <cstdio>
+
+// Inlining of the chain's device functions: by default the compiler decides
+// and two rare paths stay out of line.  A TU whose kernels pass their
+// parameter structs to these functions defines both macros as
+// __forceinline__: an out-of-line call taking a reference to a kernel
+// parameter makes the compiler copy the parameter block to local memory,
+// and every field access becomes a local load instead of a constant-bank
+// operand (measured: 2-3x on the chain's latency).
+#ifndef LBW_CHAIN_FN
+#define LBW_CHAIN_FN __device__
+#endif
+#ifndef LBW_CHAIN_COLD
+#define LBW_CHAIN_COLD __device__ __noinline__
+#endif
 
 #include "../../include/lbw.h"
 #include "lbw_alm_dev.h"
@@ -17,19 +32,19 @@ namespace {
 
 // ------------------------------------------------------------ 3x3 algebra
 // row-major 3x3; C = A B with a fixed (a0 b0 + a1 b1) + a2 b2 order
-__device__ void mm3(const double* A, const double* B, double* C) {
+LBW_CHAIN_FN void mm3(const double* A, const double* B, double* C) {
     double t[9];
     for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j)
             t[i * 3 + j] = A[i * 3] * B[j] + A[i * 3 + 1] * B[3 + j] + A[i * 3 + 2] * B[6 + j];
     for (int k = 0; k < 9; ++k) C[k] = t[k];
 }
-__device__ void mv3(const double* A, const double* v, double* out) {
+LBW_CHAIN_FN void mv3(const double* A, const double* v, double* out) {
     double t[3];
     for (int i = 0; i < 3; ++i) t[i] = A[i * 3] * v[0] + A[i * 3 + 1] * v[1] + A[i * 3 + 2] * v[2];
     for (int i = 0; i < 3; ++i) out[i] = t[i];
 }
-__device__ void cross3(const double* a, const double* b, double* out) {
+LBW_CHAIN_FN void cross3(const double* a, const double* b, double* out) {
     const double c0 = a[1] * b[2] - a[2] * b[1];
     const double c1 = a[2] * b[0] - a[0] * b[2];
     const double c2 = a[0] * b[1] - a[1] * b[0];
@@ -38,7 +53,7 @@ __device__ void cross3(const double* a, const double* b, double* out) {
     out[2] = c2;
 }
 // Gram-Schmidt on the columns (turbine.py:83-90)
-__device__ void reorth(double* T) {
+LBW_CHAIN_FN void reorth(double* T) {
     double c0[3] = {T[0], T[3], T[6]}, c1[3] = {T[1], T[4], T[7]};
     const double n0 = sqrt(c0[0] * c0[0] + c0[1] * c0[1] + c0[2] * c0[2]);
     for (int i = 0; i < 3; ++i) c0[i] /= n0;
@@ -55,7 +70,7 @@ __device__ void reorth(double* T) {
     }
 }
 // numpy float remainder (npy_divmod): result takes the divisor's sign
-__device__ double np_mod(double a, double b) {
+LBW_CHAIN_FN double np_mod(double a, double b) {
     double m = fmod(a, b);
     if (m != 0.0) {
         if ((b < 0) != (m < 0)) m += b;
@@ -68,7 +83,7 @@ __device__ double np_mod(double a, double b) {
 // Warp-cooperative 3x3 algebra on shared memory for the tree walk: every
 // lane of the warp calls; lanes 0..8 (0..2) own one entry each, with the
 // per-entry arithmetic of mm3 / mv3 / cross3 / drifted (bit-identical).
-__device__ void wmm3(const double* A, const double* B, double* C, int lane) {
+LBW_CHAIN_FN void wmm3(const double* A, const double* B, double* C, int lane) {
     double t = 0.0;
     if (lane < 9) {
         const int i = lane / 3, j = lane % 3;
@@ -78,14 +93,14 @@ __device__ void wmm3(const double* A, const double* B, double* C, int lane) {
     if (lane < 9) C[lane] = t;
     __syncwarp();
 }
-__device__ void wmv3(const double* A, const double* v, double* out, int lane) {
+LBW_CHAIN_FN void wmv3(const double* A, const double* v, double* out, int lane) {
     double t = 0.0;
     if (lane < 3) t = A[lane * 3] * v[0] + A[lane * 3 + 1] * v[1] + A[lane * 3 + 2] * v[2];
     __syncwarp();
     if (lane < 3) out[lane] = t;
     __syncwarp();
 }
-__device__ void wcross3(const double* a, const double* b, double* out, int lane) {
+LBW_CHAIN_FN void wcross3(const double* a, const double* b, double* out, int lane) {
     double t = 0.0;
     if (lane == 0) t = a[1] * b[2] - a[2] * b[1];
     if (lane == 1) t = a[2] * b[0] - a[0] * b[2];
@@ -95,7 +110,7 @@ __device__ void wcross3(const double* a, const double* b, double* out, int lane)
     __syncwarp();
 }
 // max |T^T T - I| > 1e-12 (turbine.py:_DRIFT_TOL)
-__device__ bool wdrifted(const double* T, int lane) {
+LBW_CHAIN_FN bool wdrifted(const double* T, int lane) {
     bool over = false;
     if (lane < 9) {
         const int i = lane / 3, j = lane % 3;
@@ -105,7 +120,7 @@ __device__ bool wdrifted(const double* T, int lane) {
     }
     return __any_sync(0xffffffffu, over);
 }
-__device__ void wreorth(double* T, int lane) {
+LBW_CHAIN_FN void wreorth(double* T, int lane) {
     __syncwarp();
     if (lane == 0) reorth(T);
     __syncwarp();
@@ -115,7 +130,7 @@ __device__ void wreorth(double* T, int lane) {
 // One component of the tree walk (turbine.py:259-311, sim.py:167-191) by
 // one warp: lanes 0..8 own the entries of each 3x3 product (the per-entry
 // arithmetic of mm3 / mv3 / cross3, bit-identical to a serial walk).
-__device__ void walk_component(const KinDev& k, double* prm, double* cs, int c, int advance,
+LBW_CHAIN_FN void walk_component(const KinDev& k, double* prm, double* cs, int c, int advance,
                                const double* off, const double* orient, double* wt,
                                const double* I3s, const double* zero3s, int lane) {
     double* tmp9 = wt;
@@ -197,7 +212,7 @@ __device__ void walk_component(const KinDev& k, double* prm, double* cs, int c, 
 // of dependent 3x3 products down the tree); points are then evaluated in
 // parallel.  Layout per component in smem: params[kKP] then state[kCS].
 // rel_p 3, rel_T 9, axis 3, rate 1, rstep 9, spin 9, parent 1, first 1, is_disk 1, disk p 3, T 9
-__device__ void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g, int per_x,
+LBW_CHAIN_FN void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g, int per_x,
                                int advance, double* ksm, int tid, int nthr) {
 #ifdef LBW_KK_PROF
     long long t0 = clock64();
@@ -215,40 +230,36 @@ __device__ void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g, 
                                        : reinterpret_cast<int32_t*>(cs + (size_t)k.nc * kCS);
     int32_t* sm_static = sm_order + k.nc;
     int32_t* sm_lstart = sm_static + k.nc;
-    for (int i = tid; i < k.nc; i += nthr) {
-        sm_order[i] = k.order[i];
-        sm_static[i] = k.is_static[i];
-    }
-    for (int i = tid; i <= k.nlevels; i += nthr) sm_lstart[i] = k.level_start[i];
-    if (k.skip_static)
-        for (int i = tid; i < k.nc * kCS; i += nthr)
-            if (k.is_static[i / kCS]) cs[i] = k.cs[i];
     const double* off = k.stage_points ? sm_off : k.off;
     const double* orient = k.stage_points ? sm_orient : k.orient;
     const double* lframe = k.stage_points ? sm_lframe : k.lframe;
     const int32_t* point_comp = k.stage_points ? sm_comp : k.point_comp;
-    if (k.stage_points) {
-        for (int i = tid; i < a.n * 3; i += nthr) sm_off[i] = k.off[i];
-        for (int i = tid; i < a.n * 9; i += nthr) {
-            sm_orient[i] = k.orient[i];
-            sm_lframe[i] = k.lframe[i];
+    {
+        // constant image + the dynamic spins / static components' state: all
+        // loads of a round issued before its shared stores
+        constexpr int U = 8;
+        const int n_prm = k.nc * kKP, n_img = n_prm + k.img_tail_words;
+        long long* dst_prm = reinterpret_cast<long long*>(prm);
+        long long* dst_tail = reinterpret_cast<long long*>(k.stage_points ? sm_off : (double*)sm_order);
+        for (int i0 = tid; i0 < n_img; i0 += U * nthr) {
+            long long v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * nthr;
+                if (i < n_img) v[u] = i < n_prm ? k.img_prm[i] : k.img_tail[i - n_prm];
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * nthr;
+                if (i < n_prm) dst_prm[i] = v[u];
+                else if (i < n_img) dst_tail[i - n_prm] = v[u];
+            }
         }
-        for (int i = tid; i < a.n; i += nthr) sm_comp[i] = k.point_comp[i];
-    }
-    for (int i = tid; i < k.nc * kKP; i += nthr) {
-        const int c = i / kKP, j = i % kKP;
-        double v;
-        if (j < 3) v = k.rel_p[c * 3 + j];
-        else if (j < 12) v = k.rel_T[c * 9 + j - 3];
-        else if (j < 15) v = k.axis[c * 3 + j - 12];
-        else if (j < 16) v = k.rate[c];
-        else if (j < 25) v = k.rstep[c * 9 + j - 16];
-        else if (j < 34) v = k.spin[c * 9 + j - 25];
-        else if (j < 35) v = (double)k.parent[c];
-        else if (j < 36) v = (double)k.line_first[c];
-        else if (j < 37) v = (double)k.is_disk[c];
-        else v = k.disk_center[c * 12 + j - 37];
-        prm[i] = v;
+        __syncthreads();
+        for (int i = tid; i < k.nc * 9; i += nthr) prm[(i / 9) * kKP + 25 + i % 9] = k.spin[i];
+        if (k.skip_static)
+            for (int i = tid; i < k.nc * kCS; i += nthr)
+                if (sm_static[i / kCS]) cs[i] = k.cs[i];
     }
     __syncthreads();
 #ifdef LBW_KK_PROF
@@ -363,7 +374,7 @@ __device__ void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g, 
 #endif
 }
 
-__device__ __noinline__ void load_cell_general(const void* buf, const Geom& g, bool pull, int x,
+LBW_CHAIN_COLD void load_cell_general(const void* buf, const Geom& g, bool pull, int x,
                                                int y, int z, double (&f)[27]) {
     if (pull) load_cell_any<true>(buf, g, x, y, z, f);
     else load_cell_any<false>(buf, g, x, y, z, f);
@@ -374,16 +385,16 @@ __device__ __noinline__ void load_cell_general(const void* buf, const Geom& g, b
 // (nothing written) when the cell belongs to another slab, MA_OWNED for a
 // cell of this slab, MA_CONST for a ghost value every slab knows.  Values
 // are those the reference's macro array of the storage dtype holds.
-__device__ int macro_at_raw(const Geom& g, const MacroDev& m, int64_t gx, int64_t gy, int64_t gz,
+LBW_CHAIN_FN int macro_at_raw(const Geom& g, const MacroDev& m, int64_t gx, int64_t gy, int64_t gz,
                             double out[4]);
-__device__ int macro_at(const Geom& g, const MacroDev& m, int64_t gx, int64_t gy, int64_t gz,
+LBW_CHAIN_FN int macro_at(const Geom& g, const MacroDev& m, int64_t gx, int64_t gy, int64_t gz,
                         double out[4]) {
     const int code = macro_at_raw(g, m, gx, gy, gz, out);
     if (code != MA_REMOTE && g.single)
         for (int k = 0; k < 4; ++k) out[k] = stored<float>(out[k]);
     return code;
 }
-__device__ int macro_at_raw(const Geom& g, const MacroDev& m, int64_t gx, int64_t gy, int64_t gz,
+LBW_CHAIN_FN int macro_at_raw(const Geom& g, const MacroDev& m, int64_t gx, int64_t gy, int64_t gz,
                             double out[4]) {
     const double ghost0[4] = {1.0, 0.0, 0.0, 0.0};
     auto put = [&](const double* v) {
@@ -515,7 +526,7 @@ __device__ __forceinline__ void polar_row(const AlmDev& a, const PointStatic& ps
 // np.interp (polars.py:65-80) of cl and cd at x for the whole warp: the
 // bracketing row (largest j with xp[j] <= x; tables are increasing) is
 // counted with a ballot instead of a binary search of dependent loads.
-__device__ void polar_interp(const AlmDev& a, const PointStatic& ps, double x, int lane,
+LBW_CHAIN_FN void polar_interp(const AlmDev& a, const PointStatic& ps, double x, int lane,
                              double& cl, double& cd) {
     const int n = ps.rows;
     double x0, c0l, c0d, xn, cnl, cnd;
@@ -555,7 +566,7 @@ __device__ void polar_interp(const AlmDev& a, const PointStatic& ps, double x, i
 // blade-element force on the BLADE (actuator.py:117-146, sim.py:218-235),
 // evaluated by a whole warp (identical values on every lane; lane 0 raises
 // the flags).  kr: the point's kinematics row.
-__device__ void blade_force_warp(const AlmDev& a, const PointStatic& ps, const double* kr,
+LBW_CHAIN_FN void blade_force_warp(const AlmDev& a, const PointStatic& ps, const double* kr,
                                  const double* acc, double* blade, int lane) {
     blade[0] = blade[1] = blade[2] = 0.0;
     if (ps.pid < 0) return;
@@ -608,7 +619,7 @@ __device__ __forceinline__ void gaussian_support(double xs, double eps, int64_t&
     inv_sum = 1.0 / sum;
 }
 
-__device__ void deposit_axis(double x, int64_t L, int periodic, int kernel, double eps, int kw,
+LBW_CHAIN_FN void deposit_axis(double x, int64_t L, int periodic, int kernel, double eps, int kw,
                              int32_t* dc, double* dw) {
     int cnt = 0;
     for (int q = 0; q < kw; ++q) {
@@ -662,7 +673,7 @@ __device__ __forceinline__ int32_t pair_row(const AlmDev& a, const Geom& g, int 
 
 // deposit cells of a wide (Gaussian) kernel, stored straight to the point's
 // deposit arrays; out of line to keep the Roma path of K4 compact
-__device__ __noinline__ void deposit_axis_wide(const AlmDev& a, int p, int k, double x, int64_t L,
+LBW_CHAIN_COLD void deposit_axis_wide(const AlmDev& a, int p, int k, double x, int64_t L,
                                                int per) {
     const int kw = a.kw;
     int32_t dc[kMaxKw];
@@ -733,6 +744,19 @@ __device__ __forceinline__ int pool_macro(const Geom& g, const FsPool& pl, int p
     const double* b = pl.spool + (int64_t)(uint32_t)key * 4 * g.zp + z;
 #pragma unroll
     for (int q = 0; q < 4; ++q) out[q] = __ldcg(b + (int64_t)q * g.zp);
+    if (pl.raw) {
+        // out = (rho, mx, my, mz); the force of the previous sweep at the
+        // cell, then u exactly as moments_exact forms it (dt = 1)
+        const uint64_t fkey = pl.fv.row_key ? pl.fv.row_key[(int64_t)x * g.ny + y] : 0ull;
+        double F[3];
+        if (g.single) force_from_key<float>(pl.fv, g, fkey, x, y, z, F[0], F[1], F[2]);
+        else force_from_key<double>(pl.fv, g, fkey, x, y, z, F[0], F[1], F[2]);
+        const double inv_rho = 1.0 / out[0];
+        const double hdt = 0.5 * 1.0;
+        for (int q = 0; q < 3; ++q) out[1 + q] = (out[1 + q] + hdt * F[q]) * inv_rho;
+        if (g.single)
+            for (int q = 0; q < 4; ++q) out[q] = stored<float>(out[q]);
+    }
     return MA_OWNED;
 }
 
@@ -754,7 +778,7 @@ __device__ __forceinline__ PointInputs load_point_inputs(const AlmDev& a, int p,
     return in;
 }
 
-__device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, const ForceSet& s,
+LBW_CHAIN_FN void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, const ForceSet& s,
                            int phase, const CubeArgs& cube, int p, int lane,
                            const PointInputs& in, const FsPool* pool = nullptr,
                            bool geometry = true) {
@@ -898,7 +922,7 @@ __device__ void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, co
 // area_i * axis; the blade force is its negation (sim.py:236-244).
 // Slab-local view of a disk point (multi-slab): its Roma support reaches
 // this slab / floor(x) lies in it.
-__device__ bool point_relevant(const Geom& g, int per_x, int halo, double x) {
+LBW_CHAIN_FN bool point_relevant(const Geom& g, int per_x, int halo, double x) {
     const int64_t n0 = (int64_t)floor(x);
     for (int dxc = -halo; dxc <= halo; ++dxc) {
         int64_t c = n0 + dxc;
@@ -908,7 +932,7 @@ __device__ bool point_relevant(const Geom& g, int per_x, int halo, double x) {
     return false;
 }
 
-__device__ void disk_ring(const AlmDev& a, const Geom& g, int per_x, int linked, int r) {
+LBW_CHAIN_FN void disk_ring(const AlmDev& a, const Geom& g, int per_x, int linked, int r) {
     const int first = a.ring_first[r], cnt = a.ring_count[r];
     const double ct = a.ring_ct[r];
     if (linked) {
@@ -973,42 +997,45 @@ __device__ void disk_ring(const AlmDev& a, const Geom& g, int per_x, int linked,
 // rows sweep j sums point forces in), and the rows of its sampling cube
 // (sample keys: sweep j-1 stores its macro there for K4(j)).  Rows shared
 // by several points get one key each write; any writer's slot is valid.
-__device__ void fs_geometry(const FsGeom& geo, const AlmDev& a, const Geom& g, int per_x, int tid,
+LBW_CHAIN_FN void fs_geometry(const FsGeom& geo, const AlmDev& a, const Geom& g, int per_x, int tid,
                             int nthr) {
+    // whole CTA; one thread per (point, axis), then per (point, corner row)
+    // and per deposit (x, y) pair: a point's three axes are independent
+    // chains of sqrt / division latency, so they run side by side
+    __shared__ int32_t s_dc[2][kOnTheFlyMaxPoints * kMaxKw];   // x / y deposit cells
     const int kw = a.kw;
+    for (int t = tid; t < 3 * a.n; t += nthr) {
+        const int p = t / 3, k = t % 3;
+        const double xk = a.kin[(int64_t)p * kKin + k];
+        const int64_t L = k == 0 ? g.nxg : (k == 1 ? g.ny : g.nz);
+        const int per = k == 0 ? per_x : (k == 1 ? g.per_y : g.per_z);
+        int32_t dc[kMaxKw];
+        double dw[kMaxKw];
+        deposit_axis(xk, L, per, a.kernel, a.eps, kw, dc, dw);
+        for (int q = 0; q < kw; ++q) {
+            geo.dep_cell[((int64_t)p * 3 + k) * kw + q] = dc[q];
+            geo.dep_w[((int64_t)p * 3 + k) * kw + q] = dw[q];
+            if (k < 2) s_dc[k][p * kw + q] = dc[q];
+        }
+    }
     const double zero3[3] = {0.0, 0.0, 0.0};
-    for (int p = tid; p < a.n; p += nthr) {
+    for (int t = tid; t < 4 * a.n; t += nthr) {
+        const int p = t >> 2, c = t & 3;
         const double* kr = a.kin + (int64_t)p * kKin;
-        const double xl[3] = {kr[0], kr[1], kr[2]};
-        int32_t dcx[kMaxKw], dcy[kMaxKw];
-        for (int k = 0; k < 3; ++k) {
-            const int64_t L = k == 0 ? g.nxg : (k == 1 ? g.ny : g.nz);
-            const int per = k == 0 ? per_x : (k == 1 ? g.per_y : g.per_z);
-            int32_t dc[kMaxKw];
-            double dw[kMaxKw];
-            deposit_axis(xl[k], L, per, a.kernel, a.eps, kw, dc, dw);
-            for (int q = 0; q < kw; ++q) {
-                geo.dep_cell[((int64_t)p * 3 + k) * kw + q] = dc[q];
-                geo.dep_w[((int64_t)p * 3 + k) * kw + q] = dw[q];
-                if (k == 0) dcx[q] = dc[q];
-                if (k == 1) dcy[q] = dc[q];
-            }
-        }
-        for (int i = 0; i < kw; ++i)
-            for (int l = 0; l < kw; ++l) {
-                const int32_t cxg = dcx[i], cy = dcy[l];
-                const int64_t x = (int64_t)cxg - g.x0;
-                if (cxg >= 0 && cy >= 0 && x >= 0 && x < g.nxl)
-                    geo.frow_key[x * g.ny + cy] = row_key_of(geo.tag, 0);
-            }
-        const int64_t j0x = (int64_t)floor(xl[0] - 0.5), j0y = (int64_t)floor(xl[1] - 0.5);
-        for (int c = 0; c < 4; ++c) {
-            int x = 0, y = 0, z = 0;
-            double v[4];
-            if (corner_map(g, per_x, geo.inflow, zero3, j0x + (c >> 1), j0y + (c & 1), 0, x, y, z,
-                           v) == MA_OWNED)
-                geo.skey[(int64_t)x * g.ny + y] = row_key_of(geo.tag, p * 4 + c);
-        }
+        const int64_t j0x = (int64_t)floor(kr[0] - 0.5), j0y = (int64_t)floor(kr[1] - 0.5);
+        int x = 0, y = 0, z = 0;
+        double v[4];
+        if (corner_map(g, per_x, geo.inflow, zero3, j0x + (c >> 1), j0y + (c & 1), 0, x, y, z,
+                       v) == MA_OWNED)
+            geo.skey[(int64_t)x * g.ny + y] = row_key_of(geo.tag, p * 4 + c);
+    }
+    __syncthreads();
+    for (int t = tid; t < a.n * kw * kw; t += nthr) {
+        const int p = t / (kw * kw), i = (t / kw) % kw, l = t % kw;
+        const int32_t cxg = s_dc[0][p * kw + i], cy = s_dc[1][p * kw + l];
+        const int64_t x = (int64_t)cxg - g.x0;
+        if (cxg >= 0 && cy >= 0 && x >= 0 && x < g.nxl)
+            geo.frow_key[x * g.ny + cy] = row_key_of(geo.tag, 0);
     }
 }
 

@@ -83,6 +83,8 @@ struct lbw_domain {
     bool touched = true;              // state changed by a call since the last step
     bool sweep_alt = true;            // alternate the interior plane order (LBW_SWEEP_ALT)
     bool fused = false;               // one fused launch per actuator step when eligible (LBW_FUSED=1)
+    bool chainb = true;               // flag-ordered actuator chain when eligible (LBW_CHAIN_FLAGS)
+    bool chainb_forced = false;       // LBW_CHAIN_FLAGS=1: regardless of the slab size
     // x-slab neighbours (lbw_peer.cu): side 0 = lo (x-1), side 1 = hi (x+1)
     bool linked = false;
     int nb_rank[2] = {-1, -1};
@@ -128,6 +130,14 @@ int alm_fused_launch(lbw_domain* d, bool pull, ForceView* fv_out);
 // the previous step was a fused launch (its point forces are written inside
 // that launch: a standalone chain must wait for all of it)
 bool alm_after_fused(const lbw_domain* d);
+// Flag-ordered actuator chain ("chain B", lbw_alm.cu): single slab, device
+// kinematics, <= 64 points without disks.  Fills the chain fields of the
+// sweep of step m (and its force view), queues what the chain needs first,
+// and after the sweep (alm_chainb_after) the chain of the next step.
+bool alm_chainb_eligible(const lbw_domain* d);
+int alm_chainb_before(lbw_domain* d, SweepArgs* a);
+int alm_chainb_after(lbw_domain* d, int64_t m);
+bool alm_after_chainb(const lbw_domain* d);
 // Wait for queued actuator work and forget any prelaunched step (the
 // caller is about to change state it reads).
 int alm_invalidate(lbw_domain* d);
@@ -147,6 +157,8 @@ int ensure_stage(lbw_domain* d, size_t bytes);
 
 // lbw_green.cu: SM partition between the sweep and the actuator chain
 int alm_sm_count(const lbw_domain* d);
+// a profiler / sanitizer that serialises kernels is injected in the process
+bool tool_injected();
 int green_partition(lbw_domain* d, int alm_sms);
 cudaStream_t green_alm_stream(lbw_domain* d);   // nullptr without a partition
 void green_release(lbw_domain* d);

@@ -67,7 +67,7 @@ const GreenApi& api() {
 // for a chain kernel that the tool has not run yet.
 // (ncu and compute-sanitizer load an injection library into the target:
 // look for it among the mapped objects, and for the variables they use.)
-static bool tool_injected() {
+bool tool_injected() {
     static const bool injected = [] {
         if (getenv("CUDA_INJECTION64_PATH") || getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR"))
             return true;

@@ -125,6 +125,27 @@ struct SweepArgs {
     // gate timeout: set to 1 by a CTA whose bounded wait expired (the host
     // reports it as an error instead of the kernel trapping)
     int32_t* gate_error;
+    // Flag-ordered actuator chain (lbw_alm.cu, "chain B"; kin_flag != nullptr):
+    // the sweep reads the geometry of steps m / m+1 only once KK(m+1) is done
+    // (*kin_flag >= kin_value), a tile holding force rows waits for the point
+    // forces of step m (*k4_flag >= k4_value), tiles holding rows of step
+    // m+1's sampling cubes store their collide's (rho, u) into spool, and the
+    // last of those tiles (*pool_tiles of them) publishes *box_flag = box_value.
+    const uint32_t* kin_flag;
+    uint32_t kin_value;
+    const uint32_t* k4_flag;
+    uint32_t k4_value;
+    const uint64_t* skey;
+    double* spool;
+    uint32_t store_tag;
+    uint32_t* pool_cnt;
+    const int32_t* pool_tiles;
+    uint32_t* box_flag;
+    uint32_t box_value;
+    // plane order of the chain-B sweep: ascending from x_first (descending
+    // from x_first + x_len - 1 when reverse), both mod nxl, so the planes
+    // around the rotor (a hint from KK, x_len of them) are swept first
+    int32_t x_first, x_len;
 };
 
 // exact flavour (lbw_kernels_exact.cu, -fmad=false)

@@ -247,11 +247,12 @@ __device__ __forceinline__ void actuator_force_k(const ForceView& fv, int64_t xg
             if (dc[2 * kw + t] == z) {
                 const double w = __dmul_rn(wxy, dw[2 * kw + t]);
                 for (int c = 0; c < 3; ++c)
-                    // flat may have been written earlier in this very launch
-                    // (fused step): a volatile load never hits a stale L1
-                    // line (generic: the K4 copy of the view is in smem)
-                    F[c] = (double)(T)__dadd_rn(
-                        F[c], __dmul_rn(w, *(const volatile double*)(fv.flat + p * 3 + c)));
+                    // plain (L1-coherent) loads: flat is written by another
+                    // kernel or, in the flag-ordered / fused steps, by
+                    // another CTA whose completion flag this CTA acquired
+                    // (the acquire invalidates this SM's L1) -- never
+                    // ld.global.nc here
+                    F[c] = (double)(T)__dadd_rn(F[c], __dmul_rn(w, fv.flat[p * 3 + c]));
             }
         }
     }
@@ -390,11 +391,102 @@ __device__ __forceinline__ void gate_wait(const uint32_t* flag, uint32_t value, 
         uint32_t v;
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
         if (v >= value) break;
-        __nanosleep(128);
-        if (++n > 20000000LL) {
+        __nanosleep(32);
+        if (++n > 40000000LL) {
             if (err) atomicExch(err, 1);
             break;
         }
+    }
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Chain-B cell update (SweepArgs kin_flag != nullptr): CTA-uniform control
+// flow (valid = the thread has a cell); see SweepArgs for the flags.
+template <int OP, bool PULL, class T>
+__device__ __forceinline__ void sweep_cell_chain(const SweepArgs& a, int x, int y, int z, bool valid,
+                                                 int tid) {
+    const Geom& g = a.g;
+    const T* src = static_cast<const T*>(a.src);
+    const int64_t row = (int64_t)x * g.ny + y;
+    // the flag (thread 0) and both row keys are loaded with the populations
+    // (one round trip); keys read before the geometry of step m+1 was
+    // published are re-read after the wait
+    const uint32_t kin = tid == 0 ? ld_acquire_u32(a.kin_flag) : a.kin_value;
+    uint64_t key = 0ull, skey = 0ull;
+    double f[27];
+    if (valid) {
+        key = a.fv.row_key[row];
+        skey = a.skey[row];
+        if (PULL && pull_is_simple(g, x, y, z)) load_cell_simple(src, g, x, y, z, f);
+        else load_cell<PULL>(src, g, x, y, z, f);
+    }
+    if (__syncthreads_or(kin < a.kin_value)) {
+        if (tid == 0) gate_wait(a.kin_flag, a.kin_value, a.gate_error);
+        __syncthreads();
+        if (valid) {
+            key = *(const volatile uint64_t*)(a.fv.row_key + row);
+            skey = *(const volatile uint64_t*)(a.skey + row);
+        }
+    }
+    // rows of step m+1's sampling cubes: store the force-free half of this
+    // collide's macro (rho, sum f c) now -- the sampling of step m+1
+    // completes u with this step's force -- so the next step's chain can
+    // start before this tile has its force
+    const bool store = valid && (uint32_t)(skey >> 32) == a.store_tag;
+    if (store) {
+        double rho, mx, my, mz;
+        raw_sums_exact(f, rho, mx, my, mz);
+        double* b = a.spool + (int64_t)(uint32_t)skey * 4 * g.zp + z;
+        b[0] = rho;
+        b[g.zp] = mx;
+        b[2 * g.zp] = my;
+        b[3 * g.zp] = mz;
+    }
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0 &&
+        *(const volatile int32_t*)a.pool_tiles == 0) {
+        // no sampling row in this slab: nothing to wait for
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.box_flag), "r"(a.box_value)
+                     : "memory");
+    }
+    const bool any_store = __syncthreads_or(store);
+    if (any_store) {
+        LBW_TRACE_BEGIN(7, a.step);
+        LBW_TRACE_END(7, a.step);
+    }
+    if (any_store && tid == 0) {
+        // the last pool tile publishes "the samples of step m+1 are stored"
+        const uint32_t target = (uint32_t)*(const volatile int32_t*)a.pool_tiles;
+        __threadfence();
+        const uint32_t done = atomicAdd(a.pool_cnt, 1u) + 1u;
+        if (done == target) {
+            *a.pool_cnt = 0u;   // for the next sweep (it starts after this one completes)
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.box_flag), "r"(a.box_value)
+                         : "memory");
+            LBW_TRACE_END(5, a.step);
+        }
+    }
+    // a tile with force rows of step m waits for the point forces of step m
+    const bool need = valid && (uint32_t)(key >> 32) == a.fv.tag;
+    if (__syncthreads_or(need)) {
+        LBW_TRACE_BEGIN(6, a.step);
+        if (tid == 0) gate_wait(a.k4_flag, a.k4_value, a.gate_error);
+        __syncthreads();
+        LBW_TRACE_END(6, a.step);
+    }
+    if (valid) {
+        double Fx, Fy, Fz;
+        force_from_key<T>(a.fv, g, key, x, y, z, Fx, Fy, Fz);
+        const Macro m = collide_cell<OP>(f, Fx, Fy, Fz, a.r);
+        flag_nonfinite<T>(a.nan_key, a.step, ((g.x0 + x) * g.ny + y) * (int64_t)g.nz + z, m);
+        T* d = static_cast<T*>(a.dst) + buf_index(g, x + 1, 0, y, z);
+#pragma unroll
+        for (int i = 0; i < 27; ++i) st_pop(d + i * (int)g.dir_stride, f[i]);
     }
 }
 
@@ -431,6 +523,26 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) k_sweep(SweepArgs a) {
     LBW_TRACE_BEGIN(0, a.step);
     if (z < g.nz && y < g.ny) sweep_cell<OP, PULL, T>(a, x, y, z);
     if (edge) edge_done(a.halo);  // whole CTA, uniform branch
+    LBW_TRACE_END(0, a.step);
+}
+
+// K1 with the flag-ordered actuator chain (single slab, SweepArgs kin_flag):
+// the same plane order (ascending / alternating), no halo, no box gate.
+template <int OP, bool PULL, int MINB, class T>
+__global__ void __launch_bounds__(kSweepThreads, MINB) k_sweep_cb(SweepArgs a) {
+    const Geom& g = a.g;
+    const int z = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y * blockDim.y + threadIdx.y;
+    const int bz = (int)blockIdx.z;
+    const int np = a.x_end - a.x_begin;
+    // rotated plane order: the rotor's planes first (single slab: np == nxl)
+    const int r = a.reverse ? a.x_first + a.x_len - 1 - bz : a.x_first + bz;
+    const int x = a.x_begin + ((r % np) + np) % np;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    LBW_TRACE_BEGIN(0, a.step);
+    sweep_cell_chain<OP, PULL, T>(a, x, y, z, z < g.nz && y < g.ny,
+                                  (int)(threadIdx.x + threadIdx.y * blockDim.x));
     LBW_TRACE_END(0, a.step);
 }
 
@@ -493,8 +605,9 @@ inline bool sweep_pdl() {
 // one K1 launch, programmatic stream serialisation allowed (see k_sweep)
 template <int OP, bool PULL, int MINB, class T>
 void launch_k_sweep_pdl(dim3 grd, dim3 blk, const SweepArgs& b, cudaStream_t s) {
+    auto kern = b.kin_flag ? k_sweep_cb<OP, PULL, MINB, T> : k_sweep<OP, PULL, MINB, T>;
     if (!sweep_pdl() || !b.pdl) {
-        k_sweep<OP, PULL, MINB, T><<<grd, blk, 0, s>>>(b);
+        kern<<<grd, blk, 0, s>>>(b);
         return;
     }
     cudaLaunchConfig_t cfg = {};
@@ -507,7 +620,7 @@ void launch_k_sweep_pdl(dim3 grd, dim3 blk, const SweepArgs& b, cudaStream_t s) 
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_sweep<OP, PULL, MINB, T>, b);
+    cudaLaunchKernelEx(&cfg, kern, b);
 }
 
 template <int MINB, class T>

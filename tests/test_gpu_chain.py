@@ -1,0 +1,71 @@
+"""The flag-ordered actuator chain (default for a single slab with device
+kinematics and <= 64 points; lbw_alm.cu "chain B"): KK two steps ahead
+computes the geometry, the sweep stores the (rho, u) of the next step's
+sampling rows and signals when they are stored, K4 waits for that in-kernel
+and samples them, the sweep's force tiles wait in-kernel for K4 -- no stream
+event on the main stream.  It must equal the event-ordered chain
+(LBW_CHAIN_FLAGS=0): bit for bit in the exact flavour (the pooled macro IS
+the collide's output, which the event-ordered chain recomputes with the same
+arithmetic), within the fast flavour's tolerance otherwise; across priming,
+state changes, advance(n) and the load series."""
+
+import numpy as np
+import pytest
+
+from tests.test_gpu_fused import CASES, _run
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_flags_exact_bitwise_vs_events(gpu, monkeypatch, case):
+    a = _run(monkeypatch, False, case, "exact", 30, chain="flags")
+    b = _run(monkeypatch, False, case, "exact", 30, chain="events")
+    for n in range(30):
+        assert np.array_equal(a["samples"][n], b["samples"][n]), n
+        assert np.array_equal(a["blade"][n], b["blade"][n]), n
+    assert np.array_equal(a["kin"], b["kin"])
+    assert np.array_equal(a["f"], b["f"])
+    assert np.array_equal(a["force"], b["force"])
+
+
+@pytest.mark.parametrize("case", ["periodic", "inflow"])
+def test_flags_fast_vs_events(gpu, monkeypatch, case):
+    a = _run(monkeypatch, False, case, "fast", 40, chain="flags")
+    b = _run(monkeypatch, False, case, "fast", 40, chain="events")
+    for n in range(40):
+        np.testing.assert_allclose(a["samples"][n], b["samples"][n], rtol=1e-12, atol=1e-16)
+        np.testing.assert_allclose(a["blade"][n], b["blade"][n], rtol=1e-10, atol=1e-13)
+    np.testing.assert_allclose(a["f"], b["f"], rtol=0, atol=1e-14)
+
+
+def test_flags_state_changes_and_loads(gpu, monkeypatch):
+    def upload(sim):
+        sim.fields[0].interior = sim.fields[0].interior
+
+    poke = {2: upload, 5: lambda s: s._recompute_moments(), 6: upload,
+            11: lambda s: s.fields[0].interior}
+    a = _run(monkeypatch, False, "inflow", "exact", 16, poke=poke, loads=True, chain="flags")
+    b = _run(monkeypatch, False, "inflow", "exact", 16, poke=poke, loads=True, chain="events")
+    for n in range(16):
+        assert np.array_equal(a["blade"][n], b["blade"][n]), n
+    assert np.array_equal(a["f"], b["f"])
+    assert np.array_equal(a["loads"], b["loads"])
+
+
+def test_flags_advance_many_steps(gpu, monkeypatch):
+    from paper_2402_13171_b200 import Simulation
+    from tests.scenarios import rotor_config
+    monkeypatch.setenv("LBW_FUSED", "0")
+    monkeypatch.setenv("LBW_CHAIN_FLAGS", "1")
+    cells, per, bc, pos = CASES["periodic"]
+    cfg, tmp = rotor_config(cells=cells, periodic=per, boundary=bc, position=pos)
+    sim = Simulation(cfg)
+    sim.advance(50)
+    sim.synchronize()
+    fa, ba = sim.fields[0].interior.copy(), sim._alm_results()[2].copy()
+    sim.close()
+    tmp.cleanup()
+    b = _run(monkeypatch, False, "periodic", "exact", 50, chain="events")
+    assert np.array_equal(ba, b["blade"][-1])
+    assert np.array_equal(fa, b["f"])

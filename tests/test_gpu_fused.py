@@ -25,8 +25,11 @@ CASES = {
 }
 
 
-def _run(monkeypatch, fused, case, arithmetic, steps, poke=None, loads=False):
+def _run(monkeypatch, fused, case, arithmetic, steps, poke=None, loads=False, chain=None):
+    """fused: LBW_FUSED=1; else the standalone chain, event-ordered
+    (chain="events") or flag-ordered (chain="flags", the default mode)."""
     monkeypatch.setenv("LBW_FUSED", "1" if fused else "0")
+    monkeypatch.setenv("LBW_CHAIN_FLAGS", "0" if chain == "events" else "1")
     cells, per, bc, pos = CASES[case]
     cfg, tmp = rotor_config(cells=cells, periodic=per, boundary=bc, position=pos,
                             arithmetic=arithmetic)
@@ -54,7 +57,7 @@ def _run(monkeypatch, fused, case, arithmetic, steps, poke=None, loads=False):
 @pytest.mark.parametrize("case", sorted(CASES))
 def test_fused_exact_bitwise_vs_standalone_chain(gpu, monkeypatch, case):
     a = _run(monkeypatch, True, case, "exact", 24)
-    b = _run(monkeypatch, False, case, "exact", 24)
+    b = _run(monkeypatch, False, case, "exact", 24, chain="events")
     for n in range(24):
         assert np.array_equal(a["samples"][n], b["samples"][n]), n
         assert np.array_equal(a["blade"][n], b["blade"][n]), n
@@ -66,7 +69,7 @@ def test_fused_exact_bitwise_vs_standalone_chain(gpu, monkeypatch, case):
 @pytest.mark.parametrize("case", ["periodic", "inflow"])
 def test_fused_fast_vs_standalone_chain(gpu, monkeypatch, case):
     a = _run(monkeypatch, True, case, "fast", 40)
-    b = _run(monkeypatch, False, case, "fast", 40)
+    b = _run(monkeypatch, False, case, "fast", 40, chain="events")
     for n in range(40):
         np.testing.assert_allclose(a["samples"][n], b["samples"][n], rtol=1e-12, atol=1e-16)
         np.testing.assert_allclose(a["blade"][n], b["blade"][n], rtol=1e-10, atol=1e-13)
@@ -86,7 +89,7 @@ def test_fused_survives_state_changes(gpu, monkeypatch):
 
     poke = {3: upload, 7: recompute, 8: upload, 15: lambda s: s.fields[0].interior}
     a = _run(monkeypatch, True, "inflow", "exact", 20, poke=poke)
-    b = _run(monkeypatch, False, "inflow", "exact", 20, poke=poke)
+    b = _run(monkeypatch, False, "inflow", "exact", 20, poke=poke, chain="events")
     for n in range(20):
         assert np.array_equal(a["blade"][n], b["blade"][n]), n
     assert np.array_equal(a["f"], b["f"])
@@ -96,7 +99,7 @@ def test_fused_load_series(gpu, monkeypatch):
     """The per-step blade loads the fused step writes in-kernel into the
     pinned ring equal the standalone chain's copies."""
     a = _run(monkeypatch, True, "periodic", "exact", 12, loads=True)
-    b = _run(monkeypatch, False, "periodic", "exact", 12, loads=True)
+    b = _run(monkeypatch, False, "periodic", "exact", 12, loads=True, chain="events")
     assert a["loads"].shape == b["loads"].shape == (12, 18, 3)
     assert np.array_equal(a["loads"], b["loads"])
     assert np.array_equal(a["loads"][-1], a["blade"][-1])
@@ -113,7 +116,7 @@ def test_fused_advance_many_steps(gpu, monkeypatch):
     fa = sim.fields[0].interior.copy()
     ba = sim._alm_results()[2].copy()
     sim.close()
-    b = _run(monkeypatch, False, "inflow", "exact", 30)
+    b = _run(monkeypatch, False, "inflow", "exact", 30, chain="events")
     assert np.array_equal(ba, b["blade"][-1])
     assert np.array_equal(fa, b["f"])
     tmp.cleanup()

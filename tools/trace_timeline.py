@@ -43,6 +43,23 @@ for tu in ("fast", "alm"):
     tabs[tu] = buf
 t0 = int(tabs["fast"][0, s0 & 63, 0])
 names = [("fast", 0, "sweep"), ("alm", 1, "KK"), ("alm", 2, "K4"), ("alm", 4, "K5")]
+# chain-B sweep events: first force-tile wait start / last release, samples stored
+for st in range(s0 + 30, s0 + 34):
+    b = int(tabs["fast"][0, st & 63, 0])
+    fb, fe = (int(v) for v in tabs["fast"][6, st & 63])
+    pe = int(tabs["fast"][5, st & 63, 1])
+    sb, se = (int(v) for v in tabs["fast"][7, st & 63])
+    if fe and pe:
+        print(f"sweep({st}): force tiles wait {(fb - b) / 1e3:.2f} .. {(fe - b) / 1e3:.2f} us, "
+              f"sample tiles {(sb - b) / 1e3:.2f} .. {(se - b) / 1e3:.2f}, "
+              f"samples stored at {(pe - b) / 1e3:.2f} us (after the sweep start)")
+# chain-B KK phase ends (END markers only: kinematics, geometry), as offsets from KK start
+for st in range(s0 + 30, s0 + 34):
+    b = int(tabs["alm"][1, st & 63, 0])
+    e5, e6, e1 = (int(tabs["alm"][i, st & 63, 1]) for i in (5, 6, 1))
+    if b != int(np.uint64(~np.uint64(0))) and e5 and e6:
+        print(f"KK({st}) phases: kinematics {(e5 - b) / 1e3:.2f} us, geometry "
+              f"{(e6 - e5) / 1e3:.2f} us, count+publish {(e1 - e6) / 1e3:.2f} us")
 print("step  " + "  ".join(f"{nm:>17s}" for _, _, nm in names))
 spans = {nm: [] for _, _, nm in names}
 for st in range(s0, s0 + 40):
