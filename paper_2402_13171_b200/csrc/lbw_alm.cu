@@ -124,6 +124,9 @@ struct AlmState {
     uint32_t* cb_flags = nullptr;
     int32_t* cb_pool_tiles = nullptr;   // (kSlots)
     int32_t* cb_box_h = nullptr;        // (kSlots, 2) pinned, device-mapped: [x_first, x_len] hint per KK
+    int32_t* cb_cf_n = nullptr;         // (kSlots, P, 8) corner-force term counts
+    int16_t* cb_cf_p = nullptr;         // (kSlots, P, 8, kCornerTerms)
+    double* cb_cf_w = nullptr;
     int32_t* cb_box_d = nullptr;
     int64_t cb_next = -1;               // step the chain-B pipeline is primed for
     int64_t fs_prof_n = 0;
@@ -311,10 +314,67 @@ __global__ void k_fs_prime(KinDev k, AlmDev a, Geom g, int per_x, int advance, i
 // row keys (fs_geometry), the number of sweep tiles holding rows of step j's
 // sampling cubes, the plane-order hint, then "geometry(j) done" = j+1 once
 // geometry(j-1) has published (flags are maxima: publish in step order).
+struct CornerLists {
+    const int32_t* prev_cell;   // deposit cells / weights of the step before J
+    const double* prev_w;       // (nullptr: not built)
+    const double* ckin;         // kinematics rows of step J (its sampling corners)
+    uint32_t ckin_value;        // wait for "kinematics done" >= this first (0: no wait)
+    uint32_t k4_value;          // ... and for "K4 done" >= this (the slot's last reader)
+    int32_t* n;                 // (P, 8)
+    int16_t* p;                 // (P, 8, kCornerTerms)
+    double* w;
+    int32_t inflow;
+    double u_in[3];
+};
+
+// For each sampling corner of this step: the previous step's deposit terms
+// reaching that cell, in the order actuator_force_k adds them (ascending
+// point, the last x / y match, every z match), weight (wx wy) wz rounded as
+// there -- so the sampling sums a few terms instead of scanning the points.
+__device__ __forceinline__ void cb_corner_lists(const AlmDev& a, const Geom& g, int per_x,
+                                                const CornerLists& L, int tid, int nthr) {
+    const int kw = a.kw;
+    for (int q = tid; q < 8 * a.n; q += nthr) {
+        const int pt = q >> 3, c = q & 7;
+        const double* kr = L.ckin + (int64_t)pt * kKin;
+        int64_t j0[3];
+        for (int k = 0; k < 3; ++k) j0[k] = (int64_t)floor(kr[k] - 0.5);
+        int x = 0, y = 0, z = 0;
+        double v[4];
+        const int code = corner_map(g, per_x, L.inflow, L.u_in, j0[0] + ((c >> 2) & 1),
+                                    j0[1] + ((c >> 1) & 1), j0[2] + (c & 1), x, y, z, v);
+        int cnt = 0;
+        if (code == MA_OWNED) {
+            const int64_t xg = g.x0 + x;
+            for (int p = 0; p < a.n && cnt >= 0; ++p) {
+                const int32_t* dc = L.prev_cell + (int64_t)p * 3 * kw;
+                const double* dw = L.prev_w + (int64_t)p * 3 * kw;
+                double wx = 0.0, wy = 0.0;
+                bool hx = false, hy = false;
+                for (int t = 0; t < kw; ++t) {
+                    if (dc[t] == xg) { hx = true; wx = dw[t]; }
+                    if (dc[kw + t] == y) { hy = true; wy = dw[kw + t]; }
+                }
+                if (!(hx && hy)) continue;
+                const double wxy = __dmul_rn(wx, wy);
+                for (int t = 0; t < kw; ++t) {
+                    if (dc[2 * kw + t] != z) continue;
+                    if (cnt >= kCornerTerms) { cnt = -1; break; }
+                    L.p[(int64_t)q * kCornerTerms + cnt] = (int16_t)p;
+                    L.w[(int64_t)q * kCornerTerms + cnt] = __dmul_rn(wxy, dw[2 * kw + t]);
+                    ++cnt;
+                }
+            }
+        }
+        L.n[q] = cnt;
+    }
+}
+
 __device__ __forceinline__ void cb_geometry_body(const AlmDev& a, const Geom& g, int per_x,
                                                  const FsGeom& geo, int ty, int tiles_x,
                                                  int32_t* pool_tiles, uint32_t* flags,
-                                                 uint32_t value, int32_t* box_hint) {
+                                                 uint32_t value, int32_t* box_hint,
+                                                 const CornerLists& cl) {
     __shared__ uint32_t pairs[4 * kOnTheFlyMaxPoints];
     __shared__ uint32_t dup[4 * kOnTheFlyMaxPoints];
     __shared__ int cnt, blo, bhi;
@@ -326,6 +386,15 @@ __device__ __forceinline__ void cb_geometry_body(const AlmDev& a, const Geom& g,
         bhi = INT_MIN;
     }
     fs_geometry(geo, a, g, per_x, tid, nthr);   // synchronises the CTA
+    if (cl.prev_cell) {
+        if (tid == 0) {
+            int32_t* err = reinterpret_cast<int32_t*>(flags + 5);
+            if (cl.ckin_value) gate_wait(flags, cl.ckin_value, err);
+            if (cl.k4_value) gate_wait(flags + 1, cl.k4_value, err);
+        }
+        __syncthreads();
+        cb_corner_lists(a, g, per_x, cl, tid, nthr);
+    }
     // sampling rows -> sweep tiles (x plane, y block), and the plane range
     // of the points relative to point 0 (wrapped on a periodic x axis)
     const double zero3[3] = {0.0, 0.0, 0.0};
@@ -393,12 +462,12 @@ __device__ __forceinline__ void cb_kin_body(const KinDev& k, const AlmDev& a, co
 // priming: kinematics + geometry of step j in one CTA, serially
 __global__ void k_cb_kk(KinDev k, AlmDev a, Geom g, int per_x, int advance, int do_kin,
                         FsGeom geo, int ty, int tiles_x, int32_t* pool_tiles, uint32_t* flags,
-                        uint32_t value, int32_t* box_hint) {
+                        uint32_t value, int32_t* box_hint, CornerLists cl) {
     extern __shared__ double csm[];
     LBW_TRACE_BEGIN(1, a.step);
     cb_kin_body(k, a, g, per_x, advance, do_kin, flags, value, csm);
     __syncthreads();
-    cb_geometry_body(a, g, per_x, geo, ty, tiles_x, pool_tiles, flags, value, box_hint);
+    cb_geometry_body(a, g, per_x, geo, ty, tiles_x, pool_tiles, flags, value, box_hint, cl);
     LBW_TRACE_END(1, a.step);
 }
 
@@ -425,6 +494,7 @@ struct CbChainArgs {
     uint32_t kin_value;         // jk + 1
     uint32_t slot_value;        // the slot of step jk is free once box >= slot_value
     int32_t* box_hint;          // (2) plane-order hint of step jk (mapped host memory)
+    CornerLists cl;             // geometry: corner-force lists of step jk
 };
 
 // The chain of step j: three launches on the actuator stream -- K4(j),
@@ -463,7 +533,7 @@ __global__ void __launch_bounds__(128) k_cb_chain(CbChainArgs A) {
         __syncthreads();
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         cb_geometry_body(A.akk, A.g, A.per_x, A.geo, A.ty, A.tiles_x, A.pool_tiles_kk, A.flags,
-                         A.kin_value, A.box_hint);
+                         A.kin_value, A.box_hint, A.cl);
         LBW_TRACE_END(1, A.akk.step);
         return;
     }
@@ -472,7 +542,7 @@ __global__ void __launch_bounds__(128) k_cb_chain(CbChainArgs A) {
     double* sw = csm;                                          // (n, 3, kw) weights
     double* sfl = sw + (size_t)A.a.n * 3 * A.a.kw;             // (n, 3) forces
     int32_t* sdc = reinterpret_cast<int32_t*>(sfl + (size_t)A.a.n * 3);  // (n, 3, kw) cells
-    const bool stage = A.use_pool && A.pool.fv.npts > 0;
+    const bool stage = false;   // deposit terms come from the corner lists
     if (tid == 0) {
         gate_wait(A.flags + 6, A.k4_value, err);   // geometry(j) done: flag >= j+1
         if (A.use_pool && *(const volatile int32_t*)A.pool_tiles > 0)
@@ -503,8 +573,8 @@ __global__ void __launch_bounds__(128) k_cb_chain(CbChainArgs A) {
     if (stage) {
         pool.fv.dep_w = sw;
         pool.fv.dep_cell = sdc;
-        pool.fv.flat = sfl;
     }
+    if (A.use_pool) pool.fv.flat = sfl;   // staged after K4(j-1)
     ForceSet none{};
     CubeArgs cube{};
     point_warp(A.a, A.g, A.md, none, 0, cube, p, lane, in, A.use_pool ? &pool : nullptr, false);
@@ -643,6 +713,13 @@ int dev_alloc(lbw_domain* d, AlmState* s, T** p, size_t count) {
 
 bool alm_active(const lbw_domain* d) { return d->alm != nullptr && d->alm->n > 0; }
 
+cudaError_t alm_sync_side(const lbw_domain* d) {
+    if (!d->alm) return cudaSuccess;
+    cudaError_t e = cudaSuccess;
+    if (d->alm->kin_stream && e == cudaSuccess) e = cudaStreamSynchronize(d->alm->kin_stream);
+    return e;
+}
+
 int alm_support_halo(const lbw_domain* d) { return alm_active(d) ? d->alm->halo_x : 0; }
 
 double* alm_cube(const lbw_domain* d) { return alm_active(d) ? d->alm->cube : nullptr; }
@@ -720,6 +797,7 @@ int alm_invalidate(lbw_domain* d) {
     d->touched = true;
     if (!alm_active(d)) return LBW_OK;
     LBW_CK(cudaStreamSynchronize(d->alm_stream));
+    LBW_CK(alm_sync_side(d));
     if (d->alm->kin_stream) LBW_CK(cudaStreamSynchronize(d->alm->kin_stream));
     d->alm->ready_step = -1;
     d->alm->fs_next = -1;
@@ -919,6 +997,7 @@ int alm_fused_launch(lbw_domain* d, bool pull, ForceView* fv_out) {
         // whatever the standalone chain queued is finished before its
         // outputs are rewritten here
         LBW_CK(cudaStreamSynchronize(d->alm_stream));
+    LBW_CK(alm_sync_side(d));
         if (s->kin_stream) LBW_CK(cudaStreamSynchronize(s->kin_stream));
         int rc = fs_prime(d, m);
         if (!rc) rc = fs_prime(d, m + 1);
@@ -1042,10 +1121,12 @@ int alm_fused_launch(lbw_domain* d, bool pull, ForceView* fv_out) {
 bool alm_chainb_eligible(const lbw_domain* d) {
     const AlmState* s = d->alm;
     if (!(d->chainb && s && s->n > 0 && s->kin_device && s->on_the_fly && s->n_rings == 0 &&
-          !d->linked && !d->user_active && d->prelaunch && !tool_injected() &&
-          s->kin_smem <= 48 * 1024))
+          !d->linked && !d->user_active && d->prelaunch && s->kin_smem <= 48 * 1024))
         return false;
+    // forced (LBW_CHAIN_FLAGS=1) it also runs under a profiler that
+    // serialises kernels: every wait is on work launched earlier
     if (d->chainb_forced) return true;
+    if (tool_injected()) return false;
     return (int64_t)d->g.nxl * d->g.ny * d->g.nz < 1500000;
 }
 
@@ -1062,6 +1143,10 @@ static int cb_allocate(lbw_domain* d) {
     if (!s->cb_flags) {
         int rc = dev_alloc(d, s, &s->cb_flags, 8);
         if (!rc) rc = dev_alloc(d, s, &s->cb_pool_tiles, kSlots);
+        const size_t nc8 = (size_t)kSlots * s->n * 8;
+        if (!rc) rc = dev_alloc(d, s, &s->cb_cf_n, nc8);
+        if (!rc) rc = dev_alloc(d, s, &s->cb_cf_p, nc8 * kCornerTerms);
+        if (!rc) rc = dev_alloc(d, s, &s->cb_cf_w, nc8 * kCornerTerms);
         if (rc) return rc;
         LBW_CK(cudaMemset(s->cb_flags, 0, 8 * sizeof(uint32_t)));
         LBW_CK(cudaMemset(s->cb_pool_tiles, 0, kSlots * sizeof(int32_t)));
@@ -1074,8 +1159,29 @@ static int cb_allocate(lbw_domain* d) {
     return LBW_OK;
 }
 
+// corner-force lists of step j (from the deposit geometry of step j-1 and
+// the sampling corners of step j); built by the geometry kernel of step j
+// (priming) or of step j-1 (steady state: it waits for the kinematics of j)
+static CornerLists cb_lists(const lbw_domain* d, int64_t j, bool build) {
+    const AlmState* s = d->alm;
+    CornerLists L{};
+    if (build) {
+        const FsGeom prev = fs_geom(d, j - 1);
+        L.prev_cell = prev.dep_cell;
+        L.prev_w = prev.dep_w;
+        L.ckin = s->kin + (size_t)(j % kSlots) * s->n * kKin;
+    }
+    const size_t off = (size_t)(j % kSlots) * s->n * 8;
+    L.n = s->cb_cf_n + off;
+    L.p = s->cb_cf_p + off * kCornerTerms;
+    L.w = s->cb_cf_w + off * kCornerTerms;
+    L.inflow = d->desc.boundary == LBW_BC_INFLOW_OUTFLOW ? 1 : 0;
+    for (int k = 0; k < 3; ++k) L.u_in[k] = d->desc.u_in[k];
+    return L;
+}
+
 // KK(j) of chain B on stream st
-static int cb_kk(lbw_domain* d, int64_t j, cudaStream_t st) {
+static int cb_kk(lbw_domain* d, int64_t j, cudaStream_t st, bool lists) {
     AlmState* s = d->alm;
     int do_kin = 0, advance = 0;
     if (s->kin_valid[j % kSlots] != j) {
@@ -1094,7 +1200,7 @@ static int cb_kk(lbw_domain* d, int64_t j, cudaStream_t st) {
     k_cb_kk<<<1, 128, do_kin ? s->kin_smem : 0, st>>>(
         kd, s->dev(j), d->g, d->desc.periodic[0] ? 1 : 0, advance, do_kin, fs_geom(d, j),
         (int)blk.y, tiles_x, s->cb_pool_tiles + j % kSlots, s->cb_flags, (uint32_t)(j + 1),
-        s->cb_box_d + 2 * (j % kSlots));
+        s->cb_box_d + 2 * (j % kSlots), cb_lists(d, j, lists));
     count_launch();
     LBW_CK(cudaGetLastError());
     if (do_kin) {
@@ -1124,6 +1230,12 @@ static int cb_chain(lbw_domain* d, int64_t j, cudaStream_t st, bool use_pool, bo
     A.pool.error_flags = s->error_flags;
     A.pool.raw = 1;
     A.pool.fv = fs_view(d, j - 1);
+    {
+        const CornerLists L = cb_lists(d, j, false);
+        A.pool.cf_n = L.n;
+        A.pool.cf_p = L.p;
+        A.pool.cf_w = L.w;
+    }
     A.use_pool = use_pool ? 1 : 0;
     A.box_flag = s->cb_flags + 2;
     A.box_value = (uint32_t)j;
@@ -1175,6 +1287,11 @@ static int cb_chain(lbw_domain* d, int64_t j, cudaStream_t st, bool use_pool, bo
         C.kin_value = (uint32_t)(jg + 1);
         C.slot_value = (uint32_t)(jg - 4);
         C.box_hint = s->cb_box_d + 2 * (jg % kSlots);
+        // lists of step jg+1: its kinematics first, and the slot's last
+        // reader K4(jg+1-6) done
+        C.cl = cb_lists(d, jg + 1, true);
+        C.cl.ckin_value = (uint32_t)(jg + 2);
+        C.cl.k4_value = (uint32_t)(jg - 4);
         LBW_CK(launch_cb_chain(C, 1, 0, st, true));
         count_launch();
     }
@@ -1192,12 +1309,13 @@ int alm_chainb_before(lbw_domain* d, SweepArgs* a) {
         // geometry of steps m .. m+4 and the forces of step m (sampled by
         // recomputation from the last collide's input) go on the main stream
         LBW_CK(cudaStreamSynchronize(d->alm_stream));
+    LBW_CK(alm_sync_side(d));
         if (s->kin_stream) LBW_CK(cudaStreamSynchronize(s->kin_stream));
         LBW_CK(cudaMemsetAsync(s->cb_flags + 3, 0, 2 * sizeof(uint32_t), d->stream));
         // kinematics + geometry of m .. m+4 (geometry publishes in step
         // order: restart its flag at m)
         rc = stream_write32(d->stream, s->cb_flags + 6, (uint32_t)m);
-        for (int64_t j = m; j <= m + 4 && !rc; ++j) rc = cb_kk(d, j, d->stream);
+        for (int64_t j = m; j <= m + 4 && !rc; ++j) rc = cb_kk(d, j, d->stream, j > m);
         if (!rc) rc = cb_chain(d, m, d->stream, false, false);
         if (rc) return rc;
         // the chains queued from now on (actuator stream) read what these
@@ -1235,8 +1353,8 @@ int alm_chainb_before(lbw_domain* d, SweepArgs* a) {
 
 int alm_chainb_after(lbw_domain* d, int64_t m) {
     AlmState* s = d->alm;
-    // the chain of step m+1 (K4(m+1) + KK(m+5)) on the actuator stream: it
-    // waits in-kernel for sweep m's samples; nothing else orders it
+    // the chain of step m+1 (K4(m+1), kinematics(m+5), geometry(m+4)) on
+    // the actuator stream, ordered by flags only
     int rc = cb_chain(d, m + 1, d->alm_stream, true, true);
     if (rc) return rc;
     s->cb_next = m + 1;
@@ -1367,6 +1485,7 @@ int lbw_alm_configure(lbw_domain* d, const lbw_alm_desc* desc) {
     }
     LBW_CK(cudaStreamSynchronize(d->stream));
     LBW_CK(cudaStreamSynchronize(d->alm_stream));
+    LBW_CK(alm_sync_side(d));
     alm_destroy(d);
     const int P = desc->n_points;
     if (P == 0) return LBW_OK;
@@ -1532,6 +1651,7 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
     LBW_CK(cudaSetDevice(d->device));
     LBW_CK(cudaStreamSynchronize(d->stream));
     LBW_CK(cudaStreamSynchronize(d->alm_stream));
+    LBW_CK(alm_sync_side(d));
     std::vector<int32_t> point_comp(P, -1);
     for (int c = 0; c < C; ++c)
         for (int k = 0; k < kd->line_count[c]; ++k) point_comp[kd->line_first[c] + k] = c;
@@ -1724,6 +1844,7 @@ int lbw_alm_download_kinematics(lbw_domain* d, double* kin, double* spin, double
     LBW_CK(cudaSetDevice(d->device));
     LBW_CK(cudaStreamSynchronize(d->stream));
     LBW_CK(cudaStreamSynchronize(d->alm_stream));
+    LBW_CK(alm_sync_side(d));
     if (s->kin_stream) LBW_CK(cudaStreamSynchronize(s->kin_stream));
     if (kin)
         LBW_CK(cudaMemcpy(kin, s->kin + (size_t)(d->step > 0 ? (d->step - 1) % kSlots : 0) * s->n * kKin,
@@ -1813,6 +1934,7 @@ int lbw_alm_record_loads(lbw_domain* d, int64_t capacity) {
     AlmState* s = d->alm;
     LBW_CK(cudaSetDevice(d->device));
     LBW_CK(cudaStreamSynchronize(d->alm_stream));
+    LBW_CK(alm_sync_side(d));
     LBW_CK(cudaStreamSynchronize(d->stream));
     if (s->h_loads) cudaFreeHost(s->h_loads);
     s->h_loads = nullptr;
@@ -1844,6 +1966,7 @@ int lbw_alm_read_loads(lbw_domain* d, double* out, int64_t max_steps, int64_t* f
     LBW_REQ(avail < s->loads_cap || avail == 0,
             "load ring overflow: read the loads at least every capacity-1 steps");
     LBW_CK(cudaStreamSynchronize(d->alm_stream));
+    LBW_CK(alm_sync_side(d));
     LBW_CK(cudaStreamSynchronize(d->stream));   // the fused step writes loads in-kernel
     const int64_t k = std::min(avail, max_steps);
     const size_t row = (size_t)s->n * 3;

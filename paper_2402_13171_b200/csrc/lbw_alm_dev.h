@@ -104,6 +104,9 @@ struct KinDev {
 constexpr int kKP = 49;
 constexpr int kMaxKw = 13;   // eps <= 2 -> at most floor(6 eps * 2) + 1 cells
 constexpr int kOnTheFlyMaxPoints = 64;
+// corner-force lists (flag-ordered chain): at most this many deposit terms
+// per sampling corner; beyond it the sampling scans the points itself
+constexpr int kCornerTerms = 24;
 enum { MA_REMOTE = 0, MA_OWNED = 1, MA_CONST = 2 };
 
 
@@ -163,6 +166,13 @@ struct FsPool {
     // cell, u = (sum f c + F dt / 2) / rho -- moments_exact's arithmetic
     int32_t raw;
     ForceView fv;          // the force of sweep j-1
+    // optional: for each (point, corner) of step j the deposit terms of step
+    // j-1 that reach the corner cell -- (point, weight (wx wy) wz) in the
+    // order actuator_force_k adds them -- built by the geometry kernel of
+    // step j; count < 0: not listed (the sampling scans fv)
+    const int32_t* cf_n;   // (P, 8)
+    const int16_t* cf_p;   // (P, 8, kCornerTerms)
+    const double* cf_w;    // (P, 8, kCornerTerms)
 };
 
 // One launch of the fused step kernel (lbw_fused.cuh): sweep m, the point

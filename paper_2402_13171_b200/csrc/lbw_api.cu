@@ -195,6 +195,7 @@ static void free_domain(lbw_domain* d) {
     cudaSetDevice(d->device);
     if (d->stream) cudaStreamSynchronize(d->stream);
     if (d->alm_stream) cudaStreamSynchronize(d->alm_stream);
+    alm_sync_side(d);
     alm_destroy(d);
     for (void*& b : d->buf)
         if (b) cudaFree(b);
@@ -841,6 +842,7 @@ int lbw_domain_sync(lbw_domain* d) {
     LBW_CK(cudaSetDevice(d->device));
     LBW_CK(cudaStreamSynchronize(d->stream));
     LBW_CK(cudaStreamSynchronize(d->alm_stream));
+    LBW_CK(alm_sync_side(d));
     return alm_check_gate(d);
 }
 

@@ -731,7 +731,7 @@ __device__ __forceinline__ int corner_map(const Geom& g, int per_x, int inflow, 
 // the (rho, u) its collide computed for the keyed rows, already rounded
 // to the storage type as the reference's macro array holds them.
 __device__ __forceinline__ int pool_macro(const Geom& g, const FsPool& pl, int per_x, int64_t gx,
-                                          int64_t gy, int64_t gz, double out[4]) {
+                                          int64_t gy, int64_t gz, double out[4], int pc = -1) {
     int x = 0, y = 0, z = 0;
     const int code = corner_map(g, per_x, pl.inflow, pl.u_in, gx, gy, gz, x, y, z, out);
     if (code != MA_OWNED) return code;
@@ -747,10 +747,24 @@ __device__ __forceinline__ int pool_macro(const Geom& g, const FsPool& pl, int p
     if (pl.raw) {
         // out = (rho, mx, my, mz); the force of the previous sweep at the
         // cell, then u exactly as moments_exact forms it (dt = 1)
-        const uint64_t fkey = pl.fv.row_key ? pl.fv.row_key[(int64_t)x * g.ny + y] : 0ull;
         double F[3];
-        if (g.single) force_from_key<float>(pl.fv, g, fkey, x, y, z, F[0], F[1], F[2]);
-        else force_from_key<double>(pl.fv, g, fkey, x, y, z, F[0], F[1], F[2]);
+        const int nt = (pl.cf_n && pc >= 0) ? pl.cf_n[pc] : -1;
+        if (nt >= 0) {
+            // the listed deposit terms, in actuator_force_k's order
+            F[0] = F[1] = F[2] = 0.0;
+            for (int t = 0; t < nt; ++t) {
+                const int p = pl.cf_p[(int64_t)pc * kCornerTerms + t];
+                const double w = pl.cf_w[(int64_t)pc * kCornerTerms + t];
+                for (int c = 0; c < 3; ++c) {
+                    const double v = __dadd_rn(F[c], __dmul_rn(w, pl.fv.flat[p * 3 + c]));
+                    F[c] = g.single ? (double)(float)v : v;
+                }
+            }
+        } else {
+            const uint64_t fkey = pl.fv.row_key ? pl.fv.row_key[(int64_t)x * g.ny + y] : 0ull;
+            if (g.single) force_from_key<float>(pl.fv, g, fkey, x, y, z, F[0], F[1], F[2]);
+            else force_from_key<double>(pl.fv, g, fkey, x, y, z, F[0], F[1], F[2]);
+        }
         const double inv_rho = 1.0 / out[0];
         const double hdt = 0.5 * 1.0;
         for (int q = 0; q < 3; ++q) out[1 + q] = (out[1 + q] + hdt * F[q]) * inv_rho;
@@ -826,7 +840,7 @@ LBW_CHAIN_FN void point_warp(const AlmDev& a, const Geom& g, const MacroDev& m, 
     } else if (lane < 8) {
         const int64_t cgx = j0[0] + ((lane >> 2) & 1), cgy = j0[1] + ((lane >> 1) & 1),
                       cgz = j0[2] + (lane & 1);
-        const int code = pool ? pool_macro(g, *pool, m.per_x, cgx, cgy, cgz, v)
+        const int code = pool ? pool_macro(g, *pool, m.per_x, cgx, cgy, cgz, v, p * 8 + lane)
                               : macro_at(g, m, cgx, cgy, cgz, v);
         if (phase == 1) {
             const int64_t o = ((int64_t)p * 8 + lane) * 4;

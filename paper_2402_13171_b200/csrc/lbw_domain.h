@@ -143,6 +143,8 @@ bool alm_after_chainb(const lbw_domain* d);
 int alm_invalidate(lbw_domain* d);
 void alm_destroy(lbw_domain* d);
 bool alm_active(const lbw_domain* d);
+// wait for the kinematics stream of the actuator chain
+cudaError_t alm_sync_side(const lbw_domain* d);
 int alm_support_halo(const lbw_domain* d);   // spreading support half-width in x (cells)
 // device cube buffer (2, P, 8, 4) of the actuator sampling, or nullptr
 double* alm_cube(const lbw_domain* d);
