@@ -1115,8 +1115,12 @@ int alm_fused_launch(lbw_domain* d, bool pull, ForceView* fv_out) {
 // planes, and the main stream never waits for another stream.
 
 // Used on slabs below 1.5 M cells, where the chain's latency sets the step
-// time; on larger slabs the sweep hides the event-ordered chain and its
-// plainer kernel is faster (C2: 0.275 vs 0.291 ms per sweep).
+// time.  On larger slabs the sweep hides the event-ordered chain, and the
+// flag-ordered one costs the sweep ~5 % (C2: 0.2718 vs 0.2863 ms in the
+// same run; identical in isolation under ncu, 267.6 vs 268.8 us): its
+// chain launches wait resident for a whole sweep, holding registers of
+// ~2 SMs, and each CTA's acquire of the geometry flag flushes its SM's L1
+// (a relaxed read with L2-only key loads recovers ~1 %).
 // LBW_CHAIN_FLAGS: 0 never, 1 always (when eligible), unset: by size.
 bool alm_chainb_eligible(const lbw_domain* d) {
     const AlmState* s = d->alm;

@@ -420,8 +420,8 @@ __device__ __forceinline__ void sweep_cell_chain(const SweepArgs& a, int x, int 
     uint64_t key = 0ull, skey = 0ull;
     double f[27];
     if (valid) {
-        key = a.fv.row_key[row];
-        skey = a.skey[row];
+        key = __ldcg(reinterpret_cast<const unsigned long long*>(a.fv.row_key) + row);
+        skey = __ldcg(reinterpret_cast<const unsigned long long*>(a.skey) + row);
         if (PULL && pull_is_simple(g, x, y, z)) load_cell_simple(src, g, x, y, z, f);
         else load_cell<PULL>(src, g, x, y, z, f);
     }
