@@ -235,3 +235,43 @@ def test_standalone_abi_example(gpu):
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "energy decay rate" in r.stdout
+
+
+def test_abort_mode_config():
+    base = {"domain": {"cells": [8, 8, 8]},
+            "fluid": {"kinematic_viscosity": 0.1, "wind": [1.0, 0.0, 0.0]},
+            "resolution": {"mach": 0.1}}
+    assert parse_config(base).abort == "deferred"
+    raw = dict(base, run={"abort": "immediate"})
+    cfg = parse_config(raw)
+    assert cfg.abort == "immediate"
+    assert cfg.echo()["run"]["abort"] == "immediate"
+    with pytest.raises(ConfigError, match="run.abort"):
+        parse_config(dict(base, run={"abort": "sometimes"}))
+
+
+def test_bench_clock_summary_uses_timed_region_samples():
+    """bench.py's NVML clock sampler: the median and reasons come from the
+    samples inside the timed region when there are any (else the whole
+    window), throttle reasons are decoded from the NVML bit mask."""
+    import types
+
+    import bench
+    nv = types.SimpleNamespace(nvmlClocksEventReasonHwSlowdown=8,
+                               nvmlClocksEventReasonHwThermalSlowdown=64,
+                               nvmlClocksEventReasonSwThermalSlowdown=32,
+                               nvmlClocksEventReasonSwPowerCap=4)
+    cs = bench.ClockSampler(0)
+    cs.nv, cs.smax = nv, 1965.0
+    cs.samples = [(0.0, 1965.0, 0), (1.0, 1500.0, 4), (2.0, 1600.0, 4), (3.0, 1965.0, 0)]
+    cs.window = [0.5, 2.5]
+    s = cs.summary()
+    assert s["samples_in_timed_region"] == 2 and s["sm_mhz"] == 1550.0
+    assert s["reasons"] == ["sw_power_cap"] and s["window"] == "timed region"
+    cs.window = [10.0, 11.0]
+    s = cs.summary()
+    assert s["samples_in_timed_region"] == 0 and s["samples"] == 4
+    assert s["window"] == "warm-up + timed region"
+    cs.nv = None
+    cs.error = "NVML unavailable: test"
+    assert cs.summary()["reasons"] == ["NVML unavailable: test"]
