@@ -319,3 +319,4 @@ cudaError_t launch_force_from_aos(const double* aos, const Geom& g, uint64_t* ro
 }
 
 }  // namespace lbw
+LBW_TRACE_EXPORT(exact)

@@ -31,24 +31,25 @@ sim = Simulation(parse_config(raw, base_dir=tmp))
 lib = _lib.load()
 sim.advance(40)
 sim.synchronize()
-for tu in ("fast", "alm"):
+SW = "exact" if arith == "exact" else "fast"   # the TU holding the sweep kernels
+for tu in (SW, "alm"):
     getattr(lib, f"lbw_trace_reset_{tu}")()
 s0 = sim.step_index
 sim.advance(40)
 sim.synchronize()
 tabs = {}
-for tu in ("fast", "alm"):
+for tu in (SW, "alm"):
     buf = np.zeros((8, 64, 2), dtype=np.uint64)
     getattr(lib, f"lbw_trace_dump_{tu}")(buf.ctypes.data_as(ctypes.c_void_p))
     tabs[tu] = buf
-t0 = int(tabs["fast"][0, s0 & 63, 0])
-names = [("fast", 0, "sweep"), ("alm", 1, "KK"), ("alm", 2, "K4"), ("alm", 4, "K5")]
+t0 = int(tabs[SW][0, s0 & 63, 0])
+names = [(SW, 0, "sweep"), ("alm", 1, "KK"), ("alm", 2, "K4"), ("alm", 4, "K5")]
 # chain-B sweep events: first force-tile wait start / last release, samples stored
 for st in range(s0 + 30, s0 + 34):
-    b = int(tabs["fast"][0, st & 63, 0])
-    fb, fe = (int(v) for v in tabs["fast"][6, st & 63])
-    pe = int(tabs["fast"][5, st & 63, 1])
-    sb, se = (int(v) for v in tabs["fast"][7, st & 63])
+    b = int(tabs[SW][0, st & 63, 0])
+    fb, fe = (int(v) for v in tabs[SW][6, st & 63])
+    pe = int(tabs[SW][5, st & 63, 1])
+    sb, se = (int(v) for v in tabs[SW][7, st & 63])
     if fe and pe:
         print(f"sweep({st}): force tiles wait {(fb - b) / 1e3:.2f} .. {(fe - b) / 1e3:.2f} us, "
               f"sample tiles {(sb - b) / 1e3:.2f} .. {(se - b) / 1e3:.2f}, "
