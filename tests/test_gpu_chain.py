@@ -69,3 +69,58 @@ def test_flags_advance_many_steps(gpu, monkeypatch):
     b = _run(monkeypatch, False, "periodic", "exact", 50, chain="events")
     assert np.array_equal(ba, b["blade"][-1])
     assert np.array_equal(fa, b["f"])
+
+
+def _run_raw(monkeypatch, chain, raw, steps, upload_first=False):
+    import os
+    import tempfile
+
+    from paper_2402_13171_b200 import Simulation, parse_config
+    from tests.scenarios import write_rotor_files
+    monkeypatch.setenv("LBW_FUSED", "0")
+    monkeypatch.setenv("LBW_CHAIN_FLAGS", "1" if chain == "flags" else "0")
+    tmp = tempfile.TemporaryDirectory()
+    write_rotor_files(tmp.name)
+    sim = Simulation(parse_config(raw, base_dir=tmp.name))
+    if upload_first:   # a pre-collision state: the first sweep collides in place
+        f = sim.fields[0].interior
+        sim.fields[0].interior = f * (1.0 + 1e-3 * np.sin(np.arange(f.size)).reshape(f.shape))
+    blades = []
+    for _ in range(steps):
+        sim.step()
+        blades.append(sim._alm_results()[2].copy())
+    out = (np.array(blades), sim.fields[0].interior.copy(), sim.fields[0].interior_force.copy())
+    sim.close()
+    tmp.cleanup()
+    return out
+
+
+VARIANTS = {
+    "single": dict(precision="single"),
+    "gauss": dict(spreading={"kernel": "gaussian", "epsilon": 1.5}),
+    "walls": dict(periodic=(True, False, False),
+                  walls={"y_lo": "no_slip", "y_hi": "free_slip", "z_lo": "no_slip"}),
+    "bgk": dict(operator="bgk"),
+    "pre": dict(upload_first=True),
+}
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+def test_flags_variants_bitwise_vs_events(gpu, monkeypatch, variant):
+    """fp32 storage, Gaussian spreading (9 deposit cells per axis), walls,
+    BGK and a first in-place collide through the flag-ordered chain: bit
+    for bit the event-ordered chain."""
+    from tests.scenarios import rotor_raw
+    v = dict(VARIANTS[variant])
+    upload_first = v.pop("upload_first", False)
+    periodic = v.pop("periodic", (True, True, True))
+    raw = rotor_raw((24, 20, 16), periodic, "periodic", (0.9, 1.25, 0.2),
+                    precision=v.pop("precision", "double"), operator=v.pop("operator", "cumulant"))
+    if "spreading" in v:
+        raw["run"]["spreading"] = v.pop("spreading")
+    if "walls" in v:
+        raw["run"]["walls"] = v.pop("walls")
+    a = _run_raw(monkeypatch, "flags", raw, 16, upload_first)
+    b = _run_raw(monkeypatch, "events", raw, 16, upload_first)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
