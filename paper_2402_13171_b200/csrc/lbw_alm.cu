@@ -25,6 +25,7 @@
 //                          set (last read by this step's K4) for the next step.
 #include <algorithm>
 #include <climits>
+#include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -123,6 +124,11 @@ struct AlmState {
     // [4] K4 count, [5] a bounded wait expired; pool tiles per geometry slot
     uint32_t* cb_flags = nullptr;
     int32_t* cb_pool_tiles = nullptr;   // (kSlots)
+    bool loop_loaded = false;           // sweep kernels loaded (lazy module loading)
+    int64_t cb_loop_end = -1;           // K4 cluster loop queued up to (excluding) this step
+    cudaStream_t loop_stream = nullptr; // its stream, on the chain's SMs
+    cudaEvent_t loop_ev = nullptr;      // stream handover per-step chain <-> loop
+    bool loop_last = false;             // the last chain launch was the loop
     int32_t* cb_box_h = nullptr;        // (kSlots, 2) pinned, device-mapped: [x_first, x_len] hint per KK
     int32_t* cb_cf_n = nullptr;         // (kSlots, P, 8) corner-force term counts
     int16_t* cb_cf_p = nullptr;         // (kSlots, P, 8, kCornerTerms)
@@ -389,8 +395,8 @@ __device__ __forceinline__ void cb_geometry_body(const AlmDev& a, const Geom& g,
     if (cl.prev_cell) {
         if (tid == 0) {
             int32_t* err = reinterpret_cast<int32_t*>(flags + 5);
-            if (cl.ckin_value) gate_wait(flags, cl.ckin_value, err);
-            if (cl.k4_value) gate_wait(flags + 1, cl.k4_value, err);
+            if (cl.ckin_value) gate_wait(flags, cl.ckin_value, err, 33);
+            if (cl.k4_value) gate_wait(flags + 1, cl.k4_value, err, 34);
         }
         __syncthreads();
         cb_corner_lists(a, g, per_x, cl, tid, nthr);
@@ -433,7 +439,7 @@ __device__ __forceinline__ void cb_geometry_body(const AlmDev& a, const Geom& g,
     __syncthreads();
     if (tid == 0) {
         *pool_tiles = cnt * tiles_x;
-        gate_wait(flags + 6, value - 1u, reinterpret_cast<int32_t*>(flags + 5));
+        gate_wait(flags + 6, value - 1u, reinterpret_cast<int32_t*>(flags + 5), 35);
         __threadfence();
         asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags + 6), "r"(value) : "memory");
         if (box_hint) {   // a hint in mapped host memory: after the release, no fence
@@ -509,11 +515,12 @@ struct CbChainArgs {
 //   kin(jk):   kin(jk-1) done; the slot of step jk free (box >= jk-4: sweep
 //              jk-5 started, so sweep jk-6 -- the slot's last reader -- is done)
 //   geo(jk):   kin(jk) done; slot free as above
+template <int ROLE>
 __global__ void __launch_bounds__(128) k_cb_chain(CbChainArgs A) {
     extern __shared__ double csm[];
     const int tid = (int)threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int32_t* err = reinterpret_cast<int32_t*>(A.flags + 5);
-    if (A.role == 1) {
+    if (ROLE == 1) {
         if (tid == 0) {
             gate_wait(A.flags, A.kin_value - 1u, err);
             gate_wait(A.box_flag, A.slot_value, err);
@@ -525,7 +532,7 @@ __global__ void __launch_bounds__(128) k_cb_chain(CbChainArgs A) {
         LBW_TRACE_END(5, A.akk.step);
         return;
     }
-    if (A.role == 2) {
+    if (ROLE == 2) {
         if (tid == 0) {
             gate_wait(A.flags, A.kin_value, err);
             gate_wait(A.box_flag, A.slot_value, err);
@@ -593,6 +600,185 @@ __global__ void __launch_bounds__(128) k_cb_chain(CbChainArgs A) {
     LBW_TRACE_END(2, A.a.step);
 }
 
+// The whole flag-ordered chain of steps j0 .. j0+nsteps-1 in ONE resident
+// launch (a persistent kernel; 4 CTAs, clusters of 2):
+//   CTAs 0-1 (cluster 0): K4(j), one warp per point, half the points each.
+//     Each step's point forces stay in shared memory -- a CTA writes its
+//     half into its own and, through distributed shared memory, its
+//     partner's copy -- so the next step's sampling completes its sums
+//     without a global round trip; steps hand over with a cluster barrier.
+//   CTA 2: kinematics of steps j0+4 .. (serial, the turbine state advances)
+//   CTA 3: geometry of steps j0+3 .. and the corner lists of the step after
+// All ordering is by the chain flags, as with the per-step launches.  One
+// kernel instead of three launches per step: streams of one green context
+// do not overlap each other's kernels, and a launch chained by PDL only
+// overlaps its direct predecessor, so a long-lived K4 loop beside per-step
+// kinematics / geometry launches cannot make progress.
+constexpr int kLoopMaxPoints = 18;
+constexpr int kLoopThreads = 32 * ((kLoopMaxPoints + 1) / 2);   // 288
+constexpr int kLoopGeoCtas = 3;                                 // geometry CTAs (grid 3 + this, even)
+struct CbPersistArgs {
+    Geom g;
+    AlmDev a0;                 // constants; per-step pointers from the bases below
+    KinDev k0;
+    double *kin_base, *samples_base, *blade_base, *flat_base, *loads_base;
+    int64_t loads_cap;
+    FsPool pool0;              // constants (inflow, u_in, error flags, raw)
+    uint64_t* skey_base;
+    const double* spool_base;
+    size_t spool_stride;
+    uint64_t* frow_base;
+    int32_t* dep_cell_base;
+    double* dep_w_base;
+    int32_t* cf_n_base;
+    int16_t* cf_p_base;
+    double* cf_w_base;
+    int32_t* pool_tiles;
+    int32_t* box_hint;         // (kSlots, 2) mapped host memory
+    uint32_t* flags;
+    int64_t rows, j0;
+    int32_t nsteps, per_x, ty, tiles_x, inflow, first_skip_static;
+    double u_in[3];
+};
+
+__device__ __forceinline__ AlmDev cb_step_view(const CbPersistArgs& P, int64_t j) {
+    AlmDev a = P.a0;
+    const int n = a.n;
+    a.kin = P.kin_base + (size_t)(j % kSlots) * n * kKin;
+    a.samples = P.samples_base + (size_t)(j & 1) * n * 4;
+    a.blade = P.blade_base + (size_t)(j & 1) * n * 3;
+    a.flat = P.flat_base + (size_t)(j & 1) * n * 3;
+    a.loads_row = P.loads_base ? P.loads_base + (size_t)(j % P.loads_cap) * n * 3 : nullptr;
+    a.step = j;
+    return a;
+}
+
+__device__ __forceinline__ FsGeom cb_step_geo(const CbPersistArgs& P, int64_t j) {
+    const size_t dep = (size_t)P.a0.n * 3 * P.a0.kw;
+    FsGeom geo;
+    geo.dep_cell = P.dep_cell_base + (size_t)(j % kSlots) * dep;
+    geo.dep_w = P.dep_w_base + (size_t)(j % kSlots) * dep;
+    geo.frow_key = P.frow_base + (size_t)(j % kSlots) * P.rows;
+    geo.skey = P.skey_base + (size_t)(j % kSlots) * P.rows;
+    geo.tag = (uint32_t)(j + 1);
+    geo.inflow = P.inflow;
+    return geo;
+}
+
+__global__ void __launch_bounds__(kLoopThreads, 1) k_cb_persist(CbPersistArgs P) {
+    namespace cg = cooperative_groups;
+    extern __shared__ double csm[];
+    __shared__ double sfl[2][3 * kLoopMaxPoints];   // K4: every point's force, by step parity
+    const int tid = (int)threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int n = P.a0.n, kw = P.a0.kw;
+    int32_t* err = reinterpret_cast<int32_t*>(P.flags + 5);
+    if (blockIdx.x == 2) {   // ---------------------------------- kinematics
+        for (int st = 0; st < P.nsteps; ++st) {
+            const int64_t jk = P.j0 + 4 + st;
+            if (tid == 0) gate_wait(P.flags + 2, (uint32_t)(jk - 4), err, 2100 + (int32_t)(jk % 100));   // slot of jk-6 free
+            __syncthreads();
+            KinDev k = P.k0;
+            k.hist_slot = (int32_t)(jk % kSlots);
+            k.skip_static = (st > 0 || P.first_skip_static) ? 1 : 0;
+            const AlmDev a = cb_step_view(P, jk);
+            LBW_TRACE_BEGIN(1, jk);
+            cb_kin_body(k, a, P.g, P.per_x, 1, 1, P.flags, (uint32_t)(jk + 1), csm);
+            LBW_TRACE_END(5, jk);
+            __syncthreads();
+        }
+        return;
+    }
+    if (blockIdx.x >= 3) {   // ------------------------------------ geometry
+        // kLoopGeoCtas CTAs take the steps round robin (one geometry CTA
+        // would take longer than a step); they publish in step order
+        for (int st = (int)blockIdx.x - 3; st < P.nsteps; st += kLoopGeoCtas) {
+            const int64_t jg = P.j0 + 3 + st;
+            if (tid == 0) {
+                gate_wait(P.flags, (uint32_t)(jg + 1), err, 3100 + (int32_t)(jg % 100));            // kinematics of jg
+                gate_wait(P.flags + 2, (uint32_t)(jg - 4), err, 3200 + (int32_t)(jg % 100));        // its slot free
+            }
+            __syncthreads();
+            const AlmDev a = cb_step_view(P, jg);
+            CornerLists cl{};
+            cl.prev_cell = cb_step_geo(P, jg).dep_cell;
+            cl.prev_w = cb_step_geo(P, jg).dep_w;
+            cl.ckin = P.kin_base + (size_t)((jg + 1) % kSlots) * n * kKin;
+            cl.ckin_value = (uint32_t)(jg + 2);
+            cl.k4_value = (uint32_t)(jg - 4);
+            const size_t off = (size_t)((jg + 1) % kSlots) * n * 8;
+            cl.n = P.cf_n_base + off;
+            cl.p = P.cf_p_base + off * kCornerTerms;
+            cl.w = P.cf_w_base + off * kCornerTerms;
+            cl.inflow = P.inflow;
+            for (int c = 0; c < 3; ++c) cl.u_in[c] = P.u_in[c];
+            cb_geometry_body(a, P.g, P.per_x, cb_step_geo(P, jg), P.ty, P.tiles_x,
+                             P.pool_tiles + jg % kSlots, P.flags, (uint32_t)(jg + 1),
+                             P.box_hint + 2 * (jg % kSlots), cl);
+            LBW_TRACE_END(1, jg);
+            __syncthreads();
+        }
+        return;
+    }
+    // -------------------------------------------------------- K4 (cluster 0)
+    cg::cluster_group cluster = cg::this_cluster();
+    const unsigned rank = cluster.block_rank();
+    const int half = (n + 1) / 2;
+    const int p = (int)rank * half + w;
+    const bool mine = w < half && p < n;
+    double* peer = cluster.map_shared_rank(&sfl[0][0], rank ^ 1u);
+    if (tid == 0) gate_wait(P.flags + 1, (uint32_t)P.j0, err, 41);   // K4(j0-1) done
+    __syncthreads();
+    for (int i = tid; i < 3 * n; i += (int)blockDim.x)
+        sfl[(P.j0 - 1) & 1][i] = P.flat_base[(size_t)((P.j0 - 1) & 1) * n * 3 + i];
+    cluster.sync();
+    const MacroDev md{};
+    for (int st = 0; st < P.nsteps; ++st) {
+        const int64_t j = P.j0 + st;
+        if (tid == 0) {
+            gate_wait(P.flags + 6, (uint32_t)(j + 1), err, 4200 + (int32_t)(j % 100));   // geometry(j)
+            if (*(const volatile int32_t*)(P.pool_tiles + j % kSlots) > 0)
+                gate_wait(P.flags + 2, (uint32_t)j, err, 4300 + (int32_t)(j % 100));       // sums stored by sweep j-1
+        }
+        __syncthreads();
+        if (mine) {
+            const AlmDev a = cb_step_view(P, j);
+            FsPool pool = P.pool0;
+            pool.skey = P.skey_base + (size_t)(j % kSlots) * P.rows;
+            pool.spool = P.spool_base + (size_t)(j & 1) * P.spool_stride;
+            pool.tag = (uint32_t)(j + 1);
+            const FsGeom gp = cb_step_geo(P, j - 1);
+            pool.fv = ForceView{gp.frow_key, nullptr, (uint32_t)j};
+            pool.fv.npts = n;
+            pool.fv.kw = kw;
+            pool.fv.dep_cell = gp.dep_cell;
+            pool.fv.dep_w = gp.dep_w;
+            pool.fv.flat = sfl[(j - 1) & 1];
+            pool.cf_n = P.cf_n_base + (size_t)(j % kSlots) * n * 8;
+            pool.cf_p = P.cf_p_base + (size_t)(j % kSlots) * n * 8 * kCornerTerms;
+            pool.cf_w = P.cf_w_base + (size_t)(j % kSlots) * n * 8 * kCornerTerms;
+            LBW_TRACE_BEGIN(2, j);
+            const PointInputs in = load_point_inputs(a, p, lane);
+            ForceSet none{};
+            CubeArgs cube{};
+            point_warp(a, P.g, md, none, 0, cube, p, lane, in, &pool, false);
+            __syncwarp();
+            if (lane < 3) {
+                const double v = a.flat[p * 3 + lane];   // this warp's own store
+                sfl[j & 1][p * 3 + lane] = v;
+                peer[(j & 1) * 3 * kLoopMaxPoints + p * 3 + lane] = v;
+            }
+            LBW_TRACE_END(2, j);
+        }
+        cluster.sync();   // both halves of step j's forces in both CTAs
+        if (rank == 0 && tid == 0) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.flags + 1),
+                         "r"((uint32_t)(j + 1))
+                         : "memory");
+        }
+    }
+}
+
 // one chain launch; pdl: programmatic stream serialisation (actuator stream)
 static cudaError_t launch_cb_chain(const CbChainArgs& A, unsigned grid, size_t smem,
                                    cudaStream_t st, bool pdl) {
@@ -606,7 +792,11 @@ static cudaError_t launch_cb_chain(const CbChainArgs& A, unsigned grid, size_t s
     attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_cb_chain, A);
+    // one instantiation per role: each gets its own register allocation
+    // (the kinematics / geometry CTAs wait resident on the chain's SMs)
+    if (A.role == 1) return cudaLaunchKernelEx(&cfg, k_cb_chain<1>, A);
+    if (A.role == 2) return cudaLaunchKernelEx(&cfg, k_cb_chain<2>, A);
+    return cudaLaunchKernelEx(&cfg, k_cb_chain<0>, A);
 }
 
 // K5: one warp per deposit pair q.  The lowest pair touching a row owns it:
@@ -717,6 +907,7 @@ cudaError_t alm_sync_side(const lbw_domain* d) {
     if (!d->alm) return cudaSuccess;
     cudaError_t e = cudaSuccess;
     if (d->alm->kin_stream && e == cudaSuccess) e = cudaStreamSynchronize(d->alm->kin_stream);
+    if (d->alm->loop_stream && e == cudaSuccess) e = cudaStreamSynchronize(d->alm->loop_stream);
     return e;
 }
 
@@ -728,6 +919,11 @@ void alm_destroy(lbw_domain* d) {
     AlmState* s = d->alm;
     if (!s) return;
     if (s->kin_stream) cudaStreamSynchronize(s->kin_stream);
+    if (s->loop_stream) {
+        cudaStreamSynchronize(s->loop_stream);
+        cudaStreamDestroy(s->loop_stream);
+        cudaEventDestroy(s->loop_ev);
+    }
     for (void* p : s->allocs) cudaFree(p);
     for (auto& e : s->ring_ev)
         if (e) cudaEventDestroy(e);
@@ -802,6 +998,7 @@ int alm_invalidate(lbw_domain* d) {
     d->alm->ready_step = -1;
     d->alm->fs_next = -1;
     d->alm->cb_next = -1;
+    d->alm->cb_loop_end = -1;
     return LBW_OK;
 }
 
@@ -1217,7 +1414,131 @@ static int cb_kk(lbw_domain* d, int64_t j, cudaStream_t st, bool lists) {
 
 // The chain launch of step j (K4(j) [+ KK(j+4) when kk]) on stream st;
 // use_pool: samples stored by sweep j-1, else recomputed from msrc (priming)
-static int cb_chain(lbw_domain* d, int64_t j, cudaStream_t st, bool use_pool, bool kk) {
+// the K4 cluster loop: only with the chain's own SMs (a resident CTA pair
+// beside the sweep's CTAs could starve for registers) and <= 32 points
+static bool cb_loop_ok(const lbw_domain* d) {
+    return d->chain_loop && d->green_alm && d->alm->n <= kLoopMaxPoints &&
+           d->alm->kin_smem <= 48 * 1024;
+}
+
+static int cb_loop_stream(lbw_domain* d) {
+    AlmState* s = d->alm;
+    if (!s->loop_stream) {
+        s->loop_stream = green_alm_stream(d);
+        if (!s->loop_stream) {
+            set_error("no stream on the actuator chain's SMs");
+            return LBW_ECUDA;
+        }
+        LBW_CK(cudaEventCreateWithFlags(&s->loop_ev, cudaEventDisableTiming));
+    }
+    return LBW_OK;
+}
+
+// Hand the chain over between the per-step launches (actuator stream) and
+// the resident loop (its own stream): the kinematics of either side advance
+// the state the other one continues from.  Waiting for the other stream is
+// safe both ways: all either side waits for is already queued.
+static int cb_stream_handover(lbw_domain* d, bool to_loop) {
+    AlmState* s = d->alm;
+    if (s->loop_last == to_loop) return LBW_OK;
+    cudaStream_t from = to_loop ? d->alm_stream : s->loop_stream;
+    cudaStream_t to = to_loop ? s->loop_stream : d->alm_stream;
+    LBW_CK(cudaEventRecord(s->loop_ev, from));
+    LBW_CK(cudaStreamWaitEvent(to, s->loop_ev, 0));
+    s->loop_last = to_loop;
+    return LBW_OK;
+}
+
+static int cb_persist(lbw_domain* d, int64_t j0, int32_t nsteps) {
+    AlmState* s = d->alm;
+    {
+        int rc = cb_loop_stream(d);
+        if (rc) return rc;
+    }
+    if (!s->loop_loaded) {
+        // the sweeps this kernel waits for are queued after it: load them now
+        LBW_CK(d->desc.mode == LBW_MODE_FAST ? preload_sweep_cb_fast(d->desc.op, d->g.single)
+                                             : preload_sweep_cb_exact(d->desc.op, d->g.single));
+        s->loop_loaded = true;
+    }
+    {
+        int rc = cb_stream_handover(d, true);
+        if (rc) return rc;
+    }
+    // the kinematics of j0+4 .. j0+nsteps+3 advance the state one step each
+    if (s->kin_state_step != j0 + 3 || s->kin_valid[(j0 + 4) % kSlots] == j0 + 4) {
+        set_error("persistent chain: unexpected kinematics state");
+        return LBW_ESTATE;
+    }
+    CbPersistArgs P{};
+    P.g = d->g;
+    P.a0 = s->dev(j0);
+    P.k0 = s->kdev();
+    P.kin_base = s->kin;
+    P.samples_base = s->samples;
+    P.blade_base = s->blade;
+    P.flat_base = s->flat;
+    P.loads_base = (s->loads_cap > 0 && s->d_loads) ? s->d_loads : nullptr;
+    P.loads_cap = s->loads_cap > 0 ? s->loads_cap : 1;
+    P.inflow = d->desc.boundary == LBW_BC_INFLOW_OUTFLOW ? 1 : 0;
+    for (int k = 0; k < 3; ++k) P.u_in[k] = P.pool0.u_in[k] = d->desc.u_in[k];
+    P.pool0.inflow = P.inflow;
+    P.pool0.error_flags = s->error_flags;
+    P.pool0.raw = 1;
+    P.rows = (int64_t)d->g.nxl * d->g.ny;
+    P.skey_base = s->fs_skey;
+    P.spool_base = s->fs_spool;
+    P.spool_stride = (size_t)4 * s->n * 4 * d->g.zp;
+    P.frow_base = s->fs_frow;
+    P.dep_cell_base = s->fs_dep_cell;
+    P.dep_w_base = s->fs_dep_w;
+    P.cf_n_base = s->cb_cf_n;
+    P.cf_p_base = s->cb_cf_p;
+    P.cf_w_base = s->cb_cf_w;
+    P.pool_tiles = s->cb_pool_tiles;
+    P.box_hint = s->cb_box_d;
+    P.flags = s->cb_flags;
+    P.j0 = j0;
+    P.nsteps = nsteps;
+    P.per_x = d->desc.periodic[0] ? 1 : 0;
+    const dim3 blk = sweep_block(d->g);
+    P.ty = (int32_t)blk.y;
+    P.tiles_x = (int32_t)((d->g.nz + blk.x - 1) / blk.x);
+    P.first_skip_static = s->kin_static_ready ? 1 : 0;
+    const size_t smem = s->kin_smem;
+    static bool attr_set = false;
+    if (!attr_set && smem > 48 * 1024) {
+        LBW_CK(cudaFuncSetAttribute(k_cb_persist, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(3 + kLoopGeoCtas, 1, 1);
+    cfg.blockDim = dim3(kLoopThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s->loop_stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    {
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, k_cb_persist, P);
+        LBW_CK(e);
+    }
+    count_launch();
+    s->kin_static_ready = true;
+    for (int64_t jk = j0 + 4; jk < j0 + 4 + nsteps; ++jk) s->kin_valid[jk % kSlots] = jk;
+    s->kin_state_step = j0 + 3 + nsteps;
+    s->cb_loop_end = j0 + nsteps;
+    s->ready_step = -1;
+    return LBW_OK;
+}
+
+static int cb_chain(lbw_domain* d, int64_t j, cudaStream_t st, bool use_pool, bool kk,
+                    bool k4 = true) {
     AlmState* s = d->alm;
     const int64_t rows = (int64_t)d->g.nxl * d->g.ny;
     CbChainArgs A{};
@@ -1254,8 +1575,10 @@ static int cb_chain(lbw_domain* d, int64_t j, cudaStream_t st, bool use_pool, bo
     // by recomputation from buffers the previous sweep wrote
     A.role = 0;
     const size_t k4_smem = (size_t)s->n * (3 * s->kw * 12 + 24);
-    LBW_CK(launch_cb_chain(A, (unsigned)((s->n + 3) / 4), k4_smem, st, use_pool));
-    count_launch();
+    if (k4) {
+        LBW_CK(launch_cb_chain(A, (unsigned)((s->n + 3) / 4), k4_smem, st, use_pool));
+        count_launch();
+    }
     if (kk) {
         // kinematics of step j+4 (serial chain) and geometry of step j+3
         const int64_t jk = j + 4;
@@ -1324,8 +1647,17 @@ int alm_chainb_before(lbw_domain* d, SweepArgs* a) {
         if (rc) return rc;
         // the chains queued from now on (actuator stream) read what these
         // priming kernels wrote: kinematics, geometry, pool-tile counts
+        // (the K4 loop's stream exists from here on: its first launch must
+        // come after this priming too)
+        if (cb_loop_ok(d)) {
+            rc = cb_loop_stream(d);
+            if (rc) return rc;
+        }
         LBW_CK(cudaEventRecord(d->ev_main, d->stream));
         LBW_CK(cudaStreamWaitEvent(d->alm_stream, d->ev_main, 0));
+        if (s->loop_stream) LBW_CK(cudaStreamWaitEvent(s->loop_stream, d->ev_main, 0));
+        s->loop_last = false;
+        s->cb_loop_end = -1;
     }
     const int64_t rows = (int64_t)d->g.nxl * d->g.ny;
     a->fv = fs_view(d, m);
@@ -1355,11 +1687,21 @@ int alm_chainb_before(lbw_domain* d, SweepArgs* a) {
     return LBW_OK;
 }
 
-int alm_chainb_after(lbw_domain* d, int64_t m) {
+int alm_chainb_after(lbw_domain* d, int64_t m, int32_t remaining) {
     AlmState* s = d->alm;
     // the chain of step m+1 (K4(m+1), kinematics(m+5), geometry(m+4)) on
-    // the actuator stream, ordered by flags only
-    int rc = cb_chain(d, m + 1, d->alm_stream, true, true);
+    // the actuator stream, ordered by flags only; K4 of this call's
+    // remaining steps as one resident cluster loop when it fits
+    int rc = LBW_OK;
+    if (cb_loop_ok(d) && remaining >= 4) {
+        // one persistent chain launch covers this call's remaining steps
+        if (s->cb_loop_end <= m + 1 || s->cb_next != m) rc = cb_persist(d, m + 1, remaining);
+    } else if (s->cb_loop_end > m + 1 && s->cb_next == m) {
+        // still inside the last loop's steps (a short call after a long one)
+    } else {
+        rc = cb_stream_handover(d, false);
+        if (!rc) rc = cb_chain(d, m + 1, d->alm_stream, true, true);
+    }
     if (rc) return rc;
     s->cb_next = m + 1;
     return LBW_OK;
@@ -1370,7 +1712,15 @@ int alm_chainb_check(lbw_domain* d) {
     uint32_t err = 0;
     LBW_CK(cudaMemcpy(&err, d->alm->cb_flags + 5, sizeof(err), cudaMemcpyDeviceToHost));
     if (err) {
-        set_error("an in-kernel wait of the flag-ordered actuator chain expired (results invalid)");
+        // the error word holds the first expired wait's site (x100) + step % 100
+        uint32_t f[7] = {};
+        cudaMemcpy(f, d->alm->cb_flags, sizeof f, cudaMemcpyDeviceToHost);
+        char msg[256];
+        snprintf(msg, sizeof msg,
+                 "an in-kernel wait of the flag-ordered actuator chain expired (results invalid; "
+                 "wait site %u, flags kin %u k4 %u box %u geometry %u)",
+                 f[5], f[0], f[1], f[2], f[6]);
+        set_error(msg);
         return LBW_ECUDA;
     }
     return LBW_OK;

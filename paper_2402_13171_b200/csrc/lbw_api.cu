@@ -271,6 +271,10 @@ int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out) {
         const char* cb = getenv("LBW_CHAIN_FLAGS");  // 0: event-ordered chain (A/B)
         d->chainb = !(cb && cb[0] == '0');
         d->chainb_forced = cb && cb[0] == '1';
+        // LBW_CHAIN_LOOP=1: one resident chain kernel per multi-step call
+        // (lbw_alm.cu k_cb_persist); off by default, see DESIGN.md section 10
+        const char* lp = getenv("LBW_CHAIN_LOOP");
+        d->chain_loop = lp && lp[0] == '1';
     }
     d->device = s.device;
     if (cudaSetDevice(d->device) != cudaSuccess) {
@@ -765,7 +769,7 @@ int lbw_domain_step(lbw_domain* d, int32_t nsteps) {
         // before — exactly the preconditions of this sweep (ev_ready) — so it
         // overlaps this sweep.
         if (cb) {
-            int rc = alm_chainb_after(d, d->step - 1);
+            int rc = alm_chainb_after(d, d->step - 1, nsteps - s);
             if (rc) return rc;
         } else if (alm_active(d) && alm_can_prelaunch(d)) {
             LBW_CK(cudaStreamWaitEvent(d->alm_stream, d->ev_ready, 0));

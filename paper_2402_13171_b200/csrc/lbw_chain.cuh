@@ -270,7 +270,7 @@ LBW_CHAIN_FN void kinematics_cta(const KinDev& k, const AlmDev& a, const Geom& g
         // each.  Components whose world transform never changes (no
         // rotation on their path) keep the state of the first launch.
         __shared__ double I3s[9], zero3s[3];
-        __shared__ double wtmp[8][24];
+        __shared__ double wtmp[32][24];   // one per warp (up to 1024 threads)
         const int lane = tid & 31, warp = tid >> 5, nwarp = nthr >> 5;
         if (tid < 9) I3s[tid] = (tid % 4 == 0) ? 1.0 : 0.0;
         if (tid < 3) zero3s[tid] = 0.0;

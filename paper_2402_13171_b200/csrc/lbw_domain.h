@@ -85,6 +85,7 @@ struct lbw_domain {
     bool fused = false;               // one fused launch per actuator step when eligible (LBW_FUSED=1)
     bool chainb = true;               // flag-ordered actuator chain when eligible (LBW_CHAIN_FLAGS)
     bool chainb_forced = false;       // LBW_CHAIN_FLAGS=1: regardless of the slab size
+    bool chain_loop = false;          // LBW_CHAIN_LOOP=1: resident chain kernel per call
     // x-slab neighbours (lbw_peer.cu): side 0 = lo (x-1), side 1 = hi (x+1)
     bool linked = false;
     int nb_rank[2] = {-1, -1};
@@ -136,7 +137,7 @@ bool alm_after_fused(const lbw_domain* d);
 // and after the sweep (alm_chainb_after) the chain of the next step.
 bool alm_chainb_eligible(const lbw_domain* d);
 int alm_chainb_before(lbw_domain* d, SweepArgs* a);
-int alm_chainb_after(lbw_domain* d, int64_t m);
+int alm_chainb_after(lbw_domain* d, int64_t m, int32_t remaining);
 bool alm_after_chainb(const lbw_domain* d);
 // Wait for queued actuator work and forget any prelaunched step (the
 // caller is about to change state it reads).

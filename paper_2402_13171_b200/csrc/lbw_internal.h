@@ -150,6 +150,7 @@ struct SweepArgs {
 
 // exact flavour (lbw_kernels_exact.cu, -fmad=false)
 cudaError_t launch_sweep_exact(int op, bool pull, const SweepArgs& a, cudaStream_t s);
+cudaError_t preload_sweep_cb_exact(int op, bool single);
 cudaError_t launch_batch_exact(int op, double* f2, const double* F2, double* macro2, int64_t n,
                                Relax r, cudaStream_t s);
 cudaError_t launch_block_collide_exact(int op, double* f, const double* force, double* macro,
@@ -157,6 +158,7 @@ cudaError_t launch_block_collide_exact(int op, double* f, const double* force, d
                                        cudaStream_t s);
 // fast flavour (lbw_kernels_fast.cu)
 cudaError_t launch_sweep_fast(int op, bool pull, const SweepArgs& a, cudaStream_t s);
+cudaError_t preload_sweep_cb_fast(int op, bool single);
 cudaError_t launch_batch_fast(int op, double* f2, const double* F2, double* macro2, int64_t n,
                               Relax r, cudaStream_t s);
 cudaError_t launch_block_collide_fast(int op, double* f, const double* force, double* macro,

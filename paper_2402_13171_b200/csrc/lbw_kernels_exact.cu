@@ -13,6 +13,10 @@ cudaError_t launch_fused_exact(int op, bool pull, const FusedArgs& a, size_t sme
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+cudaError_t preload_sweep_cb_exact(int op, bool single) {
+    return single ? preload_k_sweep_cb<4, float>(op) : preload_k_sweep_cb<4, double>(op);
+}
+
 cudaError_t launch_sweep_exact(int op, bool pull, const SweepArgs& a, cudaStream_t s) {
     const dim3 blk = sweep_block(a.g);
     const dim3 grd((a.g.nz + blk.x - 1) / blk.x, (a.g.ny + blk.y - 1) / blk.y, a.x_end - a.x_begin);

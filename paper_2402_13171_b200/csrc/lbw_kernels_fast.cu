@@ -14,6 +14,16 @@ cudaError_t launch_fused_fast(int op, bool pull, const FusedArgs& a, size_t smem
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+cudaError_t preload_sweep_cb_fast(int op, bool single) {
+    const char* e = getenv("LBW_SWEEP_MINB");
+    const int minb = e ? atoi(e) : 5;
+    if (single)
+        return minb == 6 ? preload_k_sweep_cb<6, float>(op)
+               : minb == 4 ? preload_k_sweep_cb<4, float>(op) : preload_k_sweep_cb<5, float>(op);
+    return minb == 6 ? preload_k_sweep_cb<6, double>(op)
+           : minb == 4 ? preload_k_sweep_cb<4, double>(op) : preload_k_sweep_cb<5, double>(op);
+}
+
 cudaError_t launch_sweep_fast(int op, bool pull, const SweepArgs& a, cudaStream_t s) {
     const dim3 blk = sweep_block(a.g);
     const dim3 grd((a.g.nz + blk.x - 1) / blk.x, (a.g.ny + blk.y - 1) / blk.y, a.x_end - a.x_begin);

@@ -385,7 +385,8 @@ __device__ __forceinline__ void sweep_cell(const SweepArgs& a, int x, int y, int
 // In-kernel wait for the actuator chain of this step (see SweepArgs gate):
 // bounded; an expired wait raises the gate error flag (reported by the host
 // as LBW_ECUDA) and lets the CTA finish rather than trapping the context.
-__device__ __forceinline__ void gate_wait(const uint32_t* flag, uint32_t value, int32_t* err) {
+__device__ __forceinline__ void gate_wait(const uint32_t* flag, uint32_t value, int32_t* err,
+                                          int32_t site = 1) {
     long long n = 0;
     while (true) {
         uint32_t v;
@@ -393,7 +394,7 @@ __device__ __forceinline__ void gate_wait(const uint32_t* flag, uint32_t value, 
         if (v >= value) break;
         __nanosleep(32);
         if (++n > 40000000LL) {
-            if (err) atomicExch(err, 1);
+            if (err) atomicCAS(err, 0, site);   // the first expired wait's site
             break;
         }
     }
@@ -426,7 +427,7 @@ __device__ __forceinline__ void sweep_cell_chain(const SweepArgs& a, int x, int 
         else load_cell<PULL>(src, g, x, y, z, f);
     }
     if (__syncthreads_or(kin < a.kin_value)) {
-        if (tid == 0) gate_wait(a.kin_flag, a.kin_value, a.gate_error);
+        if (tid == 0) gate_wait(a.kin_flag, a.kin_value, a.gate_error, 11);
         __syncthreads();
         if (valid) {
             key = *(const volatile uint64_t*)(a.fv.row_key + row);
@@ -475,7 +476,7 @@ __device__ __forceinline__ void sweep_cell_chain(const SweepArgs& a, int x, int 
     const bool need = valid && (uint32_t)(key >> 32) == a.fv.tag;
     if (__syncthreads_or(need)) {
         LBW_TRACE_BEGIN(6, a.step);
-        if (tid == 0) gate_wait(a.k4_flag, a.k4_value, a.gate_error);
+        if (tid == 0) gate_wait(a.k4_flag, a.k4_value, a.gate_error, 12);
         __syncthreads();
         LBW_TRACE_END(6, a.step);
     }
@@ -632,6 +633,21 @@ void launch_k_sweep(int op, bool pull, dim3 grd, dim3 blk, const SweepArgs& b, c
         if (pull) launch_k_sweep_pdl<0, true, MINB, T>(grd, blk, b, s);
         else launch_k_sweep_pdl<0, false, MINB, T>(grd, blk, b, s);
     }
+}
+
+// load the chain-B sweep kernels of an operator now: with lazy module loading
+// the first launch of a kernel waits for the kernels already running, and a
+// resident chain kernel spinning on a flag that only this sweep will set
+// would never finish
+template <int MINB, class T>
+cudaError_t preload_k_sweep_cb(int op) {
+    cudaFuncAttributes fa;
+    cudaError_t e = op == 1 ? cudaFuncGetAttributes(&fa, k_sweep_cb<1, true, MINB, T>)
+                            : cudaFuncGetAttributes(&fa, k_sweep_cb<0, true, MINB, T>);
+    if (e == cudaSuccess)
+        e = op == 1 ? cudaFuncGetAttributes(&fa, k_sweep_cb<1, false, MINB, T>)
+                    : cudaFuncGetAttributes(&fa, k_sweep_cb<0, false, MINB, T>);
+    return e;
 }
 
 }  // namespace LBW_FLAVOR

@@ -124,3 +124,39 @@ def test_flags_variants_bitwise_vs_events(gpu, monkeypatch, variant):
     b = _run_raw(monkeypatch, "events", raw, 16, upload_first)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+def _calls(monkeypatch, loop, case, arithmetic):
+    from paper_2402_13171_b200 import Simulation
+    from tests.scenarios import rotor_config
+    monkeypatch.setenv("LBW_FUSED", "0")
+    monkeypatch.setenv("LBW_CHAIN_FLAGS", "1")
+    monkeypatch.setenv("LBW_CHAIN_LOOP", "1" if loop else "0")
+    cells, per, bc, pos = CASES[case]
+    cfg, tmp = rotor_config(cells=cells, periodic=per, boundary=bc, position=pos,
+                            arithmetic=arithmetic)
+    sim = Simulation(cfg)
+    out = []
+    # long calls (one resident chain kernel each), short calls (per-step
+    # launches) and a state change between them
+    for n in (7, 1, 2, 10, 1, 4, 3, 12):
+        sim.advance(n)
+        out.append(sim._alm_results()[2].copy())
+        if n == 2:
+            sim.fields[0].interior = sim.fields[0].interior
+    out.append(sim.fields[0].interior.copy())
+    sim.close()
+    tmp.cleanup()
+    return out
+
+
+@pytest.mark.parametrize("case", ["periodic", "inflow"])
+def test_resident_loop_bitwise_vs_per_step(gpu, monkeypatch, case):
+    """LBW_CHAIN_LOOP=1 (one resident chain kernel for the K4 / kinematics /
+    geometry of a call's steps, lbw_alm.cu k_cb_persist): bit for bit the
+    per-step chain launches, across calls of every length and a state
+    change."""
+    a = _calls(monkeypatch, True, case, "exact")
+    b = _calls(monkeypatch, False, case, "exact")
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
