@@ -120,8 +120,8 @@ struct AlmState {
     int64_t fs_next = -1;             // step the pipeline is primed for
     unsigned long long* fs_prof = nullptr;   // (256, 8) timeline ring (LBW_FUSED_PROF)
     // chain B (flag-ordered, alm_chainb_*): flags [0] KK done (j+1), [1] K4
-    // done (j+1), [2] samples of step j stored (j), [3] pool-tile count,
-    // [4] K4 count, [5] a bounded wait expired; pool tiles per geometry slot
+    // done (j+1), [2] samples of step j stored (j), [3] sample-warp count,
+    // [4] K4 count, [5] a bounded wait expired; sample warps per geometry slot
     uint32_t* cb_flags = nullptr;
     int32_t* cb_pool_tiles = nullptr;   // (kSlots)
     bool loop_loaded = false;           // sweep kernels loaded (lazy module loading)
@@ -377,7 +377,7 @@ __device__ __forceinline__ void cb_corner_lists(const AlmDev& a, const Geom& g, 
 }
 
 __device__ __forceinline__ void cb_geometry_body(const AlmDev& a, const Geom& g, int per_x,
-                                                 const FsGeom& geo, int ty, int tiles_x,
+                                                 const FsGeom& geo, int warps_row,
                                                  int32_t* pool_tiles, uint32_t* flags,
                                                  uint32_t value, int32_t* box_hint,
                                                  const CornerLists& cl) {
@@ -413,7 +413,7 @@ __device__ __forceinline__ void cb_geometry_body(const AlmDev& a, const Geom& g,
         double v[4];
         pairs[q] = corner_map(g, per_x, geo.inflow, zero3, j0x + (c >> 1), j0y + (c & 1), 0, x, y,
                               z, v) == MA_OWNED
-                       ? ((uint32_t)x << 16) | (uint32_t)(y / ty)
+                       ? ((uint32_t)x << 16) | (uint32_t)y
                        : 0xffffffffu;
         dup[q] = 0u;
         if (c == 0) {
@@ -424,7 +424,7 @@ __device__ __forceinline__ void cb_geometry_body(const AlmDev& a, const Geom& g,
         }
     }
     __syncthreads();
-    // distinct tiles: every pair (r < q) compared once, spread over the CTA
+    // distinct rows: every pair (r < q) compared once, spread over the CTA
     const int npair = nq * (nq - 1) / 2;
     for (int t = tid; t < npair; t += nthr) {
         int q = (int)((1.0 + sqrt(1.0 + 8.0 * (double)t)) * 0.5);
@@ -438,7 +438,7 @@ __device__ __forceinline__ void cb_geometry_body(const AlmDev& a, const Geom& g,
         if (pairs[q] != 0xffffffffu && !dup[q]) atomicAdd(&cnt, 1);
     __syncthreads();
     if (tid == 0) {
-        *pool_tiles = cnt * tiles_x;
+        *pool_tiles = cnt * warps_row;   // sweep warps that store samples
         gate_wait(flags + 6, value - 1u, reinterpret_cast<int32_t*>(flags + 5), 35);
         __threadfence();
         asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags + 6), "r"(value) : "memory");
@@ -467,13 +467,13 @@ __device__ __forceinline__ void cb_kin_body(const KinDev& k, const AlmDev& a, co
 
 // priming: kinematics + geometry of step j in one CTA, serially
 __global__ void k_cb_kk(KinDev k, AlmDev a, Geom g, int per_x, int advance, int do_kin,
-                        FsGeom geo, int ty, int tiles_x, int32_t* pool_tiles, uint32_t* flags,
+                        FsGeom geo, int warps_row, int32_t* pool_tiles, uint32_t* flags,
                         uint32_t value, int32_t* box_hint, CornerLists cl) {
     extern __shared__ double csm[];
     LBW_TRACE_BEGIN(1, a.step);
     cb_kin_body(k, a, g, per_x, advance, do_kin, flags, value, csm);
     __syncthreads();
-    cb_geometry_body(a, g, per_x, geo, ty, tiles_x, pool_tiles, flags, value, box_hint, cl);
+    cb_geometry_body(a, g, per_x, geo, warps_row, pool_tiles, flags, value, box_hint, cl);
     LBW_TRACE_END(1, a.step);
 }
 
@@ -495,7 +495,7 @@ struct CbChainArgs {
     KinDev k;
     AlmDev akk;
     FsGeom geo;
-    int32_t per_x, ty, tiles_x;
+    int32_t per_x, warps_row;
     int32_t* pool_tiles_kk;
     uint32_t kin_value;         // jk + 1
     uint32_t slot_value;        // the slot of step jk is free once box >= slot_value
@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(128) k_cb_chain(CbChainArgs A) {
         }
         __syncthreads();
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-        cb_geometry_body(A.akk, A.g, A.per_x, A.geo, A.ty, A.tiles_x, A.pool_tiles_kk, A.flags,
+        cb_geometry_body(A.akk, A.g, A.per_x, A.geo, A.warps_row, A.pool_tiles_kk, A.flags,
                          A.kin_value, A.box_hint, A.cl);
         LBW_TRACE_END(1, A.akk.step);
         return;
@@ -637,7 +637,7 @@ struct CbPersistArgs {
     int32_t* box_hint;         // (kSlots, 2) mapped host memory
     uint32_t* flags;
     int64_t rows, j0;
-    int32_t nsteps, per_x, ty, tiles_x, inflow, first_skip_static;
+    int32_t nsteps, per_x, warps_row, inflow, first_skip_static;
     double u_in[3];
 };
 
@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(kLoopThreads, 1) k_cb_persist(CbPersistArgs P)
             cl.w = P.cf_w_base + off * kCornerTerms;
             cl.inflow = P.inflow;
             for (int c = 0; c < 3; ++c) cl.u_in[c] = P.u_in[c];
-            cb_geometry_body(a, P.g, P.per_x, cb_step_geo(P, jg), P.ty, P.tiles_x,
+            cb_geometry_body(a, P.g, P.per_x, cb_step_geo(P, jg), P.warps_row,
                              P.pool_tiles + jg % kSlots, P.flags, (uint32_t)(jg + 1),
                              P.box_hint + 2 * (jg % kSlots), cl);
             LBW_TRACE_END(1, jg);
@@ -1396,11 +1396,10 @@ static int cb_kk(lbw_domain* d, int64_t j, cudaStream_t st, bool lists) {
     KinDev kd = s->kdev();
     kd.hist_slot = (int32_t)(j % kSlots);
     kd.skip_static = s->kin_static_ready ? 1 : 0;
-    const dim3 blk = sweep_block(d->g);
-    const int tiles_x = (int)((d->g.nz + blk.x - 1) / blk.x);
+    const int warps_row = (int)((d->g.nz + 31) / 32);
     k_cb_kk<<<1, 128, do_kin ? s->kin_smem : 0, st>>>(
         kd, s->dev(j), d->g, d->desc.periodic[0] ? 1 : 0, advance, do_kin, fs_geom(d, j),
-        (int)blk.y, tiles_x, s->cb_pool_tiles + j % kSlots, s->cb_flags, (uint32_t)(j + 1),
+        warps_row, s->cb_pool_tiles + j % kSlots, s->cb_flags, (uint32_t)(j + 1),
         s->cb_box_d + 2 * (j % kSlots), cb_lists(d, j, lists));
     count_launch();
     LBW_CK(cudaGetLastError());
@@ -1501,9 +1500,7 @@ static int cb_persist(lbw_domain* d, int64_t j0, int32_t nsteps) {
     P.j0 = j0;
     P.nsteps = nsteps;
     P.per_x = d->desc.periodic[0] ? 1 : 0;
-    const dim3 blk = sweep_block(d->g);
-    P.ty = (int32_t)blk.y;
-    P.tiles_x = (int32_t)((d->g.nz + blk.x - 1) / blk.x);
+    P.warps_row = (int32_t)((d->g.nz + 31) / 32);
     P.first_skip_static = s->kin_static_ready ? 1 : 0;
     const size_t smem = s->kin_smem;
     static bool attr_set = false;
@@ -1568,9 +1565,7 @@ static int cb_chain(lbw_domain* d, int64_t j, cudaStream_t st, bool use_pool, bo
     A.flags = s->cb_flags;
     A.k4_value = (uint32_t)(j + 1);
     A.per_x = d->desc.periodic[0] ? 1 : 0;
-    const dim3 blk = sweep_block(d->g);
-    A.ty = (int32_t)blk.y;
-    A.tiles_x = (int32_t)((d->g.nz + blk.x - 1) / blk.x);
+    A.warps_row = (int32_t)((d->g.nz + 31) / 32);
     // K4(j); priming (on the main stream) is an ordinary launch: it samples
     // by recomputation from buffers the previous sweep wrote
     A.role = 0;

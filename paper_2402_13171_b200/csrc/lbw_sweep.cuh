@@ -406,33 +406,35 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
     return v;
 }
 
-// Chain-B cell update (SweepArgs kin_flag != nullptr): CTA-uniform control
-// flow (valid = the thread has a cell); see SweepArgs for the flags.
+// Chain-B cell update (SweepArgs kin_flag != nullptr): warp-uniform control
+// flow (valid = the lane has a cell).  Every flag is waited for and every
+// count is kept per warp -- a warp is 32 z-cells of one row, so a row's
+// keys are warp-uniform -- with no CTA barrier: lane 0 acquires and
+// __syncwarp orders the other lanes behind it.
 template <int OP, bool PULL, class T>
 __device__ __forceinline__ void sweep_cell_chain(const SweepArgs& a, int x, int y, int z, bool valid,
                                                  int tid) {
     const Geom& g = a.g;
     const T* src = static_cast<const T*>(a.src);
     const int64_t row = (int64_t)x * g.ny + y;
-    // the flag (thread 0) and both row keys are loaded with the populations
-    // (one round trip); keys read before the geometry of step m+1 was
-    // published are re-read after the wait
-    const uint32_t kin = tid == 0 ? ld_acquire_u32(a.kin_flag) : a.kin_value;
-    uint64_t key = 0ull, skey = 0ull;
+    const int lane = tid & 31;
+    // The populations are loaded first: an acquire load orders every later
+    // load of its thread behind it.  Then the geometry flag (lane 0) and the
+    // row keys, which come from L2 while the populations are in flight.
     double f[27];
     if (valid) {
-        key = __ldcg(reinterpret_cast<const unsigned long long*>(a.fv.row_key) + row);
-        skey = __ldcg(reinterpret_cast<const unsigned long long*>(a.skey) + row);
         if (PULL && pull_is_simple(g, x, y, z)) load_cell_simple(src, g, x, y, z, f);
         else load_cell<PULL>(src, g, x, y, z, f);
     }
-    if (__syncthreads_or(kin < a.kin_value)) {
-        if (tid == 0) gate_wait(a.kin_flag, a.kin_value, a.gate_error, 11);
-        __syncthreads();
-        if (valid) {
-            key = *(const volatile uint64_t*)(a.fv.row_key + row);
-            skey = *(const volatile uint64_t*)(a.skey + row);
-        }
+    // one acquire per CTA: a gpu-scope acquire also invalidates the SM's L1
+    // (which holds the neighbouring cells' population sectors)
+    if (tid == 0 && ld_acquire_u32(a.kin_flag) < a.kin_value)
+        gate_wait(a.kin_flag, a.kin_value, a.gate_error, 11);
+    __syncthreads();
+    uint64_t key = 0ull, skey = 0ull;
+    if (valid) {
+        key = __ldcg(reinterpret_cast<const unsigned long long*>(a.fv.row_key) + row);
+        skey = __ldcg(reinterpret_cast<const unsigned long long*>(a.skey) + row);
     }
     // rows of step m+1's sampling cubes: store the force-free half of this
     // collide's macro (rho, sum f c) now -- the sampling of step m+1
@@ -454,30 +456,31 @@ __device__ __forceinline__ void sweep_cell_chain(const SweepArgs& a, int x, int 
         asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.box_flag), "r"(a.box_value)
                      : "memory");
     }
-    const bool any_store = __syncthreads_or(store);
-    if (any_store) {
+    if (__any_sync(0xffffffffu, store)) {
         LBW_TRACE_BEGIN(7, a.step);
         LBW_TRACE_END(7, a.step);
-    }
-    if (any_store && tid == 0) {
-        // the last pool tile publishes "the samples of step m+1 are stored"
-        const uint32_t target = (uint32_t)*(const volatile int32_t*)a.pool_tiles;
-        __threadfence();
-        const uint32_t done = atomicAdd(a.pool_cnt, 1u) + 1u;
-        if (done == target) {
-            *a.pool_cnt = 0u;   // for the next sweep (it starts after this one completes)
+        __syncwarp();
+        if (lane == 0) {
+            // the last sample warp publishes "the samples of step m+1 are stored"
+            const uint32_t target = (uint32_t)*(const volatile int32_t*)a.pool_tiles;
             __threadfence();
-            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.box_flag), "r"(a.box_value)
-                         : "memory");
-            LBW_TRACE_END(5, a.step);
+            const uint32_t done = atomicAdd(a.pool_cnt, 1u) + 1u;
+            if (done == target) {
+                *a.pool_cnt = 0u;   // for the next sweep (it starts after this one completes)
+                __threadfence();
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.box_flag),
+                             "r"(a.box_value)
+                             : "memory");
+                LBW_TRACE_END_HERE(5, a.step);
+            }
         }
     }
-    // a tile with force rows of step m waits for the point forces of step m
+    // a warp with force rows of step m waits for the point forces of step m
     const bool need = valid && (uint32_t)(key >> 32) == a.fv.tag;
-    if (__syncthreads_or(need)) {
+    if (__any_sync(0xffffffffu, need)) {
         LBW_TRACE_BEGIN(6, a.step);
-        if (tid == 0) gate_wait(a.k4_flag, a.k4_value, a.gate_error, 12);
-        __syncthreads();
+        if (lane == 0) gate_wait(a.k4_flag, a.k4_value, a.gate_error, 12);
+        __syncwarp();
         LBW_TRACE_END(6, a.step);
     }
     if (valid) {

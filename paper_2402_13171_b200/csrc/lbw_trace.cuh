@@ -20,6 +20,9 @@ __device__ __forceinline__ unsigned long long lbw_gtime() {
         if (threadIdx.x == 0 && threadIdx.y == 0)                                   \
             atomicMax(&lbw_trace_tab[id][(step) & 63][1], lbw_gtime());             \
     } while (0)
+// recorded by the calling thread (the caller picks one)
+#define LBW_TRACE_END_HERE(id, step) \
+    atomicMax(&lbw_trace_tab[id][(step) & 63][1], lbw_gtime())
 #define LBW_TRACE_EXPORT(tu)                                                        \
     extern "C" int lbw_trace_dump_##tu(unsigned long long* out) {                  \
         cudaDeviceSynchronize();                                                    \
@@ -38,6 +41,9 @@ __device__ __forceinline__ unsigned long long lbw_gtime() {
     } while (0)
 #define LBW_TRACE_END(id, step) \
     do {                        \
+    } while (0)
+#define LBW_TRACE_END_HERE(id, step) \
+    do {                             \
     } while (0)
 #define LBW_TRACE_EXPORT(tu)
 #endif

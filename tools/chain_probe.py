@@ -11,6 +11,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 arith = sys.argv[2] if len(sys.argv) > 2 else "fast"
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 300
 alone = len(sys.argv) > 4 and sys.argv[4] == "alone"   # synchronize after every step
+bare = len(sys.argv) > 4 and sys.argv[4] == "bare"     # no turbine
 tmp = tempfile.mkdtemp()
 write_rotor_files(tmp)
 raw = {"domain": {"cells": [n, n, n]},
@@ -19,6 +20,8 @@ raw = {"domain": {"cells": [n, n, n]},
        "run": {"arithmetic": arith, "collision": {"operator": "cumulant"}},
        "turbines": [{"file": "rotor.yaml", "position": [1.0, 1.0, 0.2]}],
        "polars": [{"id": "sym", "file": "sym.csv"}]}
+if bare:
+    del raw["turbines"], raw["polars"]
 sim = Simulation(parse_config(raw, base_dir=tmp))
 if alone:
     for _ in range(steps):
