@@ -1661,8 +1661,8 @@ int alm_chainb_before(lbw_domain* d, SweepArgs* a) {
     a->gate_value = 0;
     a->gate_error = reinterpret_cast<int32_t*>(s->cb_flags + 5);
     a->pdl = 1;
-    a->kin_flag = s->cb_flags + 6;      // geometry of step m+1 done
-    a->kin_value = (uint32_t)(m + 2);
+    a->kin_flag = s->cb_flags + 6;      // geometry of step m+2 done (for sweep m+1)
+    a->kin_value = (uint32_t)(m + 3);
     a->k4_flag = s->cb_flags + 1;
     a->k4_value = (uint32_t)(m + 1);
     a->skey = s->fs_skey + (size_t)((m + 1) % kSlots) * rows;

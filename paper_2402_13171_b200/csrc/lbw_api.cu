@@ -271,10 +271,13 @@ int lbw_domain_create(const lbw_domain_desc* desc, lbw_domain** out) {
         const char* cb = getenv("LBW_CHAIN_FLAGS");  // 0: event-ordered chain (A/B)
         d->chainb = !(cb && cb[0] == '0');
         d->chainb_forced = cb && cb[0] == '1';
-        // LBW_CHAIN_LOOP=1: one resident chain kernel per multi-step call
-        // (lbw_alm.cu k_cb_persist); off by default, see DESIGN.md section 10
+        // one resident chain kernel per multi-step call (lbw_alm.cu
+        // k_cb_persist): by default with the FMA arithmetic, where the
+        // per-step chain launches set the small-slab step time; the exact
+        // flavour's slower sweep hides them.
+        // LBW_CHAIN_LOOP=0/1 forces it off / on.
         const char* lp = getenv("LBW_CHAIN_LOOP");
-        d->chain_loop = lp && lp[0] == '1';
+        d->chain_loop = lp ? lp[0] == '1' : s.mode == LBW_MODE_FAST;
     }
     d->device = s.device;
     if (cudaSetDevice(d->device) != cudaSuccess) {

@@ -126,8 +126,10 @@ struct SweepArgs {
     // reports it as an error instead of the kernel trapping)
     int32_t* gate_error;
     // Flag-ordered actuator chain (lbw_alm.cu, "chain B"; kin_flag != nullptr):
-    // the sweep reads the geometry of steps m / m+1 only once KK(m+1) is done
-    // (*kin_flag >= kin_value), a tile holding force rows waits for the point
+    // the geometry of steps m / m+1 is visible when the sweep starts (its
+    // predecessor sweep completed after acquiring it, see k_sweep_cb); CTA 0
+    // acquires the geometry of step m+2 (*kin_flag >= kin_value) before it
+    // ends, for the next sweep; a warp holding force rows waits for the point
     // forces of step m (*k4_flag >= k4_value), tiles holding rows of step
     // m+1's sampling cubes store their collide's (rho, u) into spool, and the
     // last of those tiles (*pool_tiles of them) publishes *box_flag = box_value.

@@ -407,9 +407,9 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
 }
 
 // Chain-B cell update (SweepArgs kin_flag != nullptr): warp-uniform control
-// flow (valid = the lane has a cell).  Every flag is waited for and every
-// count is kept per warp -- a warp is 32 z-cells of one row, so a row's
-// keys are warp-uniform -- with no CTA barrier: lane 0 acquires and
+// flow (valid = the lane has a cell).  The K4 flag is waited for and the
+// sample stores are counted per warp -- a warp is 32 z-cells of one row, so
+// a row's keys are warp-uniform -- with no CTA barrier: lane 0 acquires and
 // __syncwarp orders the other lanes behind it.
 template <int OP, bool PULL, class T>
 __device__ __forceinline__ void sweep_cell_chain(const SweepArgs& a, int x, int y, int z, bool valid,
@@ -418,23 +418,15 @@ __device__ __forceinline__ void sweep_cell_chain(const SweepArgs& a, int x, int 
     const T* src = static_cast<const T*>(a.src);
     const int64_t row = (int64_t)x * g.ny + y;
     const int lane = tid & 31;
-    // The populations are loaded first: an acquire load orders every later
-    // load of its thread behind it.  Then the geometry flag (lane 0) and the
-    // row keys, which come from L2 while the populations are in flight.
-    double f[27];
-    if (valid) {
-        if (PULL && pull_is_simple(g, x, y, z)) load_cell_simple(src, g, x, y, z, f);
-        else load_cell<PULL>(src, g, x, y, z, f);
-    }
-    // one acquire per CTA: a gpu-scope acquire also invalidates the SM's L1
-    // (which holds the neighbouring cells' population sectors)
-    if (tid == 0 && ld_acquire_u32(a.kin_flag) < a.kin_value)
-        gate_wait(a.kin_flag, a.kin_value, a.gate_error, 11);
-    __syncthreads();
+    // the geometry of steps m (force rows) and m+1 (sampling rows) is
+    // visible from the start (k_sweep_cb): keys and populations load together
     uint64_t key = 0ull, skey = 0ull;
+    double f[27];
     if (valid) {
         key = __ldcg(reinterpret_cast<const unsigned long long*>(a.fv.row_key) + row);
         skey = __ldcg(reinterpret_cast<const unsigned long long*>(a.skey) + row);
+        if (PULL && pull_is_simple(g, x, y, z)) load_cell_simple(src, g, x, y, z, f);
+        else load_cell<PULL>(src, g, x, y, z, f);
     }
     // rows of step m+1's sampling cubes: store the force-free half of this
     // collide's macro (rho, sum f c) now -- the sampling of step m+1
@@ -545,8 +537,17 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) k_sweep_cb(SweepArgs a) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     LBW_TRACE_BEGIN(0, a.step);
-    sweep_cell_chain<OP, PULL, T>(a, x, y, z, z < g.nz && y < g.ny,
-                                  (int)(threadIdx.x + threadIdx.y * blockDim.x));
+    const int tid = (int)(threadIdx.x + threadIdx.y * blockDim.x);
+    sweep_cell_chain<OP, PULL, T>(a, x, y, z, z < g.nz && y < g.ny, tid);
+    // The next sweep reads the geometry of step m+2 without waiting: CTA 0
+    // acquires it here, and that sweep's griddepcontrol.wait (or stream
+    // order) follows this grid's completion.  KK computes it three steps
+    // ahead, so this normally finds the flag set; it depends on sweeps up
+    // to m-2 only.  Acquiring at the start of every CTA instead put an
+    // acquire and a dependent key load (two round trips) before each CTA's
+    // arithmetic (~0.7-1 us per 64^3 step).
+    if (bz == 0 && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0)
+        gate_wait(a.kin_flag, a.kin_value, a.gate_error, 11);
     LBW_TRACE_END(0, a.step);
 }
 

@@ -150,13 +150,14 @@ def _calls(monkeypatch, loop, case, arithmetic):
     return out
 
 
-@pytest.mark.parametrize("case", ["periodic", "inflow"])
-def test_resident_loop_bitwise_vs_per_step(gpu, monkeypatch, case):
-    """LBW_CHAIN_LOOP=1 (one resident chain kernel for the K4 / kinematics /
-    geometry of a call's steps, lbw_alm.cu k_cb_persist): bit for bit the
-    per-step chain launches, across calls of every length and a state
-    change."""
-    a = _calls(monkeypatch, True, case, "exact")
-    b = _calls(monkeypatch, False, case, "exact")
+@pytest.mark.parametrize("case,arithmetic", [("periodic", "exact"), ("inflow", "exact"),
+                                             ("periodic", "fast"), ("inflow", "fast")])
+def test_resident_loop_bitwise_vs_per_step(gpu, monkeypatch, case, arithmetic):
+    """The resident chain kernel (K4 / kinematics / geometry of a call's
+    steps in one launch, lbw_alm.cu k_cb_persist; the default with the FMA
+    arithmetic): bit for bit the per-step chain launches, across calls of
+    every length and a state change."""
+    a = _calls(monkeypatch, True, case, arithmetic)
+    b = _calls(monkeypatch, False, case, arithmetic)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
