@@ -129,6 +129,7 @@ struct AlmState {
     cudaStream_t loop_stream = nullptr; // its stream, on the chain's SMs
     cudaEvent_t loop_ev = nullptr;      // stream handover per-step chain <-> loop
     bool loop_last = false;             // the last chain launch was the loop
+    int loop_fit = -1;                  // resident chain fits the chain's SMs (-1: not checked)
     int32_t* cb_box_h = nullptr;        // (kSlots, 2) pinned, device-mapped: [x_first, x_len] hint per KK
     int32_t* cb_cf_n = nullptr;         // (kSlots, P, 8) corner-force term counts
     int16_t* cb_cf_p = nullptr;         // (kSlots, P, 8, kCornerTerms)
@@ -1413,11 +1414,38 @@ static int cb_kk(lbw_domain* d, int64_t j, cudaStream_t st, bool lists) {
 
 // The chain launch of step j (K4(j) [+ KK(j+4) when kk]) on stream st;
 // use_pool: samples stored by sweep j-1, else recomputed from msrc (priming)
-// the K4 cluster loop: only with the chain's own SMs (a resident CTA pair
-// beside the sweep's CTAs could starve for registers) and <= 32 points
-static bool cb_loop_ok(const lbw_domain* d) {
-    return d->chain_loop && d->green_alm && d->alm->n <= kLoopMaxPoints &&
-           d->alm->kin_smem <= 48 * 1024;
+static int cb_loop_stream(lbw_domain* d);
+
+// the resident chain: only on the chain's own SMs (its CTAs beside the
+// sweep's could starve for registers), <= kLoopMaxPoints points, and only
+// when all its CTAs fit there at once (they wait on each other)
+static bool cb_loop_ok(lbw_domain* d) {
+    AlmState* s = d->alm;
+    if (!(d->chain_loop && d->green_alm && s->n <= kLoopMaxPoints && s->kin_smem <= 48 * 1024))
+        return false;
+    if (s->loop_fit < 0) {
+        s->loop_fit = 0;
+        if (cb_loop_stream(d) == LBW_OK) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(3 + kLoopGeoCtas, 1, 1);
+            cfg.blockDim = dim3(kLoopThreads, 1, 1);
+            cfg.dynamicSmemBytes = s->kin_smem;
+            cfg.stream = s->loop_stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            int clusters = 0;
+            if (cudaOccupancyMaxActiveClusters(&clusters, k_cb_persist, &cfg) == cudaSuccess &&
+                2 * clusters >= 3 + kLoopGeoCtas)
+                s->loop_fit = 1;
+        }
+        cudaGetLastError();
+    }
+    return s->loop_fit == 1;
 }
 
 static int cb_loop_stream(lbw_domain* d) {
