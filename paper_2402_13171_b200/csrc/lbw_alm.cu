@@ -602,19 +602,22 @@ __global__ void __launch_bounds__(128) k_cb_chain(CbChainArgs A) {
 }
 
 // The whole flag-ordered chain of steps j0 .. j0+nsteps-1 in ONE resident
-// launch (a persistent kernel; 4 CTAs, clusters of 2):
+// launch (a persistent kernel on the chain's SMs; 6 CTAs, clusters of 2):
 //   CTAs 0-1 (cluster 0): K4(j), one warp per point, half the points each.
 //     Each step's point forces stay in shared memory -- a CTA writes its
 //     half into its own and, through distributed shared memory, its
 //     partner's copy -- so the next step's sampling completes its sums
 //     without a global round trip; steps hand over with a cluster barrier.
 //   CTA 2: kinematics of steps j0+4 .. (serial, the turbine state advances)
-//   CTA 3: geometry of steps j0+3 .. and the corner lists of the step after
+//   CTAs 3..5: geometry of steps j0+3 .. round robin (one geometry takes
+//     longer than a step) and the corner lists of the step after; they
+//     publish in step order.
 // All ordering is by the chain flags, as with the per-step launches.  One
-// kernel instead of three launches per step: streams of one green context
-// do not overlap each other's kernels, and a launch chained by PDL only
-// overlaps its direct predecessor, so a long-lived K4 loop beside per-step
-// kinematics / geometry launches cannot make progress.
+// kernel instead of three PDL-chained launches per step (a launch chained
+// by PDL only overlaps its direct predecessor, so the per-step chain is a
+// serial sequence of launch latencies).  Unlike those launches it waits for
+// sweeps queued AFTER it: the sweep kernels must be loaded before it runs
+// (lazy module loading), and it needs all its CTAs resident (cb_loop_ok).
 constexpr int kLoopMaxPoints = 18;
 constexpr int kLoopThreads = 32 * ((kLoopMaxPoints + 1) / 2);   // 288
 constexpr int kLoopGeoCtas = 3;                                 // geometry CTAs (grid 3 + this, even)
@@ -1416,6 +1419,22 @@ static int cb_kk(lbw_domain* d, int64_t j, cudaStream_t st, bool lists) {
 // use_pool: samples stored by sweep j-1, else recomputed from msrc (priming)
 static int cb_loop_stream(lbw_domain* d);
 
+// launch configuration of the resident chain (k_cb_persist)
+static void loop_config(const AlmState* s, cudaLaunchConfig_t& cfg, cudaLaunchAttribute& attr) {
+    cfg = {};
+    cfg.gridDim = dim3(3 + kLoopGeoCtas, 1, 1);
+    cfg.blockDim = dim3(kLoopThreads, 1, 1);
+    cfg.dynamicSmemBytes = s->kin_smem;   // <= 48 KB (cb_loop_ok)
+    cfg.stream = s->loop_stream;
+    attr = {};
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 2;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+}
+
 // the resident chain: only on the chain's own SMs (its CTAs beside the
 // sweep's could starve for registers), <= kLoopMaxPoints points, and only
 // when all its CTAs fit there at once (they wait on each other)
@@ -1426,18 +1445,9 @@ static bool cb_loop_ok(lbw_domain* d) {
     if (s->loop_fit < 0) {
         s->loop_fit = 0;
         if (cb_loop_stream(d) == LBW_OK) {
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(3 + kLoopGeoCtas, 1, 1);
-            cfg.blockDim = dim3(kLoopThreads, 1, 1);
-            cfg.dynamicSmemBytes = s->kin_smem;
-            cfg.stream = s->loop_stream;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = 2;
-            attr[0].val.clusterDim.y = 1;
-            attr[0].val.clusterDim.z = 1;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
+            cudaLaunchConfig_t cfg;
+            cudaLaunchAttribute attr;
+            loop_config(s, cfg, attr);
             int clusters = 0;
             if (cudaOccupancyMaxActiveClusters(&clusters, k_cb_persist, &cfg) == cudaSuccess &&
                 2 * clusters >= 3 + kLoopGeoCtas)
@@ -1530,29 +1540,10 @@ static int cb_persist(lbw_domain* d, int64_t j0, int32_t nsteps) {
     P.per_x = d->desc.periodic[0] ? 1 : 0;
     P.warps_row = (int32_t)((d->g.nz + 31) / 32);
     P.first_skip_static = s->kin_static_ready ? 1 : 0;
-    const size_t smem = s->kin_smem;
-    static bool attr_set = false;
-    if (!attr_set && smem > 48 * 1024) {
-        LBW_CK(cudaFuncSetAttribute(k_cb_persist, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-        attr_set = true;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(3 + kLoopGeoCtas, 1, 1);
-    cfg.blockDim = dim3(kLoopThreads, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s->loop_stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    {
-        const cudaError_t e = cudaLaunchKernelEx(&cfg, k_cb_persist, P);
-        LBW_CK(e);
-    }
+    cudaLaunchConfig_t cfg;
+    cudaLaunchAttribute attr;
+    loop_config(s, cfg, attr);
+    LBW_CK(cudaLaunchKernelEx(&cfg, k_cb_persist, P));
     count_launch();
     s->kin_static_ready = true;
     for (int64_t jk = j0 + 4; jk < j0 + 4 + nsteps; ++jk) s->kin_valid[jk % kSlots] = jk;

@@ -116,13 +116,14 @@ def output_case(world, nx):
     holder = [base]
     dist.broadcast_object_list(holder, 0)
     base = holder[0]
+    from tests.scenarios import rotor_raw, write_rotor_files
+    files = os.path.join(base, "files")
+    if rank == 0:   # one writer, the others read after the barrier
+        os.makedirs(files, exist_ok=True)
+        write_rotor_files(files)
+    dist.barrier()
 
     def cfg_for(out):
-        from tests.scenarios import rotor_raw, write_rotor_files
-        files = os.path.join(base, "files")
-        if rank == 0 or not os.path.exists(files):
-            os.makedirs(files, exist_ok=True)
-            write_rotor_files(files)
         raw = rotor_raw((nx, 12, 12), (True, True, True), position=(1.5, 0.3, 0.0), steps=6,
                         arithmetic="fast")
         raw["output"] = {"directory": out, "cadence": 3, "vtk": True,
