@@ -161,3 +161,40 @@ def test_resident_loop_bitwise_vs_per_step(gpu, monkeypatch, case, arithmetic):
     b = _calls(monkeypatch, False, case, arithmetic)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("variant", ["single", "gauss", "walls", "bgk"])
+def test_resident_loop_variants_bitwise(gpu, monkeypatch, variant):
+    """The resident chain (FMA arithmetic) against the per-step launches for
+    fp32 storage, Gaussian spreading, walls and BGK, through advance(n)."""
+    import tempfile
+
+    from paper_2402_13171_b200 import Simulation, parse_config
+    from tests.scenarios import rotor_raw, write_rotor_files
+
+    def run(loop):
+        monkeypatch.setenv("LBW_FUSED", "0")
+        monkeypatch.setenv("LBW_CHAIN_FLAGS", "1")
+        monkeypatch.setenv("LBW_CHAIN_LOOP", "1" if loop else "0")
+        v = dict(VARIANTS[variant])
+        periodic = v.pop("periodic", (True, True, True))
+        raw = rotor_raw((24, 20, 16), periodic, "periodic", (0.9, 1.25, 0.2), arithmetic="fast",
+                        precision=v.pop("precision", "double"),
+                        operator=v.pop("operator", "cumulant"))
+        if "spreading" in v:
+            raw["run"]["spreading"] = v.pop("spreading")
+        if "walls" in v:
+            raw["run"]["walls"] = v.pop("walls")
+        with tempfile.TemporaryDirectory() as tmp:
+            write_rotor_files(tmp)
+            sim = Simulation(parse_config(raw, base_dir=tmp))
+            out = []
+            for n in (6, 2, 5):   # 13 steps: the walls case goes unstable near 17
+                sim.advance(n)
+                out.append(sim._alm_results()[2].copy())
+            out.append(sim.fields[0].interior.copy())
+            sim.close()
+        return out
+
+    for x, y in zip(run(True), run(False)):
+        assert np.array_equal(x, y)
