@@ -199,7 +199,10 @@ int lbw_domain_recompute_moments(lbw_domain* d, double* macro_aos);
 
 /* Advance nsteps time steps (sim.py:264-300 minus host kinematics).
  * For steps with actuator points, lbw_alm_set_kinematics must have queued
- * that step's kinematics. */
+ * that step's kinematics.  Asynchronous: returns once the steps are queued.
+ * On a small single slab with device kinematics a call of >= 4 steps may
+ * queue one resident actuator-chain kernel that waits in-kernel for the
+ * call's later sweeps; all of them are queued before the call returns. */
 int lbw_domain_step(lbw_domain* d, int32_t nsteps);
 int64_t lbw_domain_step_index(lbw_domain* d);
 int lbw_domain_set_step_index(lbw_domain* d, int64_t step);
