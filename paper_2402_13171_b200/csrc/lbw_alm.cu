@@ -1696,8 +1696,9 @@ int alm_chainb_before(lbw_domain* d, SweepArgs* a) {
     // (possibly a few steps old while the host runs ahead of the GPU);
     // every dependency is guarded by the flags, not by the order
     const volatile int32_t* hb = s->cb_box_h + 2 * ((m + 1) % kSlots);
-    a->x_first = hb[0];
-    a->x_len = hb[1] > 0 ? hb[1] : d->g.nxl;
+    const int32_t nx = d->g.nxl, h0 = hb[0], h1 = hb[1];
+    a->x_first = ((h0 % nx) + nx) % nx;
+    a->x_len = h1 > 0 && h1 <= nx ? h1 : nx;
     return LBW_OK;
 }
 

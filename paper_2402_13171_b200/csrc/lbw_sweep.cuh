@@ -531,9 +531,12 @@ __global__ void __launch_bounds__(kSweepThreads, MINB) k_sweep_cb(SweepArgs a) {
     const int y = blockIdx.y * blockDim.y + threadIdx.y;
     const int bz = (int)blockIdx.z;
     const int np = a.x_end - a.x_begin;
-    // rotated plane order: the rotor's planes first (single slab: np == nxl)
-    const int r = a.reverse ? a.x_first + a.x_len - 1 - bz : a.x_first + bz;
-    const int x = a.x_begin + ((r % np) + np) % np;
+    // rotated plane order: the rotor's planes first (single slab: np == nxl;
+    // the host keeps 0 <= x_first < np and 1 <= x_len <= np, so r lies in
+    // (-np, 2 np) and one wrap suffices)
+    int r = a.reverse ? a.x_first + a.x_len - 1 - bz : a.x_first + bz;
+    r += r < 0 ? np : (r >= np ? -np : 0);
+    const int x = a.x_begin + r;
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     LBW_TRACE_BEGIN(0, a.step);
