@@ -129,7 +129,7 @@ def test_05_wake_induction_reduced_resolution(gpu, fixtures_dir):
 
 @pytest.mark.xfail(strict=False, reason=(
     "64^3 sweeps take 16-23 us; the rotor sweep's own force / sample rows and "
-    "the gap between sweeps still add ~10 % (exact) / ~22 % (fast) -- DESIGN.md 10"))
+    "the gap between sweeps still add ~9 % (exact) / ~21 % (fast) -- DESIGN.md 10"))
 def test_07_turbine_overhead_under_ten_percent(gpu, fixtures_dir, tmp_path):
     """test_acceptance.py:558-584: one rotating 3-blade turbine vs none on
     64^3: MLUPS through run_simulation degrades by < 10 %."""
