@@ -1486,17 +1486,27 @@ static int cb_stream_handover(lbw_domain* d, bool to_loop) {
     return LBW_OK;
 }
 
+// the sweeps the resident chain waits for are queued after it: their
+// kernels must be loaded before it runs (lazy module loading)
+static int cb_preload(lbw_domain* d) {
+    AlmState* s = d->alm;
+    if (!s->loop_loaded) {
+        LBW_CK(d->desc.mode == LBW_MODE_FAST ? preload_sweep_cb_fast(d->desc.op, d->g.single)
+                                             : preload_sweep_cb_exact(d->desc.op, d->g.single));
+        s->loop_loaded = true;
+    }
+    return LBW_OK;
+}
+
 static int cb_persist(lbw_domain* d, int64_t j0, int32_t nsteps) {
     AlmState* s = d->alm;
     {
         int rc = cb_loop_stream(d);
         if (rc) return rc;
     }
-    if (!s->loop_loaded) {
-        // the sweeps this kernel waits for are queued after it: load them now
-        LBW_CK(d->desc.mode == LBW_MODE_FAST ? preload_sweep_cb_fast(d->desc.op, d->g.single)
-                                             : preload_sweep_cb_exact(d->desc.op, d->g.single));
-        s->loop_loaded = true;
+    {
+        int rc = cb_preload(d);
+        if (rc) return rc;
     }
     {
         int rc = cb_stream_handover(d, true);
@@ -2194,6 +2204,13 @@ int lbw_alm_configure_kinematics(lbw_domain* d, const lbw_kin_desc* kd) {
     s->ready_step = -1;
     s->fs_next = -1;
     s->cb_next = -1;
+    // the flag-ordered chain's buffers, and the resident chain's stream and
+    // kernels, now rather than inside the first lbw_domain_step
+    if (alm_chainb_eligible(d)) {
+        int rc = cb_allocate(d);
+        if (!rc && cb_loop_ok(d)) rc = cb_preload(d);
+        if (rc) return rc;
+    }
     return LBW_OK;
 }
 

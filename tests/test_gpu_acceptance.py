@@ -128,12 +128,15 @@ def test_05_wake_induction_reduced_resolution(gpu, fixtures_dir):
 
 
 @pytest.mark.xfail(strict=False, reason=(
-    "64^3 sweeps take 16-23 us; the rotor sweep's own force / sample rows and "
-    "the gap between sweeps still add ~9 % (exact) / ~21 % (fast) -- DESIGN.md 10"))
-def test_07_turbine_overhead_under_ten_percent(gpu, fixtures_dir, tmp_path):
+    "64^3 sweeps take 16-23 us; the rotor sweep's own force / sample rows, the "
+    "chain's SM partition and the gap between sweeps still add ~14 % (exact) / "
+    "~26 % (fast) to the step -- DESIGN.md 10"))
+@pytest.mark.parametrize("arithmetic", ["exact", "fast"])
+def test_07_turbine_overhead_under_ten_percent(gpu, fixtures_dir, tmp_path, arithmetic):
     """test_acceptance.py:558-584: one rotating 3-blade turbine vs none on
-    64^3: MLUPS through run_simulation degrades by < 10 %."""
-    def mlups(with_turbine, rep, steps=400, arithmetic="exact"):
+    64^3: MLUPS through run_simulation degrades by < 10 %, in both
+    arithmetic flavours."""
+    def mlups(with_turbine, rep, steps=400):
         raw = {"domain": {"cells": [64, 64, 64]},
                "fluid": {"kinematic_viscosity": 0.1732, "wind": [8.0, 0.0, 0.0]},
                "resolution": {"mach": 0.05},
@@ -145,9 +148,8 @@ def test_07_turbine_overhead_under_ten_percent(gpu, fixtures_dir, tmp_path):
             raw["polars"] = [{"id": "sym", "file": "sym.csv"}]
         return run_simulation(parse_config(raw, base_dir=str(fixtures_dir)))["performance"]["mlups"]
 
-    for arithmetic in ("exact", "fast"):
-        mlups(True, 99, steps=3, arithmetic=arithmetic)
-        base = max(mlups(False, r, arithmetic=arithmetic) for r in range(2))
-        turb = max(mlups(True, r, arithmetic=arithmetic) for r in range(2))
-        degradation = (base - turb) / base
-        assert degradation < 0.10, (arithmetic, f"{degradation:.1%}", base, turb)
+    mlups(True, 99, steps=8)   # untimed: loads the multi-step kernels too
+    base = max(mlups(False, r) for r in range(2))
+    turb = max(mlups(True, r) for r in range(2))
+    degradation = (base - turb) / base
+    assert degradation < 0.10, (arithmetic, f"{degradation:.1%}", base, turb)
