@@ -125,7 +125,7 @@ struct AlmState {
     uint32_t* cb_flags = nullptr;
     int32_t* cb_pool_tiles = nullptr;   // (kSlots)
     bool loop_loaded = false;           // sweep kernels loaded (lazy module loading)
-    int64_t cb_loop_end = -1;           // K4 cluster loop queued up to (excluding) this step
+    int64_t cb_loop_end = -1;           // resident chain queued up to (excluding) this step
     cudaStream_t loop_stream = nullptr; // its stream, on the chain's SMs
     cudaEvent_t loop_ev = nullptr;      // stream handover per-step chain <-> loop
     bool loop_last = false;             // the last chain launch was the loop
@@ -1671,12 +1671,9 @@ int alm_chainb_before(lbw_domain* d, SweepArgs* a) {
         if (rc) return rc;
         // the chains queued from now on (actuator stream) read what these
         // priming kernels wrote: kinematics, geometry, pool-tile counts
-        // (the K4 loop's stream exists from here on: its first launch must
-        // come after this priming too)
-        if (cb_loop_ok(d)) {
-            rc = cb_loop_stream(d);
-            if (rc) return rc;
-        }
+        // (so does the resident chain's stream: cb_loop_ok creates it if
+        // the kinematics configuration did not)
+        (void)cb_loop_ok(d);
         LBW_CK(cudaEventRecord(d->ev_main, d->stream));
         LBW_CK(cudaStreamWaitEvent(d->alm_stream, d->ev_main, 0));
         if (s->loop_stream) LBW_CK(cudaStreamWaitEvent(s->loop_stream, d->ev_main, 0));
@@ -1715,8 +1712,8 @@ int alm_chainb_before(lbw_domain* d, SweepArgs* a) {
 int alm_chainb_after(lbw_domain* d, int64_t m, int32_t remaining) {
     AlmState* s = d->alm;
     // the chain of step m+1 (K4(m+1), kinematics(m+5), geometry(m+4)) on
-    // the actuator stream, ordered by flags only; K4 of this call's
-    // remaining steps as one resident cluster loop when it fits
+    // the actuator stream, ordered by flags only -- or, for a call of >= 4
+    // steps, the whole chain of its remaining steps as one resident kernel
     int rc = LBW_OK;
     if (cb_loop_ok(d) && remaining >= 4) {
         // one persistent chain launch covers this call's remaining steps
